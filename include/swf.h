@@ -1,0 +1,234 @@
+/*
+ * swf.h — C ABI of the B200-native CSPH-TVD time step (libswflood_cuda.so).
+ *
+ * This is the drop-in boundary for the one hot path this repository builds:
+ * swflood::CsphTvdStepper::step (reference: proj/src/stepper.cpp:706-749) and
+ * the surrounding solver API of proj/include/swflood/stepper.hpp:76-169.
+ * The reference has no FFI of its own; the entry points below
+ * are the ones a binding for that C++ class needs, one per public member, with
+ * plain pointers and sizes only.  Citations are relative to /root/reference.
+ *
+ * Status codes mirror the reference's error convention
+ * (proj/include/swflood/errors.hpp:8-21, proj/src/grid.cpp:102-110):
+ *   SWF_OK 0, SWF_ECONFIG 1 (ConfigError), SWF_ENUMERICAL 2 (NumericalError),
+ *   SWF_ERANGE 3 (std::out_of_range), SWF_ECUDA 4 (device/runtime failure).
+ * The message text of the last failure is returned by swf_last_error(ctx)
+ * (ctx may be NULL for failures of swf_create).  On SWF_ENUMERICAL the flow
+ * state is left exactly as it was before the failing step, like the
+ * reference, which throws before FlowState is modified.
+ *
+ * Threading: one host thread per swf_ctx, like the reference's externally
+ * single-stepped stepper.  Every context owns one CUDA stream.
+ */
+#ifndef SWF_H_
+#define SWF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SWF_OK 0
+#define SWF_ECONFIG 1
+#define SWF_ENUMERICAL 2
+#define SWF_ERANGE 3
+#define SWF_ECUDA 4
+
+/* EdgeKind, stepper.hpp:20 */
+#define SWF_EDGE_REFLECTIVE 0
+#define SWF_EDGE_OPEN 1
+
+/* SourceSpec::Kind, sources.hpp:25-26 */
+#define SWF_SOURCE_DISCHARGE 0
+#define SWF_SOURCE_RAIN 1
+
+/* Terrain, grid.hpp:18-37.  b is row-major, k = i + j*nx, j northward. */
+typedef struct swf_terrain {
+  int nx, ny;
+  double h;
+  double x0, y0;
+  const double* b; /* nx*ny host doubles, copied to the device at creation */
+} swf_terrain;
+
+/* PhysicalParams, grid.hpp:59-74 (defaults grid.hpp:60-68). */
+typedef struct swf_params {
+  double g, n_manning, nu, omega_z, c_a, rho_air, rho_water, eps_dry;
+  const double* n_field; /* NULL = scalar n_manning; else nx*ny host doubles */
+} swf_params;
+
+/* TimestepControl, stepper.hpp:13-18 */
+typedef struct swf_control {
+  double courant, dt_max, dt_min;
+} swf_control;
+
+/* StepperOptions + BoundaryConfig, stepper.hpp:22-28,59-64.
+ * `workers` is accepted and ignored on the GPU. */
+typedef struct swf_options {
+  int block_size;
+  int skip_dry_blocks;
+  int workers;
+  int west, east, south, north; /* SWF_EDGE_* */
+} swf_options;
+
+/* SourceSpec, sources.hpp:25-36 (name omitted; rect is inclusive). */
+typedef struct swf_source {
+  int kind; /* SWF_SOURCE_* */
+  int i0, j0, i1, j1;
+  int n_hydro;
+  const double* hydro_t; /* n_hydro strictly increasing times */
+  const double* hydro_q; /* n_hydro discharges [m^3/s] */
+  double rate;           /* rain sigma [m/s] */
+  double vx, vy;         /* source water velocity */
+} swf_source;
+
+/* StepInfo + StageTimings, stepper.hpp:31-57.  timings[] are seconds of
+ * device time per stage bucket (mask, forces, dt, predictor, mid_forces,
+ * corrector, flux, finalize) when timing is enabled, else zeros. */
+typedef struct swf_step_info {
+  double tau;
+  double active_fraction;
+  int lagrangian_blocks, flux_blocks, total_blocks;
+  double timings[8];
+  double clamp_deficit_volume;
+  double source_volume;
+  double boundary_outflow_volume;
+} swf_step_info;
+
+/* Stage ids for swf_stage, stepper.hpp:88-96 (step() composes these). */
+enum swf_stage_id {
+  SWF_STAGE_BEGIN = 0,       /* begin_step      stepper.cpp:172-201 */
+  SWF_STAGE_FORCES = 1,      /* compute_forces  stepper.cpp:210-222 */
+  SWF_STAGE_DT = 2,          /* compute_dt      stepper.cpp:224-267 */
+  SWF_STAGE_PREDICTOR = 3,   /* predictor       stepper.cpp:269-308 */
+  SWF_STAGE_MID_FORCES = 4,  /* mid_forces      stepper.cpp:310-333 */
+  SWF_STAGE_CORRECTOR = 5,   /* corrector       stepper.cpp:335-400 */
+  SWF_STAGE_FLUX = 6,        /* flux            stepper.cpp:579-626 */
+  SWF_STAGE_FINAL = 7        /* final_update    stepper.cpp:628-704 */
+};
+
+/* Scratch ids for swf_download_scratch, the span accessors of
+ * stepper.hpp:103-119. */
+enum swf_scratch_id {
+  SWF_SCR_FN_FX = 0, SWF_SCR_FN_FY, SWF_SCR_FN_FRIC_X, SWF_SCR_FN_FRIC_Y,
+  SWF_SCR_FN_SIGMA,                                   /* forces_n()   */
+  SWF_SCR_FM_FX, SWF_SCR_FM_FY, SWF_SCR_FM_FRIC_X, SWF_SCR_FM_FRIC_Y,
+  SWF_SCR_FM_SIGMA,                                   /* forces_mid() */
+  SWF_SCR_HALF_H, SWF_SCR_HALF_HUX, SWF_SCR_HALF_HUY, /* half_depth() + momenta */
+  SWF_SCR_HT, SWF_SCR_HVTX, SWF_SCR_HVTY,             /* lagrangian_*()  */
+  SWF_SCR_DRX, SWF_SCR_DRY,                           /* displacement_*() */
+  SWF_SCR_FH, SWF_SCR_FVX, SWF_SCR_FVY,               /* flux_*()     */
+  SWF_SCR_SIGMA, SWF_SCR_SRC_VX, SWF_SCR_SRC_VY,      /* step_sources() */
+  SWF_SCR_COUNT
+};
+
+typedef struct swf_ctx swf_ctx;
+
+/* ---- lifecycle: CsphTvdStepper::CsphTvdStepper, stepper.cpp:127-159 ---- */
+int swf_create(const swf_terrain* terrain, const swf_params* params,
+               const swf_control* control, const swf_options* options,
+               swf_ctx** out);
+void swf_destroy(swf_ctx* ctx);
+const char* swf_last_error(const swf_ctx* ctx);
+
+/* ---- configuration: set_wind / set_sources, stepper.cpp:161-170;
+ *      control() / options() mutable accessors, stepper.hpp:100-101 ---- */
+int swf_set_wind(swf_ctx* ctx, int n, const double* t, const double* wx,
+                 const double* wy);
+int swf_set_sources(swf_ctx* ctx, int n, const swf_source* sources);
+int swf_set_control(swf_ctx* ctx, const swf_control* control);
+int swf_get_control(const swf_ctx* ctx, swf_control* control);
+int swf_set_options(swf_ctx* ctx, const swf_options* options);
+int swf_get_options(const swf_ctx* ctx, swf_options* options);
+
+/* ---- state: FlowState, grid.hpp:42-57.  Host arrays of nx*ny doubles. ---- */
+int swf_upload_state(swf_ctx* ctx, const double* H, const double* HUx,
+                     const double* HUy, double t);
+int swf_download_state(swf_ctx* ctx, double* H, double* HUx, double* HUy,
+                       double* t);
+/* Device pointers of the resident state (zero-copy interop).  They change
+ * after every successful step (ping-pong buffers). */
+int swf_device_state(swf_ctx* ctx, double** H, double** HUx, double** HUy);
+
+/* ---- the hot path: CsphTvdStepper::step, stepper.cpp:706-749 ---- */
+/* Drop-in form of step(FlowState&, dt_cap): host buffers in, host buffers
+ * out, t advanced in place. */
+int swf_step_host(swf_ctx* ctx, double* H, double* HUx, double* HUy,
+                  double* t, double dt_cap, swf_step_info* info);
+/* One step on the device-resident state; info may be NULL (then no host
+ * synchronisation happens and errors surface at the next synchronising
+ * call). */
+int swf_step(swf_ctx* ctx, double dt_cap, swf_step_info* info);
+/* n steps on the device-resident state without host synchronisation in
+ * between (CUDA-graph replay).  Stops at the first failing step, leaving the
+ * state as it was before that step; *done receives the steps completed. */
+int swf_run(swf_ctx* ctx, int n, double dt_cap, int* done,
+            swf_step_info* last);
+/* Synchronise the context's stream and report a pending device error. */
+int swf_sync(swf_ctx* ctx);
+/* Enable per-stage device timing in swf_step_info.timings (adds events). */
+int swf_set_timing(swf_ctx* ctx, int enabled);
+/* The CUDA stream (cudaStream_t) of the context, for interop. */
+void* swf_stream(swf_ctx* ctx);
+/* Execution path of swf_step / swf_run: 0 = fused tile kernels (default),
+ * 1 = the unfused stage kernels (one per reference stage; keeps every
+ * scratch accessor current, like the reference). */
+int swf_set_mode(swf_ctx* ctx, int mode);
+
+/* ---- stage API (stepper.hpp:88-96) for stage-differential tests. ---- */
+/* arg is dt_cap for SWF_STAGE_DT and tau for the later stages; the tau that
+ * SWF_STAGE_DT computes is written to *tau_out (may be NULL). */
+int swf_stage(swf_ctx* ctx, int stage, double arg, double* tau_out);
+/* Span accessors (stepper.hpp:103-119): nx*ny doubles. */
+int swf_download_scratch(swf_ctx* ctx, int which, double* out);
+/* BlockMask counts (block.hpp:20-36), total_blocks ints each; nbx/nby out. */
+int swf_download_mask(swf_ctx* ctx, int* interior, int* halo, int* nbx,
+                      int* nby);
+/* last_clamp_deficit / last_source_volume / last_boundary_outflow,
+ * stepper.hpp:117-119. */
+int swf_last_volumes(swf_ctx* ctx, double* clamp_deficit, double* source_volume,
+                     double* boundary_outflow);
+
+/* ---- free per-cell functions evaluated ON THE DEVICE (KAT tests) ---- */
+/* hll_face_flux, riemann.hpp:18-19: in = n x {hL,unL,utL,hR,unR,utR},
+ * out = n x {fm,fn,ft}. */
+int swf_dev_hll_face_flux(int n, const double* in, double g, double* out);
+/* the libm-compatible cube root used by friction (forcing.hpp:81). */
+int swf_dev_cbrt(int n, const double* x, double* y);
+/* bottom_friction, forcing.cpp:26-28: in = n x {ux,uy,H}, out = n x {fx,fy}. */
+int swf_dev_bottom_friction(int n, const double* in, double g, double n_manning,
+                            double* out);
+
+/* ---- row-strip decomposition (multi-GPU) ---- */
+/* A strip context owns global rows [j0, j1) of an nx x ny_global domain and
+ * keeps SWF_HALO ghost rows on each interior side.  terrain->ny must equal
+ * ny_global and terrain->b the whole global bed (only the strip + ghost rows
+ * are copied).  device selects the CUDA device. */
+#define SWF_HALO 3
+int swf_create_strip(const swf_terrain* terrain, const swf_params* params,
+                     const swf_control* control, const swf_options* options,
+                     int j0, int j1, int device, swf_ctx** out);
+/* Split step for strips.  Before phase 1 the caller fills the ghost rows of
+ * the current state (swf_strip_halo_ptrs).  Phase 1 computes sources, the
+ * block mask and the forces, and returns this strip's CFL speed (an exact,
+ * non-negative double; synchronises the stream).  Phase 2 takes the global
+ * max speed over all strips (an exact allreduce-max), computes tau and
+ * finishes the step; info (may be NULL) reports this strip's blocks. */
+int swf_strip_phase1(swf_ctx* ctx, double dt_cap, double* speed_out);
+int swf_strip_phase2(swf_ctx* ctx, double global_speed, double dt_cap,
+                     swf_step_info* info);
+/* Device addresses of the halo rows of the CURRENT state for the exchange:
+ * side 0 = south (lower j), 1 = north.  send3/recv3 receive the H, HUx, HUy
+ * pointers of the SWF_HALO owned boundary rows and of the ghost rows;
+ * *count = doubles per field (0 when that side is a domain edge). */
+int swf_strip_halo_ptrs(swf_ctx* ctx, int side, double** send3, double** recv3,
+                        size_t* count);
+/* Owned global rows [j0, j1) and the ghost-row counts below/above. */
+int swf_strip_rows(const swf_ctx* ctx, int* j0, int* j1, int* ghost_lo,
+                   int* ghost_hi);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SWF_H_ */

@@ -1,0 +1,76 @@
+"""Loader for the in-tree CUDA library libswflood_cuda.so (the product path).
+
+There is deliberately no fallback: if the library is missing or no CUDA
+device is usable, calls fail loudly (ImportError / SWF_ECUDA).
+"""
+import ctypes as C
+import os
+
+from . import _abi as A
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libswflood_cuda.so")
+
+_lib = None
+
+
+def _sig(lib, name, res, *args):
+    f = getattr(lib, name)
+    f.restype = res
+    f.argtypes = list(args)
+
+
+def declare(lib):
+    P, I, D, V = C.c_void_p, C.c_int, C.c_double, None
+    PD, PI = A.PD, A.PI
+    PT = C.POINTER(A.swf_terrain)
+    PP = C.POINTER(A.swf_params)
+    PK = C.POINTER(A.swf_control)
+    PO = C.POINTER(A.swf_options)
+    PS = C.POINTER(A.swf_source)
+    PN = C.POINTER(A.swf_step_info)
+    PPD = C.POINTER(PD)
+    _sig(lib, "swf_create", I, PT, PP, PK, PO, C.POINTER(P))
+    _sig(lib, "swf_create_strip", I, PT, PP, PK, PO, I, I, I, C.POINTER(P))
+    _sig(lib, "swf_destroy", V, P)
+    _sig(lib, "swf_last_error", C.c_char_p, P)
+    _sig(lib, "swf_set_wind", I, P, I, PD, PD, PD)
+    _sig(lib, "swf_set_sources", I, P, I, PS)
+    _sig(lib, "swf_set_control", I, P, PK)
+    _sig(lib, "swf_get_control", I, P, PK)
+    _sig(lib, "swf_set_options", I, P, PO)
+    _sig(lib, "swf_get_options", I, P, PO)
+    _sig(lib, "swf_upload_state", I, P, PD, PD, PD, D)
+    _sig(lib, "swf_download_state", I, P, PD, PD, PD, PD)
+    _sig(lib, "swf_device_state", I, P, PPD, PPD, PPD)
+    _sig(lib, "swf_step_host", I, P, PD, PD, PD, PD, D, PN)
+    _sig(lib, "swf_step", I, P, D, PN)
+    _sig(lib, "swf_run", I, P, I, D, PI, PN)
+    _sig(lib, "swf_sync", I, P)
+    _sig(lib, "swf_set_timing", I, P, I)
+    _sig(lib, "swf_stream", P, P)
+    _sig(lib, "swf_set_mode", I, P, I)
+    _sig(lib, "swf_stage", I, P, I, D, PD)
+    _sig(lib, "swf_download_scratch", I, P, I, PD)
+    _sig(lib, "swf_download_mask", I, P, PI, PI, PI, PI)
+    _sig(lib, "swf_last_volumes", I, P, PD, PD, PD)
+    _sig(lib, "swf_dev_hll_face_flux", I, I, PD, D, PD)
+    _sig(lib, "swf_dev_cbrt", I, I, PD, PD)
+    _sig(lib, "swf_dev_bottom_friction", I, I, PD, D, D, PD)
+    _sig(lib, "swf_strip_phase1", I, P, D, PD)
+    _sig(lib, "swf_strip_phase2", I, P, D, D, PN)
+    _sig(lib, "swf_strip_halo_ptrs", I, P, I, PPD, PPD, C.POINTER(C.c_size_t))
+    _sig(lib, "swf_strip_rows", I, P, PI, PI, PI, PI)
+    return lib
+
+
+def lib():
+    """The loaded CUDA library (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                "(there is no CPU fallback)")
+        _lib = declare(C.CDLL(LIB_PATH))
+    return _lib

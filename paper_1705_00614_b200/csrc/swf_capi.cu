@@ -1,0 +1,826 @@
+// swf_capi.cu — the C ABI of include/swf.h: context lifecycle, validation
+// with the reference's error convention, state transfer, the step entry
+// points, CUDA-graph replay for batched runs, and device-side KAT helpers.
+//
+// Validation messages and order follow the reference constructor and setters
+// (grid.cpp:13-21, 42-51, 77-82; sources.cpp:22-33; stepper.cpp:31-37,
+// 127-170).  There is no CPU fallback: every compute entry point launches
+// sm_100a kernels and fails with SWF_ECUDA when no device is usable.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "swf_internal.cuh"
+
+namespace swf {
+
+static thread_local std::string g_err;
+
+int set_err(swf_ctx* c, int code, const std::string& msg) {
+  (c ? c->err : g_err) = msg;
+  return code;
+}
+
+int cuda_check(swf_ctx* c, cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return SWF_OK;
+  return set_err(c, SWF_ECUDA, std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+size_t local_cells(const swf_ctx* c) { return (size_t)c->geo.nx * (size_t)c->geo.rows; }
+
+void fill_block_counts(const swf_ctx* c, const StepScalars* sc, swf_step_info* info) {
+  int total = c->geo.nbx * (c->geo.bj1 - c->geo.bj0);
+  info->total_blocks = total;
+  info->lagrangian_blocks = c->geo.skip ? sc->lag_act : total;
+  info->flux_blocks = c->geo.skip ? sc->flux_act : total;
+  // active_fraction, block.cpp:81-87 (mask-based, independent of skipping)
+  info->active_fraction = total ? static_cast<double>(sc->flux_act) / total : 0.0;
+}
+
+int check_device_error(swf_ctx* c) {
+  cudaError_t e = cudaMemcpy(c->h_sc, c->d_sc, sizeof(StepScalars), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_check(c, e, "scalar readback");
+  unsigned long long key = c->h_sc->err_key;
+  if (key == ERR_NONE) return SWF_OK;
+  unsigned long long kind = key >> 58;
+  const Geo& G = c->geo;
+  if (kind == ERR_DT) {
+    // stepper.cpp:259-262 (std::to_string formats with %f)
+    char buf[256];
+    snprintf(buf, sizeof buf,
+             "timestep %f s fell below the abort floor %f s (max wave speed %f m/s)",
+             c->h_sc->err_val[0], c->h_sc->err_val[1], c->h_sc->err_val[2]);
+    return set_err(c, SWF_ENUMERICAL, buf);
+  }
+  unsigned long long ib = (key >> 24) & ((1ull << 34) - 1);
+  unsigned long long low = key & ((1ull << 24) - 1);
+  int bi = (int)(ib % G.nbx), bj = (int)(ib / G.nbx);
+  int i0 = bi * G.bs, j0 = bj * G.bs;
+  if (kind == ERR_CFL) {
+    int i = i0 + (int)(low % G.bs), j = j0 + (int)(low / G.bs);
+    char buf[256];
+    snprintf(buf, sizeof buf,
+             "particle displacement reached h/2 at cell (%d,%d); the Courant number is too large "
+             "for this flow",
+             i, j);
+    return set_err(c, SWF_ENUMERICAL, buf);
+  }
+  // ERR_FLUX: decode the face that the reference's serial traversal reports
+  long long p = (long long)((1ull << 24) - 1 - low);
+  long long span = G.bs + 2, ss = span * span;
+  int rank = (int)(p / (2 * ss));
+  long long within = p % (2 * ss);
+  int ei0 = i0 - (rank == 1 ? G.bs : 0), ej0 = j0 - (rank == 0 ? G.bs : 0);
+  int ci, cj;
+  if (within < ss) {  // x face: a = row, f = iface; ka = (f-1, a)
+    int a = ej0 + (int)(within / span), f = ei0 + (int)(within % span);
+    ci = f - 1;
+    cj = a;
+  } else {  // y face: a = column, f = jface; ka = (a, f-1)
+    long long w2 = within - ss;
+    int a = ei0 + (int)(w2 / span), f = ej0 + (int)(w2 % span);
+    ci = a;
+    cj = f - 1;
+  }
+  char buf[128];
+  snprintf(buf, sizeof buf, "non-finite flux near cell (%d,%d)", ci, cj);
+  return set_err(c, SWF_ENUMERICAL, buf);
+}
+
+size_t fused_tile_bytes();
+
+}  // namespace swf
+
+using namespace swf;
+
+namespace {
+
+int validate_control(swf_ctx* c, const swf_control* k) {
+  if (!(k->courant > 0.0 && k->courant < 1.0))
+    return set_err(c, SWF_ECONFIG, "timestep: Courant number must be in (0,1)");
+  if (!(k->dt_max > 0.0)) return set_err(c, SWF_ECONFIG, "timestep: dt_max must be positive");
+  if (!(k->dt_min > 0.0 && k->dt_min < k->dt_max))
+    return set_err(c, SWF_ECONFIG, "timestep: need 0 < dt_min < dt_max");
+  return SWF_OK;
+}
+
+int validate_setup(const swf_terrain* T, const swf_params* P) {
+  if (!T || !P) return set_err(nullptr, SWF_ECONFIG, "null argument");
+  if (T->nx < 1 || T->ny < 1) return set_err(nullptr, SWF_ECONFIG, "terrain: nx and ny must be >= 1");
+  if (!(T->h > 0.0)) return set_err(nullptr, SWF_ECONFIG, "terrain: cell size must be positive");
+  if (!T->b) return set_err(nullptr, SWF_ECONFIG, "terrain: bed array size mismatch");
+  if ((long long)T->nx * T->ny > 2147483647LL)
+    return set_err(nullptr, SWF_ECONFIG, "terrain: more than 2^31-1 cells");
+  size_t n = (size_t)T->nx * T->ny;
+  for (size_t k = 0; k < n; ++k)
+    if (!std::isfinite(T->b[k]))
+      return set_err(nullptr, SWF_ECONFIG,
+                     "terrain: non-finite bed elevation at cell " + std::to_string(k));
+  if (!(P->g > 0.0)) return set_err(nullptr, SWF_ECONFIG, "params: gravity must be positive");
+  if (P->n_manning < 0.0) return set_err(nullptr, SWF_ECONFIG, "params: Manning coefficient must be >= 0");
+  if (P->n_field)
+    for (size_t k = 0; k < n; ++k)
+      if (P->n_field[k] < 0.0) return set_err(nullptr, SWF_ECONFIG, "params: Manning field must be >= 0");
+  if (P->nu < 0.0) return set_err(nullptr, SWF_ECONFIG, "params: viscosity must be >= 0");
+  if (!(P->rho_water > 0.0)) return set_err(nullptr, SWF_ECONFIG, "params: water density must be positive");
+  if (P->rho_air < 0.0) return set_err(nullptr, SWF_ECONFIG, "params: air density must be >= 0");
+  if (!(P->eps_dry > 0.0)) return set_err(nullptr, SWF_ECONFIG, "params: dry threshold must be positive");
+  return SWF_OK;
+}
+
+void drop_graph(swf_ctx* c) {
+  if (c->graph) cudaGraphExecDestroy(c->graph);
+  c->graph = nullptr;
+  c->graph_dt_cap = -1.0;
+}
+
+// geometry derived from options (block size, boundaries, skipping)
+int apply_options(swf_ctx* c, const swf_options* o) {
+  if (o->block_size < 1) return set_err(c, SWF_ECONFIG, "stepper: block size must be >= 1");
+  Geo& G = c->geo;
+  int old_bs = G.bs, old_bj0 = G.bj0, old_bj1 = G.bj1;
+  c->opt = *o;
+  if (c->opt.workers < 1) c->opt.workers = 1;
+  G.bs = o->block_size;
+  G.nbx = (G.nx + G.bs - 1) / G.bs;
+  G.nby = (G.ny + G.bs - 1) / G.bs;
+  int jglo = G.jg0 + G.r0, jghi = G.jg0 + G.r1;  // owned global rows
+  if (jglo % G.bs != 0 || (jghi % G.bs != 0 && jghi != G.ny))
+    return set_err(c, SWF_ECONFIG, "strip boundaries must be multiples of the block size");
+  G.bj0 = jglo / G.bs;
+  G.bj1 = (jghi + G.bs - 1) / G.bs;
+  G.west_refl = o->west == SWF_EDGE_REFLECTIVE;
+  G.east_refl = o->east == SWF_EDGE_REFLECTIVE;
+  G.south_refl = o->south == SWF_EDGE_REFLECTIVE;
+  G.north_refl = o->north == SWF_EDGE_REFLECTIVE;
+  G.skip = o->skip_dry_blocks != 0;
+  if (!c->d_interior || old_bs != G.bs || old_bj0 != G.bj0 || old_bj1 != G.bj1) {
+    cudaFree(c->d_interior);
+    cudaFree(c->d_halo);
+    cudaFree(c->d_bflag);
+    size_t nb = (size_t)G.nbx * (G.bj1 - G.bj0);
+    cudaError_t e = cudaMalloc(&c->d_interior, (nb ? nb : 1) * sizeof(int));
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_halo, (nb ? nb : 1) * sizeof(int));
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_bflag, nb ? nb : 1);
+    if (e == cudaSuccess) e = cudaMemset(c->d_interior, 0, (nb ? nb : 1) * sizeof(int));
+    if (e == cudaSuccess) e = cudaMemset(c->d_halo, 0, (nb ? nb : 1) * sizeof(int));
+    if (e == cudaSuccess) e = cudaMemset(c->d_bflag, 0, nb ? nb : 1);
+    if (e != cudaSuccess) return cuda_check(c, e, "mask allocation");
+  }
+  drop_graph(c);
+  return SWF_OK;
+}
+
+void apply_control(swf_ctx* c, const swf_control* k) {
+  c->ctl = *k;
+  c->geo.courant = k->courant;
+  c->geo.dt_max = k->dt_max;
+  c->geo.dt_min = k->dt_min;
+  drop_graph(c);
+}
+
+int create_impl(const swf_terrain* T, const swf_params* P, const swf_control* K,
+                const swf_options* O, int j0, int j1, int device, swf_ctx** out) {
+  *out = nullptr;
+  int rc = validate_setup(T, P);
+  if (rc) return rc;
+  if (!K || !O) return set_err(nullptr, SWF_ECONFIG, "null argument");
+  rc = validate_control(nullptr, K);
+  if (rc) return rc;
+  if (O->block_size < 1) return set_err(nullptr, SWF_ECONFIG, "stepper: block size must be >= 1");
+  if (j0 < 0 || j1 > T->ny || j0 >= j1) return set_err(nullptr, SWF_ECONFIG, "strip rows out of range");
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    return set_err(nullptr, SWF_ECUDA,
+                   std::string("no CUDA device available (libswflood_cuda has no CPU path): ") +
+                       cudaGetErrorString(e));
+  if (device < 0 || device >= ndev) return set_err(nullptr, SWF_ECONFIG, "device index out of range");
+  e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_check(nullptr, e, "cudaSetDevice");
+
+  swf_ctx* c = new swf_ctx();
+  c->device = device;
+  c->h = T->h;
+  c->x0 = T->x0;
+  c->y0 = T->y0;
+  c->params = *P;
+  c->params.n_field = nullptr;
+  Geo& G = c->geo;
+  G.nx = T->nx;
+  G.ny = T->ny;
+  int glo = j0 > 0 ? SWF_HALO : 0, ghi = j1 < T->ny ? SWF_HALO : 0;
+  if (j0 - glo < 0) glo = j0;
+  if (j1 + ghi > T->ny) ghi = T->ny - j1;
+  G.jg0 = j0 - glo;
+  G.rows = (j1 - j0) + glo + ghi;
+  G.r0 = glo;
+  G.r1 = glo + (j1 - j0);
+  G.has_nfield = P->n_field != nullptr;
+  G.n_manning = P->n_manning;
+  G.P.g = P->g;
+  G.P.nu = P->nu;
+  G.P.omega_z = P->omega_z;
+  G.P.c_a = P->c_a;
+  G.P.rho_air = P->rho_air;
+  G.P.rho_water = P->rho_water;
+  G.P.eps = P->eps_dry;
+  G.P.h = T->h;
+  G.P.inv_h2 = 1.0 / (T->h * T->h);
+  G.P.two_h = 2.0 * T->h;
+  G.tiles_x = (G.nx + 31) / 32;
+  G.tiles_y = (G.r1 - G.r0 + 15) / 16;
+  apply_control(c, K);
+  rc = apply_options(c, O);
+  if (rc) {
+    g_err = c->err;
+    swf_destroy(c);
+    return rc;
+  }
+  size_t n = local_cells(c);
+  size_t bytes = n * sizeof(double);
+  const double* bsrc = T->b + (size_t)G.jg0 * G.nx;
+  e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMalloc(&c->b, bytes);
+  if (e == cudaSuccess) e = cudaMemcpy(c->b, bsrc, bytes, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && P->n_field) {
+    e = cudaMalloc(&c->nf, bytes);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(c->nf, P->n_field + (size_t)G.jg0 * G.nx, bytes, cudaMemcpyHostToDevice);
+  }
+  for (int s = 0; s < 2 && e == cudaSuccess; ++s) {
+    e = cudaMalloc(&c->H[s], bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&c->HUx[s], bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&c->HUy[s], bytes);
+    if (e == cudaSuccess) e = cudaMemset(c->H[s], 0, bytes);
+    if (e == cudaSuccess) e = cudaMemset(c->HUx[s], 0, bytes);
+    if (e == cudaSuccess) e = cudaMemset(c->HUy[s], 0, bytes);
+  }
+  if (e == cudaSuccess) e = cudaMalloc(&c->fpx, bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&c->fpy, bytes);
+  size_t nt = (size_t)G.tiles_x * G.tiles_y;
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_tile_act, nt ? nt : 1);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_tile_same, nt ? nt : 1);
+  if (e == cudaSuccess) e = cudaMemset(c->d_tile_same, 1, nt ? nt : 1);  // both buffers zero
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_part, 3 * (nt ? nt : 1) * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_sig, 2 * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_sc, sizeof(StepScalars));
+  if (e == cudaSuccess) e = cudaMallocHost(&c->h_sc, sizeof(StepScalars));
+  if (e == cudaSuccess) {
+    std::memset(c->h_sc, 0, sizeof(StepScalars));
+    c->h_sc->err_key = ERR_NONE;
+    c->h_sc->fail_step = -1;
+    e = cudaMemcpy(c->d_sc, c->h_sc, sizeof(StepScalars), cudaMemcpyHostToDevice);
+  }
+  for (int i = 0; i < 10 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
+  if (e != cudaSuccess) {
+    rc = cuda_check(nullptr, e, "context allocation");
+    swf_destroy(c);
+    return rc;
+  }
+  *out = c;
+  return SWF_OK;
+}
+
+// reset the device error/step counters before a new batch
+int reset_counters(swf_ctx* c) {
+  c->h_sc->err_key = ERR_NONE;
+  c->h_sc->fail_step = -1;
+  c->h_sc->steps_done = 0;
+  cudaError_t e = cudaMemcpyAsync(&c->d_sc->err_key, &c->h_sc->err_key, sizeof(unsigned long long),
+                                  cudaMemcpyHostToDevice, c->stream);
+  int zero = 0, neg = -1;
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(&c->d_sc->steps_done, &zero, sizeof(int), cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(&c->d_sc->fail_step, &neg, sizeof(int), cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  return cuda_check(c, e, "counter reset");
+}
+
+void fill_fused_info(swf_ctx* c, swf_step_info* info) {
+  const StepScalars* s = c->h_sc;
+  std::memset(info, 0, sizeof *info);
+  info->tau = s->tau;
+  fill_block_counts(c, s, info);
+  info->clamp_deficit_volume = s->deficit;
+  info->source_volume = s->srcvol;
+  info->boundary_outflow_volume = s->outflow;
+  if (c->timing) {
+    float ms;
+    // buckets: mask (begin+K1), forces (K2), dt (K3 tail), flux (K4..K8 fused), finalize
+    int map[5][2] = {{0, 0}, {1, 1}, {2, 2}, {3, 6}, {4, 7}};
+    for (auto& m : map) {
+      if (cudaEventElapsedTime(&ms, c->ev[m[0]], c->ev[m[0] + 1]) == cudaSuccess)
+        info->timings[m[1]] = ms * 1e-3;
+    }
+  }
+}
+
+// After a synchronised batch: roll back the ping-pong index to the last
+// committed state and report the device error, if any.
+int commit_batch(swf_ctx* c, int cur_start, int enqueued, int* done) {
+  int rc = check_device_error(c);
+  int ok = c->h_sc->steps_done;
+  if (done) *done = ok;
+  (void)enqueued;
+  c->cur = (cur_start + ok) & 1;
+  c->h_t = c->h_sc->t;
+  return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+int swf_create(const swf_terrain* terrain, const swf_params* params, const swf_control* control,
+               const swf_options* options, swf_ctx** out) {
+  if (!out) return set_err(nullptr, SWF_ECONFIG, "null output pointer");
+  return create_impl(terrain, params, control, options, 0, terrain ? terrain->ny : 0, 0, out);
+}
+
+int swf_create_strip(const swf_terrain* terrain, const swf_params* params,
+                     const swf_control* control, const swf_options* options, int j0, int j1,
+                     int device, swf_ctx** out) {
+  if (!out) return set_err(nullptr, SWF_ECONFIG, "null output pointer");
+  return create_impl(terrain, params, control, options, j0, j1, device, out);
+}
+
+void swf_destroy(swf_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  drop_graph(c);
+  stage_free(c);
+  void* ptrs[] = {c->b, c->nf, c->H[0], c->H[1], c->HUx[0], c->HUx[1], c->HUy[0], c->HUy[1],
+                  c->fpx, c->fpy, c->d_src, c->d_ht, c->d_hq, c->d_sig, c->d_wt, c->d_wv,
+                  c->d_interior, c->d_halo, c->d_bflag, c->d_tile_act, c->d_tile_same,
+                  c->d_part, c->d_sc};
+  for (void* p : ptrs) cudaFree(p);
+  if (c->h_sc) cudaFreeHost(c->h_sc);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+const char* swf_last_error(const swf_ctx* c) { return c ? c->err.c_str() : g_err.c_str(); }
+
+int swf_set_wind(swf_ctx* c, int n, const double* t, const double* wx, const double* wy) {
+  for (int k = 1; k < n; ++k)
+    if (!(t[k] > t[k - 1])) return set_err(c, SWF_ECONFIG, "wind: sample times must be strictly increasing");
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  c->h_wt.assign(t, t + n);
+  c->h_wv.resize(2 * (size_t)n);
+  for (int k = 0; k < n; ++k) {
+    c->h_wv[2 * k] = wx[k];
+    c->h_wv[2 * k + 1] = wy[k];
+  }
+  cudaFree(c->d_wt);
+  cudaFree(c->d_wv);
+  c->d_wt = c->d_wv = nullptr;
+  cudaError_t e = cudaSuccess;
+  if (n > 0) {
+    e = cudaMalloc(&c->d_wt, n * sizeof(double));
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_wv, 2 * n * sizeof(double));
+    if (e == cudaSuccess) e = cudaMemcpy(c->d_wt, t, n * sizeof(double), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(c->d_wv, c->h_wv.data(), 2 * n * sizeof(double), cudaMemcpyHostToDevice);
+  }
+  c->geo.nwind = n;
+  drop_graph(c);
+  return cuda_check(c, e, "set_wind");
+}
+
+int swf_set_sources(swf_ctx* c, int n, const swf_source* s) {
+  const Geo& G = c->geo;
+  for (int k = 0; k < n; ++k) {
+    std::string nm = "source 'src" + std::to_string(k) + "': ";
+    if (s[k].i0 > s[k].i1 || s[k].j0 > s[k].j1) return set_err(c, SWF_ECONFIG, nm + "empty cell rectangle");
+    bool in0 = s[k].i0 >= 0 && s[k].i0 < G.nx && s[k].j0 >= 0 && s[k].j0 < G.ny;
+    bool in1 = s[k].i1 >= 0 && s[k].i1 < G.nx && s[k].j1 >= 0 && s[k].j1 < G.ny;
+    if (!in0 || !in1) return set_err(c, SWF_ECONFIG, nm + "cells outside grid");
+    for (int m = 1; m < s[k].n_hydro; ++m)
+      if (!(s[k].hydro_t[m] > s[k].hydro_t[m - 1]))
+        return set_err(c, SWF_ECONFIG, nm + "hydrograph times must be strictly increasing");
+    if (s[k].kind == SWF_SOURCE_DISCHARGE && s[k].n_hydro <= 0)
+      return set_err(c, SWF_ECONFIG, nm + "discharge source needs a hydrograph");
+  }
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  c->h_src.clear();
+  c->h_ht.clear();
+  c->h_hq.clear();
+  for (int k = 0; k < n; ++k) {
+    DevSrc d;
+    d.kind = s[k].kind;
+    d.i0 = s[k].i0;
+    d.j0 = s[k].j0;
+    d.i1 = s[k].i1;
+    d.j1 = s[k].j1;
+    d.nh = s[k].n_hydro;
+    d.off = (int)c->h_ht.size();
+    d.rate = s[k].rate;
+    d.vx = s[k].vx;
+    d.vy = s[k].vy;
+    int count = (d.i1 - d.i0 + 1) * (d.j1 - d.j0 + 1);
+    d.count_area = (double)count * (c->h * c->h);
+    for (int m = 0; m < d.nh; ++m) {
+      c->h_ht.push_back(s[k].hydro_t[m]);
+      c->h_hq.push_back(s[k].hydro_q[m]);
+    }
+    c->h_src.push_back(d);
+  }
+  cudaFree(c->d_src);
+  cudaFree(c->d_ht);
+  cudaFree(c->d_hq);
+  cudaFree(c->d_sig);
+  c->d_src = nullptr;
+  c->d_ht = c->d_hq = c->d_sig = nullptr;
+  cudaError_t e = cudaMalloc(&c->d_sig, 2 * (n > 0 ? n : 1) * sizeof(double));
+  if (e == cudaSuccess && n > 0) {
+    e = cudaMalloc(&c->d_src, n * sizeof(DevSrc));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(c->d_src, c->h_src.data(), n * sizeof(DevSrc), cudaMemcpyHostToDevice);
+    size_t nh = c->h_ht.size();
+    if (nh > 0) {
+      if (e == cudaSuccess) e = cudaMalloc(&c->d_ht, nh * sizeof(double));
+      if (e == cudaSuccess) e = cudaMalloc(&c->d_hq, nh * sizeof(double));
+      if (e == cudaSuccess)
+        e = cudaMemcpy(c->d_ht, c->h_ht.data(), nh * sizeof(double), cudaMemcpyHostToDevice);
+      if (e == cudaSuccess)
+        e = cudaMemcpy(c->d_hq, c->h_hq.data(), nh * sizeof(double), cudaMemcpyHostToDevice);
+    }
+  }
+  c->geo.nsrc = n;
+  if (n == 0) stage_clear_sources(c);  // src_.clear_values(), stepper.cpp:169
+  drop_graph(c);
+  return cuda_check(c, e, "set_sources");
+}
+
+int swf_set_control(swf_ctx* c, const swf_control* k) {
+  // control() is a plain mutable reference in the reference (stepper.hpp:100)
+  apply_control(c, k);
+  return SWF_OK;
+}
+
+int swf_get_control(const swf_ctx* c, swf_control* k) {
+  *k = c->ctl;
+  return SWF_OK;
+}
+
+int swf_set_options(swf_ctx* c, const swf_options* o) {
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  return apply_options(c, o);
+}
+
+int swf_get_options(const swf_ctx* c, swf_options* o) {
+  *o = c->opt;
+  return SWF_OK;
+}
+
+int swf_upload_state(swf_ctx* c, const double* H, const double* HUx, const double* HUy, double t) {
+  cudaSetDevice(c->device);
+  size_t n = local_cells(c), bytes = n * sizeof(double);
+  size_t off = (size_t)c->geo.jg0 * c->geo.nx;  // strips: rows of a global array
+  cudaError_t e = cudaMemcpyAsync(c->H[c->cur], H + off, bytes, cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(c->HUx[c->cur], HUx + off, bytes, cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(c->HUy[c->cur], HUy + off, bytes, cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(&c->d_sc->t, &t, sizeof(double), cudaMemcpyHostToDevice, c->stream);
+  size_t nt = (size_t)c->geo.tiles_x * c->geo.tiles_y;
+  if (e == cudaSuccess && nt) e = cudaMemsetAsync(c->d_tile_same, 0, nt, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  c->h_t = t;
+  return cuda_check(c, e, "upload_state");
+}
+
+int swf_download_state(swf_ctx* c, double* H, double* HUx, double* HUy, double* t) {
+  cudaSetDevice(c->device);
+  const Geo& G = c->geo;
+  size_t off = (size_t)G.r0 * G.nx, n = (size_t)(G.r1 - G.r0) * G.nx, bytes = n * sizeof(double);
+  size_t hoff = (size_t)(G.jg0 + G.r0) * G.nx;  // owned rows into a global-shaped array
+  cudaError_t e = cudaMemcpyAsync(H + hoff, c->H[c->cur] + off, bytes, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(HUx + hoff, c->HUx[c->cur] + off, bytes, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(HUy + hoff, c->HUy[c->cur] + off, bytes, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess && t) e = cudaMemcpyAsync(t, &c->d_sc->t, sizeof(double), cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  return cuda_check(c, e, "download_state");
+}
+
+int swf_device_state(swf_ctx* c, double** H, double** HUx, double** HUy) {
+  if (H) *H = c->H[c->cur];
+  if (HUx) *HUx = c->HUx[c->cur];
+  if (HUy) *HUy = c->HUy[c->cur];
+  return SWF_OK;
+}
+
+int swf_step(swf_ctx* c, double dt_cap, swf_step_info* info) {
+  cudaSetDevice(c->device);
+  if (c->mode == 1) {
+    int rc = reset_counters(c);
+    if (rc) return rc;
+    swf_step_info tmp;
+    return stage_step(c, dt_cap, info ? info : &tmp);
+  }
+  int cur0 = c->cur;
+  int rc = reset_counters(c);
+  if (rc) return rc;
+  rc = fused_enqueue_step(c, dt_cap);
+  if (rc) {
+    c->cur = cur0;
+    return rc;
+  }
+  if (!info) return SWF_OK;  // errors surface at the next synchronising call
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return cuda_check(c, e, "step");
+  rc = commit_batch(c, cur0, 1, nullptr);
+  if (rc) return rc;
+  fill_fused_info(c, info);
+  return SWF_OK;
+}
+
+int swf_step_host(swf_ctx* c, double* H, double* HUx, double* HUy, double* t, double dt_cap,
+                  swf_step_info* info) {
+  int rc = swf_upload_state(c, H, HUx, HUy, *t);
+  if (rc) return rc;
+  swf_step_info tmp;
+  rc = swf_step(c, dt_cap, info ? info : &tmp);
+  if (rc) return rc;  // state untouched on abort (stepper.cpp:391-399, 568-577)
+  return swf_download_state(c, H, HUx, HUy, t);
+}
+
+int swf_run(swf_ctx* c, int n, double dt_cap, int* done, swf_step_info* last) {
+  cudaSetDevice(c->device);
+  if (done) *done = 0;
+  if (n <= 0) return SWF_OK;
+  if (c->mode == 1) {
+    for (int k = 0; k < n; ++k) {
+      swf_step_info tmp;
+      int rc = swf_step(c, dt_cap, last ? last : &tmp);
+      if (rc) return rc;
+      if (done) *done = k + 1;
+    }
+    return SWF_OK;
+  }
+  int cur0 = c->cur;
+  int rc = reset_counters(c);
+  if (rc) return rc;
+  int enq = 0;
+  // leading single step to reach an even buffer parity for the graph
+  if (c->cur != 0) {
+    if ((rc = fused_enqueue_step(c, dt_cap))) return rc;
+    ++enq;
+  }
+  int pairs = (n - enq) / 2;
+  if (pairs > 0) {
+    if (!c->graph || c->graph_dt_cap != dt_cap || c->timing) {
+      drop_graph(c);
+      cudaGraph_t g;
+      cudaError_t e = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal);
+      if (e != cudaSuccess) return cuda_check(c, e, "graph capture");
+      bool saved = c->timing;
+      c->timing = false;
+      int rc1 = fused_enqueue_step(c, dt_cap);
+      int rc2 = rc1 ? rc1 : fused_enqueue_step(c, dt_cap);
+      c->timing = saved;
+      e = cudaStreamEndCapture(c->stream, &g);
+      if (rc2) return rc2;
+      if (e != cudaSuccess) return cuda_check(c, e, "graph capture end");
+      e = cudaGraphInstantiate(&c->graph, g, 0);
+      cudaGraphDestroy(g);
+      if (e != cudaSuccess) return cuda_check(c, e, "graph instantiate");
+      c->graph_dt_cap = dt_cap;
+    }
+    for (int p = 0; p < pairs; ++p) {
+      cudaError_t e = cudaGraphLaunch(c->graph, c->stream);
+      if (e != cudaSuccess) return cuda_check(c, e, "graph launch");
+    }
+    enq += 2 * pairs;
+    c->cur = 0;  // the captured pairs end on buffer 0
+  }
+  if (enq < n) {
+    if ((rc = fused_enqueue_step(c, dt_cap))) return rc;
+    ++enq;
+  }
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return cuda_check(c, e, "run");
+  rc = commit_batch(c, cur0, enq, done);
+  if (last && c->h_sc->steps_done > 0) fill_fused_info(c, last);
+  return rc;
+}
+
+int swf_sync(swf_ctx* c) {
+  cudaSetDevice(c->device);
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return cuda_check(c, e, "sync");
+  return check_device_error(c);
+}
+
+int swf_set_timing(swf_ctx* c, int enabled) {
+  c->timing = enabled != 0;
+  drop_graph(c);
+  return SWF_OK;
+}
+
+void* swf_stream(swf_ctx* c) { return (void*)c->stream; }
+
+int swf_set_mode(swf_ctx* c, int mode) {
+  if (mode != 0 && mode != 1) return set_err(c, SWF_ECONFIG, "mode must be 0 (fused) or 1 (staged)");
+  c->mode = mode;
+  return SWF_OK;
+}
+
+int swf_stage(swf_ctx* c, int stage, double arg, double* tau_out) {
+  cudaSetDevice(c->device);
+  if (stage == SWF_STAGE_BEGIN) {
+    int rc = reset_counters(c);
+    if (rc) return rc;
+  }
+  int rc = stage_run(c, stage, arg, tau_out);
+  if (rc) return rc;
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return cuda_check(c, e, "stage");
+  return SWF_OK;
+}
+
+int swf_download_scratch(swf_ctx* c, int which, double* out) {
+  cudaSetDevice(c->device);
+  return stage_download(c, which, out);
+}
+
+int swf_download_mask(swf_ctx* c, int* interior, int* halo, int* nbx, int* nby) {
+  cudaSetDevice(c->device);
+  const Geo& G = c->geo;
+  size_t nb = (size_t)G.nbx * (G.bj1 - G.bj0);
+  if (nbx) *nbx = G.nbx;
+  if (nby) *nby = G.bj1 - G.bj0;
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e == cudaSuccess && interior && nb)
+    e = cudaMemcpy(interior, c->d_interior, nb * sizeof(int), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && halo && nb) e = cudaMemcpy(halo, c->d_halo, nb * sizeof(int), cudaMemcpyDeviceToHost);
+  return cuda_check(c, e, "download_mask");
+}
+
+int swf_last_volumes(swf_ctx* c, double* cd, double* sv, double* bo) {
+  cudaSetDevice(c->device);
+  double v[3] = {0, 0, 0};
+  if (c->mode == 1 || c->scr) {
+    int rc = stage_volumes(c, v);
+    if (rc) return rc;
+  }
+  if (c->mode == 0) {
+    cudaError_t e = cudaMemcpy(c->h_sc, c->d_sc, sizeof(StepScalars), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_check(c, e, "volumes");
+    v[0] = c->h_sc->deficit;
+    v[1] = c->h_sc->srcvol;
+    v[2] = c->h_sc->outflow;
+  }
+  if (cd) *cd = v[0];
+  if (sv) *sv = v[1];
+  if (bo) *bo = v[2];
+  return SWF_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// device-side KAT helpers (free functions evaluated on the GPU)
+// ---------------------------------------------------------------------------
+namespace {
+
+__global__ void k_hll(int n, const double* in, double g, double* out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* a = in + 6 * (size_t)i;
+  FaceFlux f = hll_face_flux(a[0], a[1], a[2], a[3], a[4], a[5], g);
+  out[3 * (size_t)i] = f.fm;
+  out[3 * (size_t)i + 1] = f.fn;
+  out[3 * (size_t)i + 2] = f.ft;
+}
+
+__global__ void k_cbrt(int n, const double* x, double* y) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = glibc_cbrt(x[i]);
+}
+
+__global__ void k_fric(int n, const double* in, double g, double nm, double* out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double fx, fy;
+  friction_core(in[3 * (size_t)i], in[3 * (size_t)i + 1], in[3 * (size_t)i + 2], g, nm, fx, fy);
+  out[2 * (size_t)i] = fx;
+  out[2 * (size_t)i + 1] = fy;
+}
+
+template <class L>
+int run_kat(size_t nin, const double* in, size_t nout, double* out, L&& launch) {
+  double *din = nullptr, *dout = nullptr;
+  cudaError_t e = cudaMalloc(&din, (nin ? nin : 1) * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&dout, (nout ? nout : 1) * sizeof(double));
+  if (e == cudaSuccess && nin) e = cudaMemcpy(din, in, nin * sizeof(double), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    launch(din, dout);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e == cudaSuccess && nout) e = cudaMemcpy(out, dout, nout * sizeof(double), cudaMemcpyDeviceToHost);
+  cudaFree(din);
+  cudaFree(dout);
+  return cuda_check(nullptr, e, "device KAT");
+}
+
+}  // namespace
+
+extern "C" {
+
+int swf_dev_hll_face_flux(int n, const double* in, double g, double* out) {
+  return run_kat(6 * (size_t)n, in, 3 * (size_t)n, out, [&](double* di, double* dout) {
+    k_hll<<<(n + 255) / 256, 256>>>(n, di, g, dout);
+  });
+}
+
+int swf_dev_cbrt(int n, const double* x, double* y) {
+  return run_kat((size_t)n, x, (size_t)n, y, [&](double* di, double* dout) {
+    k_cbrt<<<(n + 255) / 256, 256>>>(n, di, dout);
+  });
+}
+
+int swf_dev_bottom_friction(int n, const double* in, double g, double nm, double* out) {
+  return run_kat(3 * (size_t)n, in, 2 * (size_t)n, out, [&](double* di, double* dout) {
+    k_fric<<<(n + 255) / 256, 256>>>(n, di, g, nm, dout);
+  });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// row strips (multi-GPU decomposition)
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int swf_strip_phase1(swf_ctx* c, double dt_cap, double* speed_out) {
+  cudaSetDevice(c->device);
+  int rc = reset_counters(c);
+  if (rc) return rc;
+  rc = fused_enqueue_phase1(c, dt_cap);
+  if (rc) return rc;
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return cuda_check(c, e, "strip phase 1");
+  rc = check_device_error(c);
+  if (rc) return rc;
+  if (speed_out) *speed_out = bitsd(c->h_sc->speed_bits);
+  return SWF_OK;
+}
+
+int swf_strip_phase2(swf_ctx* c, double global_speed, double dt_cap, swf_step_info* info) {
+  cudaSetDevice(c->device);
+  int cur0 = c->cur;
+  int rc = fused_enqueue_phase2(c, dt_cap, global_speed < 0.0 ? 0.0 : global_speed);
+  if (rc) {
+    c->cur = cur0;
+    return rc;
+  }
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return cuda_check(c, e, "strip phase 2");
+  rc = commit_batch(c, cur0, 1, nullptr);
+  if (rc) return rc;
+  if (info) fill_fused_info(c, info);
+  return SWF_OK;
+}
+
+int swf_strip_halo_ptrs(swf_ctx* c, int side, double** send3, double** recv3, size_t* count) {
+  const Geo& G = c->geo;
+  int ghosts = side == 0 ? G.r0 : G.rows - G.r1;
+  size_t nx = G.nx;
+  *count = (size_t)ghosts * nx;
+  int rs = side == 0 ? G.r0 : G.r1 - ghosts;  // first owned row to send
+  int rr = side == 0 ? 0 : G.r1;              // first ghost row to receive
+  double* f[3] = {c->H[c->cur], c->HUx[c->cur], c->HUy[c->cur]};
+  for (int q = 0; q < 3; ++q) {
+    send3[q] = f[q] + (size_t)rs * nx;
+    recv3[q] = f[q] + (size_t)rr * nx;
+  }
+  return SWF_OK;
+}
+
+int swf_strip_rows(const swf_ctx* c, int* j0, int* j1, int* glo, int* ghi) {
+  const Geo& G = c->geo;
+  if (j0) *j0 = G.jg0 + G.r0;
+  if (j1) *j1 = G.jg0 + G.r1;
+  if (glo) *glo = G.r0;
+  if (ghi) *ghi = G.rows - G.r1;
+  return SWF_OK;
+}
+
+}  // extern "C"

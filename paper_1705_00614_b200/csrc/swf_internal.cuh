@@ -1,0 +1,173 @@
+// swf_internal.cuh — device context of libswflood_cuda.so (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/swf.h"
+#include "swf_math.cuh"
+
+namespace swf {
+
+// A source spec on the device (sources.hpp:25-36): rectangle, velocity, and
+// the per-step sigma values at t_n and t_mid (computed by the begin/tau
+// kernels, sources.cpp:37-41).
+struct DevSrc {
+  int kind, i0, j0, i1, j1, nh, off;  // off = offset into the hydrograph arrays
+  double rate, vx, vy;
+  double count_area;  // (double)count * (h*h), sources.cpp:40
+};
+
+// Device-resident per-step scalars.
+struct StepScalars {
+  double t;      // FlowState::t on the device
+  double tau;    // this step's tau
+  double t_mid;  // t + 0.5*tau
+  double dt_cap;
+  unsigned long long speed_bits;  // max CFL speed (non-negative double bits)
+  double wind_n[2], wind_mid[2];
+  unsigned long long err_key;  // (kind << 58) | detail; ~0ull = none
+  double err_val[3];           // dt floor: cfl, dt_min, speed
+  int lag_act, flux_act;  // active B-blocks (interior>0, interior|halo>0), owned
+  int total_blocks;
+  int steps_done;   // successful steps since the counter was reset
+  int fail_step;    // step index of the first failure (-1 none)
+  double deficit, srcvol, outflow;  // this step's diagnostics (volumes)
+  double speed_local;               // strips: local max speed (phase 1 out)
+};
+
+enum ErrKind : unsigned long long { ERR_DT = 1, ERR_CFL = 2, ERR_FLUX = 3 };
+constexpr unsigned long long ERR_NONE = ~0ull;
+
+// Launch-invariant parameters of one context (passed by value to kernels).
+struct Geo {
+  int nx;        // columns
+  int ny;        // GLOBAL rows
+  int rows;      // local rows (owned + ghosts)
+  int jg0;       // global row of local row 0
+  int r0, r1;    // owned local rows [r0, r1)
+  int bs, nbx, nby;     // B-blocks over the GLOBAL grid
+  int bj0, bj1;         // owned block rows [bj0, bj1)
+  int tiles_x, tiles_y; // fused-kernel tiles over owned rows
+  int west_refl, east_refl, south_refl, north_refl;
+  int skip;
+  int has_nfield;
+  int nsrc, nwind;
+  double n_manning;
+  double courant, dt_max, dt_min;
+  PhysConst P;
+};
+
+struct Scratch;  // stage-path arrays (lazy)
+
+}  // namespace swf
+
+struct swf_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  swf::Geo geo{};
+  double h = 0, x0 = 0, y0 = 0;
+  swf_params params{};
+  swf_control ctl{};
+  swf_options opt{};
+  // device arrays (local rows)
+  double* b = nullptr;
+  double* nf = nullptr;
+  double* H[2] = {nullptr, nullptr};
+  double* HUx[2] = {nullptr, nullptr};
+  double* HUy[2] = {nullptr, nullptr};
+  int cur = 0;
+  double* fpx = nullptr;  // f_n.fx - f_n.fric_x (wet cells), fused path
+  double* fpy = nullptr;
+  // sources / wind
+  std::vector<swf::DevSrc> h_src;
+  std::vector<double> h_ht, h_hq;
+  swf::DevSrc* d_src = nullptr;
+  double* d_ht = nullptr;
+  double* d_hq = nullptr;
+  double* d_sig = nullptr;  // 2*nsrc: sigma at t_n, sigma at t_mid
+  std::vector<double> h_wt, h_wv;
+  double* d_wt = nullptr;
+  double* d_wv = nullptr;  // 2 per sample
+  // masks
+  int* d_interior = nullptr;
+  int* d_halo = nullptr;
+  unsigned char* d_bflag = nullptr;  // bit0 lagrangian-active, bit1 flux-active
+  unsigned char* d_tile_act = nullptr;
+  unsigned char* d_tile_same = nullptr;  // tile identical in both state buffers
+  double* d_part = nullptr;              // per-tile diagnostic partials (3 per tile)
+  // scalars
+  swf::StepScalars* d_sc = nullptr;
+  swf::StepScalars* h_sc = nullptr;  // pinned mirror
+  double h_t = 0.0;                  // host copy of t after the last sync
+  // stage path
+  swf::Scratch* scr = nullptr;
+  int mode = 0;  // 0 fused, 1 staged
+  // timing
+  bool timing = false;
+  cudaEvent_t ev[10] = {};
+  // CUDA graph of one fused step (captured lazily, invalidated on config change)
+  cudaGraphExec_t graph = nullptr;
+  double graph_dt_cap = -1.0;
+  // pinned staging for host-buffer steps
+  double* h_pin = nullptr;
+  size_t h_pin_cells = 0;
+  std::string err;
+};
+
+namespace swf {
+
+// stage path (swf_stage.cu)
+int stage_run(swf_ctx* c, int stage, double arg, double* tau_out);
+int stage_step(swf_ctx* c, double dt_cap, swf_step_info* info);
+int stage_download(swf_ctx* c, int which, double* out);
+void stage_free(swf_ctx* c);
+
+// fused path (swf_fused.cu)
+int fused_enqueue_step(swf_ctx* c, double dt_cap);
+int fused_enqueue_phase1(swf_ctx* c, double dt_cap);
+int fused_enqueue_phase2(swf_ctx* c, double dt_cap);
+int fused_enqueue_phase2(swf_ctx* c, double dt_cap, double global_speed);
+int launch_begin(swf_ctx* c, double dt_cap);  // sources/wind at t_n, reset counters
+int launch_mask(swf_ctx* c);                   // K1 block mask + tile flags
+int launch_tau(swf_ctx* c, double dt_cap);     // tau from speed_bits, then mid scalars
+int launch_mid(swf_ctx* c, double tau);        // mid scalars for a given tau
+void fill_block_counts(const swf_ctx* c, const StepScalars* sc, swf_step_info* info);
+int stage_volumes(swf_ctx* c, double* v3);
+void stage_clear_sources(swf_ctx* c);
+
+// shared helpers (swf_capi.cu)
+int set_err(swf_ctx* c, int code, const std::string& msg);
+int cuda_check(swf_ctx* c, cudaError_t e, const char* what);
+int check_device_error(swf_ctx* c);  // after a sync: maps err_key to status
+size_t local_cells(const swf_ctx* c);
+
+// per-cell source evaluation (sources.cpp:45-64, 66-75) on the device
+__device__ __forceinline__ double cell_source(const DevSrc* src, const double* sig, int nsrc,
+                                              int i, int jg, double& vx, double& vy) {
+  double s = 0.0;
+  for (int m = 0; m < nsrc; ++m) {
+    const DevSrc& d = src[m];
+    if (i >= d.i0 && i <= d.i1 && jg >= d.j0 && jg <= d.j1) {
+      s += sig[m];
+      vx = d.vx;
+      vy = d.vy;
+    }
+  }
+  return s;
+}
+
+__device__ __forceinline__ double cell_sigma_only(const DevSrc* src, const double* sig, int nsrc,
+                                                  int i, int jg) {
+  double s = 0.0;
+  for (int m = 0; m < nsrc; ++m) {
+    const DevSrc& d = src[m];
+    if (i >= d.i0 && i <= d.i1 && jg >= d.j0 && jg <= d.j1) s += sig[m];
+  }
+  return s;
+}
+
+}  // namespace swf

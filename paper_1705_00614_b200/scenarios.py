@@ -1,0 +1,211 @@
+"""Synthetic scenarios of BASELINE.json's configs (seed 1705), and small
+test cases.  SURVEY.md §8(d) defines them:
+
+  C1 dam_break_1d         512x64, h=1, flat bed, H=1 left of i=256, dry or 0.1 right
+  C2 circular_dam_break   2048^2, h=8, b=1e-3*x, 5 m column of radius 256 cells
+  C3 floodplain           16384^2, h=50, slope + 10 seeded cosines + two meandering
+                          channels, Manning field, ~35% wet, discharge ramp, drain,
+                          rain, wind, Coriolis, viscosity, open east edge
+  C5 floodplain           the same generator at 32768^2, h=25
+
+Every field is a function of physical coordinates evaluated on the cells of a
+`window` of the full grid, so crops (for the CPU oracle) and strips (for
+multi-GPU) see exactly the values the full grid has.  Arrays are generated
+with torch on the requested device (fast on the GPU for the 2^28-cell
+configs) and returned as float64 numpy arrays.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import List, Optional, Tuple
+
+import numpy as np
+
+from .types import (BoundaryConfig, CellRect, EdgeKind, FlowState, HydrographSample,
+                    PhysicalParams, SourceKind, SourceSpec, StepperOptions, Terrain,
+                    TimestepControl, Vec2, WindForcing, latitude_to_omega_z)
+
+SEED = 1705
+
+
+@dataclass
+class Scenario:
+    name: str
+    terrain: Terrain
+    params: PhysicalParams
+    control: TimestepControl
+    options: StepperOptions
+    state: FlowState
+    sources: List[SourceSpec] = field(default_factory=list)
+    wind: WindForcing = field(default_factory=WindForcing)
+    full_shape: Tuple[int, int] = (0, 0)
+    window: Tuple[int, int, int, int] = (0, 0, 0, 0)  # i0, j0, ni, nj
+
+    def cells(self) -> int:
+        return self.terrain.nx * self.terrain.ny
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def dam_break_1d(wet_right: bool = False, n_manning: float = 0.0, nx: int = 512,
+                 ny: int = 64) -> Scenario:
+    """C1: flat bed, reflective walls."""
+    n = nx * ny
+    b = np.zeros(n)
+    H = np.zeros((ny, nx))
+    H[:, : nx // 2] = 1.0
+    if wet_right:
+        H[:, nx // 2:] = 0.1
+    st = FlowState(nx, ny, 0.0, H.reshape(-1).copy(), np.zeros(n), np.zeros(n))
+    return Scenario("C1-dam-break" + ("-wet" if wet_right else "-dry"),
+                    Terrain(nx, ny, 1.0, 0.0, 0.0, b), PhysicalParams(n_manning=n_manning),
+                    TimestepControl(), StepperOptions(), st, full_shape=(nx, ny),
+                    window=(0, 0, nx, ny))
+
+
+def circular_dam_break(n: int = 2048, h: float = 8.0, radius_cells: int = 256,
+                       n_manning: float = 0.03, window=None, device: str = "cpu") -> Scenario:
+    """C2: sloped bed b = 1e-3 x, eta = b_center + 5 m inside the column."""
+    torch = _torch()
+    i0, j0, ni, nj = window if window else (0, 0, n, n)
+    x = (torch.arange(i0, i0 + ni, dtype=torch.float64, device=device) + 0.5) * h
+    y = (torch.arange(j0, j0 + nj, dtype=torch.float64, device=device) + 0.5) * h
+    X, Y = torch.meshgrid(x, y, indexing="xy")  # (nj, ni)
+    b = 1e-3 * X
+    c = (n * h) / 2.0
+    r = torch.sqrt((X - c) ** 2 + (Y - c) ** 2)
+    eta = 1e-3 * c + 5.0
+    H = torch.where(r < radius_cells * h, torch.clamp(eta - b, min=0.0), torch.zeros_like(b))
+    cells = ni * nj
+    st = FlowState(ni, nj, 0.0, H.reshape(-1).cpu().numpy().copy(), np.zeros(cells), np.zeros(cells))
+    return Scenario("C2-circular-dam-break", Terrain(ni, nj, h, i0 * h, j0 * h,
+                                                     b.reshape(-1).cpu().numpy().copy()),
+                    PhysicalParams(n_manning=n_manning), TimestepControl(), StepperOptions(), st,
+                    full_shape=(n, n), window=(i0, j0, ni, nj))
+
+
+def _cosines(seed: int, L: float):
+    rng = np.random.default_rng(seed)
+    terms = []
+    for _ in range(10):
+        lam = L * rng.uniform(1.0 / 16.0, 1.0 / 3.0)
+        ang = rng.uniform(0.0, math.pi)
+        k = 2.0 * math.pi / lam
+        terms.append((k * math.cos(ang), k * math.sin(ang), rng.uniform(0.0, 2.0 * math.pi)))
+    return terms
+
+
+def _floodplain_fields(X, Y, L: float, h: float, seed: int):
+    """Bed, channel mask and Manning field at physical coordinates X, Y."""
+    torch = _torch()
+    b = 5e-5 * (L - X)  # slope 5e-5, descending eastward
+    noise = torch.zeros_like(X)
+    for kx, ky, ph in _cosines(seed, L):
+        noise += 0.5 * torch.cos(kx * X + ky * Y + ph)  # 10 x 0.5 m = 5 m amplitude
+    b = b + noise
+    # main channel: 25 m deep, ~20 cells wide, meandering west -> east
+    yc = 0.5 * L + (L / 6.0) * torch.sin(2.0 * math.pi * X / (L / 3.0))
+    w1 = 10.0 * h
+    p1 = torch.clamp(1.0 - ((Y - yc) / w1) ** 2, min=0.0)
+    # secondary channel: 8 m deep, ~6 cells wide
+    yc2 = 0.25 * L + (L / 10.0) * torch.sin(2.0 * math.pi * X / (L / 5.0) + 1.0)
+    w2 = 3.0 * h
+    p2 = torch.clamp(1.0 - ((Y - yc2) / w2) ** 2, min=0.0)
+    b = b - 25.0 * p1 - 8.0 * p2
+    chan = (p1 > 0) | (p2 > 0)
+    nfield = torch.where(chan, torch.full_like(X, 0.025), torch.full_like(X, 0.04))
+    return b, noise, chan, nfield
+
+
+def _flood_offset(L: float, h: float, seed: int, wet_fraction: float = 0.35) -> float:
+    """Water-plane offset giving ~35% wet cells, from a fixed coarse sample of
+    the full-domain generator (so every crop uses the same plane)."""
+    torch = _torch()
+    m = 512
+    s = (torch.arange(m, dtype=torch.float64) + 0.5) * (L / m)
+    X, Y = torch.meshgrid(s, s, indexing="xy")
+    b, noise, chan, _ = _floodplain_fields(X, Y, L, h, seed)
+    rel = (b - 5e-5 * (L - X)).reshape(-1)
+    return float(torch.quantile(rel, wet_fraction))
+
+
+def floodplain(n: int = 16384, h: float = 50.0, window=None, device: str = "cpu",
+               seed: int = SEED) -> Scenario:
+    """C3 (n=16384, h=50) and C5 (n=32768, h=25): Volga-Akhtuba-like floodplain."""
+    torch = _torch()
+    L = n * h
+    i0, j0, ni, nj = window if window else (0, 0, n, n)
+    x = (torch.arange(i0, i0 + ni, dtype=torch.float64, device=device) + 0.5) * h
+    y = (torch.arange(j0, j0 + nj, dtype=torch.float64, device=device) + 0.5) * h
+    X, Y = torch.meshgrid(x, y, indexing="xy")
+    b, noise, chan, nfield = _floodplain_fields(X, Y, L, h, seed)
+    off = _flood_offset(L, h, seed)
+    eta0 = 5e-5 * (L - X) + off
+    H = torch.clamp(eta0 - b, min=0.0)
+    H = torch.where(H > 1e-6, H, torch.zeros_like(H))
+    cells = ni * nj
+    to_np = lambda t: t.reshape(-1).cpu().numpy().copy()
+    terrain = Terrain(ni, nj, h, i0 * h, j0 * h, to_np(b))
+    params = PhysicalParams(n_manning=0.04, n_field=to_np(nfield), nu=1.0,
+                            omega_z=latitude_to_omega_z(48.7))
+    opts = StepperOptions(boundaries=BoundaryConfig(EdgeKind.Reflective, EdgeKind.Open,
+                                                    EdgeKind.Reflective, EdgeKind.Reflective))
+    st = FlowState(ni, nj, 0.0, to_np(H), np.zeros(cells), np.zeros(cells))
+    # sources in FULL-grid cells, clipped to the window
+    jc = int((0.5 * L) / h)
+    jd = int((0.5 * L + (L / 6.0) * math.sin(2.0 * math.pi * (L - 3 * h) / (L / 3.0))) / h)
+    full_specs = [
+        SourceSpec(SourceKind.Discharge, "upstream", CellRect(1, jc - 5, 4, jc + 5),
+                   [HydrographSample(0.0, 0.0), HydrographSample(3600.0, 1.0e5)], 0.0,
+                   Vec2(1.0, 0.0)),
+        SourceSpec(SourceKind.Discharge, "drain", CellRect(n - 5, jd - 5, n - 2, jd + 5),
+                   [HydrographSample(0.0, -3.0e4)], 0.0, Vec2(0.0, 0.0)),
+        SourceSpec(SourceKind.Rain, "rain", CellRect(n // 8, (5 * n) // 8, n // 4, (3 * n) // 4),
+                   [], 1.0e-6, Vec2(0.0, 0.0)),
+    ]
+    specs = []
+    for s in full_specs:
+        a0, b0 = max(s.cells.i0, i0), max(s.cells.j0, j0)
+        a1, b1 = min(s.cells.i1, i0 + ni - 1), min(s.cells.j1, j0 + nj - 1)
+        if a0 <= a1 and b0 <= b1:
+            specs.append(SourceSpec(s.kind, s.name, CellRect(a0 - i0, b0 - j0, a1 - i0, b1 - j0),
+                                    list(s.hydrograph), s.rate, s.source_velocity))
+    name = "C3-floodplain" if n == 16384 else ("C5-floodplain" if n == 32768 else f"floodplain-{n}")
+    return Scenario(name, terrain, params, TimestepControl(), opts, st, specs,
+                    WindForcing.constant(5.0, 2.0), full_shape=(n, n), window=(i0, j0, ni, nj))
+
+
+def lake_at_rest(n: int = 128, h: float = 10.0, level: float = 0.0, seed: int = SEED) -> Scenario:
+    """SPEC.md:540 acceptance 1: still lake over a seeded bumpy bed."""
+    torch = _torch()
+    L = n * h
+    s = (torch.arange(n, dtype=torch.float64) + 0.5) * h
+    X, Y = torch.meshgrid(s, s, indexing="xy")
+    b = torch.zeros_like(X)
+    for kx, ky, ph in _cosines(seed, L):
+        b += 0.5 * torch.cos(kx * X + ky * Y + ph)
+    H = torch.clamp(level - b, min=0.0)
+    cells = n * n
+    st = FlowState(n, n, 0.0, H.reshape(-1).numpy().copy(), np.zeros(cells), np.zeros(cells))
+    return Scenario("lake-at-rest", Terrain(n, n, h, 0.0, 0.0, b.reshape(-1).numpy().copy()),
+                    PhysicalParams(), TimestepControl(), StepperOptions(), st,
+                    full_shape=(n, n), window=(0, 0, n, n))
+
+
+def build(config: str, device: str = "cpu", window=None) -> Scenario:
+    """Scenario for a BASELINE.json config id: C1, C1w, C2, C3, C5."""
+    if config in ("C1", "C1-dry"):
+        return dam_break_1d(False, 0.0)
+    if config in ("C1w", "C1-wet"):
+        return dam_break_1d(True, 0.02)
+    if config == "C2":
+        return circular_dam_break(window=window, device=device)
+    if config == "C3":
+        return floodplain(16384, 50.0, window=window, device=device)
+    if config == "C5":
+        return floodplain(32768, 25.0, window=window, device=device)
+    raise ValueError(config)
