@@ -16,6 +16,7 @@ final_update(state, tau) writes the result back into `state`.
 """
 from __future__ import annotations
 
+import copy
 import ctypes as C
 from typing import List, Optional, Tuple
 
@@ -73,7 +74,7 @@ class CsphTvdStepper:
 
     def __init__(self, terrain: Terrain, params: PhysicalParams, control: TimestepControl,
                  options: Optional[StepperOptions] = None, *, mode: int = 0):
-        options = options if options is not None else StepperOptions()
+        options = copy.deepcopy(options) if options is not None else StepperOptions()
         self._terrain = terrain
         self._params = params
         self._control = TimestepControl(control.courant, control.dt_max, control.dt_min)

@@ -1,0 +1,283 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle and
+the golden vectors generated from the compiled reference.  The bar is
+bit-exact equality of H, HUx, HUy, t and tau (fp64, no tolerance), which
+also makes the wet/dry mask bit-exact."""
+import ctypes as C
+import hashlib
+
+import numpy as np
+import pytest
+
+from helpers import (assert_bitwise, assert_state_bitwise, digest, golden, golden_factories, make)
+from paper_1705_00614_b200 import scenarios as S
+from paper_1705_00614_b200.types import HydrographSample as HS
+
+pytestmark = pytest.mark.gpu
+G = golden()
+
+
+@pytest.fixture(scope="module")
+def gpu_cls():
+    from paper_1705_00614_b200 import CsphTvdStepper
+    return CsphTvdStepper
+
+
+# ---------------------------------------------------------------- device KATs
+
+def test_device_cbrt_matches_glibc(oracle_built):
+    from paper_1705_00614_b200.stepper import cbrt_device
+    rng = np.random.default_rng(1705)
+    xs = np.concatenate([rng.uniform(0, 1e3, 50000), 2.0 ** rng.uniform(-60, 20, 50000),
+                         -rng.uniform(0, 10, 1000)])
+    ys = cbrt_device(xs)
+    assert hashlib.sha256(ys.tobytes()).hexdigest() == G["kat"]["cbrt_sha256"]
+    lib = oracle_built.load("orc")
+    more = np.concatenate([2.0 ** rng.uniform(-1074, 1023, 20000), rng.uniform(1e-7, 30, 20000),
+                           [0.0, -0.0, 5e-324, 1e-300, 1.0, 8.0, 27.0, 1e308]])
+    got = cbrt_device(more)
+    exp = np.array([lib.orc_cbrt(float(x)) for x in more])
+    assert_bitwise(got, exp, "cbrt")
+
+
+def test_device_hll_matches_oracle(oracle_built):
+    from paper_1705_00614_b200.stepper import hll_face_flux_device
+    rng = np.random.default_rng(7)
+    n = 40000
+    x = np.column_stack([rng.uniform(0, 5, n), rng.normal(0, 3, n), rng.normal(0, 1, n),
+                         rng.uniform(0, 5, n), rng.normal(0, 3, n), rng.normal(0, 1, n)])
+    x[: n // 4, 0] = 0.0  # dry left
+    x[n // 4: n // 2, 3] = 0.0  # dry right
+    x[n // 2: n // 2 + 100, [0, 3]] = 0.0  # dry/dry
+    got = hll_face_flux_device(x, 9.81)
+    lib = oracle_built.load("orc")
+    o3 = (C.c_double * 3)()
+    exp = np.empty_like(got)
+    for k in range(n):
+        lib.orc_hll_face_flux((C.c_double * 6)(*x[k]), 9.81, o3)
+        exp[k] = o3[:]
+    assert_bitwise(got, exp, "hll")
+    assert list(hll_face_flux_device(np.array([[1.0, 0, 0, 0, 0, 0]]), 9.81)[0]) == G["kat"]["hll_dam_break"]
+
+
+def test_device_friction_known_answer():
+    from paper_1705_00614_b200.stepper import bottom_friction_device
+    f = bottom_friction_device(np.array([[1.0, 0.0]]), np.array([1.0]), 9.81, 0.02)
+    assert list(f[0]) == G["kat"]["friction"]
+
+
+# ------------------------------------------------------- full-step golden runs
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("name", list(G["cases"].keys()))
+def test_golden_case(gpu_cls, name, mode):
+    case = G["cases"][name]
+    sc = golden_factories()[name]()
+    s = make(gpu_cls, sc, mode=mode)
+    st = sc.state.copy()
+    s.upload(st)
+    info = None
+    for _ in range(case["steps"]):
+        info = s.step_resident(case["dt_cap"])
+    s.download(st)
+    assert st.t.hex() == case["t"], (st.t, float.fromhex(case["t"]))
+    assert digest(st) == case["sha256"]
+    li = case["last_info"]
+    assert info.tau.hex() == li["tau"]
+    assert info.lagrangian_blocks == li["lagrangian_blocks"]
+    assert info.flux_blocks == li["flux_blocks"]
+    assert info.total_blocks == li["total_blocks"]
+    assert info.active_fraction.hex() == li["active_fraction"]
+    if mode == 1:  # the stage path sums diagnostics in the reference's block order
+        assert info.clamp_deficit_volume.hex() == li["clamp_deficit_volume"]
+        assert info.source_volume.hex() == li["source_volume"]
+        assert info.boundary_outflow_volume.hex() == li["boundary_outflow_volume"]
+    else:  # the fused path uses a deterministic tile-order reduction
+        for k in ("clamp_deficit_volume", "source_volume", "boundary_outflow_volume"):
+            ref = float.fromhex(li[k])
+            assert getattr(info, k) == pytest.approx(ref, rel=1e-12, abs=1e-9)
+
+
+def test_flood64_arrays_and_host_step(gpu_cls):
+    """The drop-in host-buffer step() against the golden arrays."""
+    z = np.load(f"{__file__.rsplit('/', 1)[0]}/golden/flood64_all_physics.npz")
+    sc = S.floodplain(64, 50.0)
+    s = make(gpu_cls, sc)
+    st = sc.state.copy()
+    for _ in range(G["cases"]["flood64_all_physics"]["steps"]):
+        s.step(st)
+    assert_bitwise(st.H, z["H"], "H")
+    assert_bitwise(st.HUx, z["HUx"], "HUx")
+    assert_bitwise(st.HUy, z["HUy"], "HUy")
+    assert st.t == float(z["t"][0])
+
+
+# ------------------------------------------------------------ stage API parity
+
+@pytest.mark.parametrize("skip", [True, False])
+def test_stagewise_against_oracle(gpu_cls, oracle_built, skip):
+    sc = S.floodplain(96, 50.0)
+    sc.options.skip_dry_blocks = skip
+    a = make(oracle_built.OracleStepper, sc, kind="orc")
+    b = make(gpu_cls, sc)
+    sa, sb = sc.state.copy(), sc.state.copy()
+    names = ["fn_fx", "fn_fy", "fn_fric_x", "fn_fric_y", "fn_sigma", "fm_fx", "fm_fy",
+             "fm_fric_x", "fm_fric_y", "fm_sigma", "half_H", "half_HUx", "half_HUy", "Ht",
+             "HVtx", "HVty", "drx", "dry", "Fh", "Fvx", "Fvy", "sigma", "src_vx", "src_vy"]
+    for step in range(5):
+        for o, s in ((a, sa), (b, sb)):
+            o.begin_step(s)
+            o.compute_forces(s)
+        ta, tb = a.compute_dt(sa), b.compute_dt(sb)
+        assert ta == tb
+        for o, s in ((a, sa), (b, sb)):
+            o.predictor(s, ta)
+            o.mid_forces(s, ta)
+            o.corrector(s, ta)
+            o.flux(s, ta)
+        for nm in names:
+            assert_bitwise(b.scratch(nm), a.scratch(nm), f"step {step} {nm}")
+        ma, mb = a.mask(), b.mask()
+        assert np.array_equal(ma.interior_wet, mb.interior_wet)
+        assert np.array_equal(ma.halo_wet, mb.halo_wet)
+        a.final_update(sa, ta)
+        b.final_update(sb, tb)
+        assert_state_bitwise(sb, sa, f"step {step}")
+        assert b._volumes() == a._volumes()
+
+
+# ----------------------------------------------------------- properties
+
+def test_run_equals_repeated_step(gpu_cls):
+    sc = S.floodplain(200, 50.0)
+    a, b = make(gpu_cls, sc), make(gpu_cls, sc)
+    sa, sb = sc.state.copy(), sc.state.copy()
+    a.upload(sa)
+    b.upload(sb)
+    done, _ = a.run(23)
+    assert done == 23
+    for _ in range(23):
+        b.step_resident()
+    a.download(sa)
+    b.download(sb)
+    assert_state_bitwise(sa, sb, "run vs step")
+
+
+@pytest.mark.parametrize("bs", [7, 16, 32])
+def test_skip_and_block_size_equivalence(gpu_cls, bs):
+    """skipping on vs off, any block size -> identical bits."""
+    sc = S.circular_dam_break(512, 8.0, 64)
+    ref = make(gpu_cls, sc)
+    st_ref = sc.state.copy()
+    ref.options().skip_dry_blocks = False
+    ref.upload(st_ref)
+    ref.run(40)
+    ref.download(st_ref)
+    sc.options.block_size = bs
+    s = make(gpu_cls, sc)
+    st = sc.state.copy()
+    s.upload(st)
+    s.run(40)
+    s.download(st)
+    assert_state_bitwise(st, st_ref, f"B={bs}")
+
+
+def test_medium_floodplain_vs_oracle(gpu_cls, oracle_built):
+    sc = S.floodplain(16384, 50.0, window=(7000, 7600, 300, 260))  # a crop of C3
+    a = make(oracle_built.OracleStepper, sc, kind="orc")
+    b = make(gpu_cls, sc)
+    sa, sb = sc.state.copy(), sc.state.copy()
+    for _ in range(8):
+        ia, ib = a.step(sa), b.step(sb)
+        assert ia.tau == ib.tau
+    assert_state_bitwise(sb, sa, "C3 crop")
+
+
+def test_lake_at_rest_is_fixed_point(gpu_cls):
+    sc = S.lake_at_rest(128)
+    s = make(gpu_cls, sc)
+    st = sc.state.copy()
+    s.upload(st)
+    s.run(1000)
+    s.download(st)
+    u = np.where(st.H > 1e-6, np.hypot(st.HUx, st.HUy) / np.maximum(st.H, 1e-300), 0.0)
+    assert u.max() <= 1e-10
+    assert np.abs(st.H - sc.state.H).max() <= 1e-12
+
+
+def test_mass_conservation_closed_basin(gpu_cls):
+    sc = S.circular_dam_break(1024, 8.0, 128, n_manning=0.03)
+    s = make(gpu_cls, sc)
+    st = sc.state.copy()
+    v0 = st.H.sum()
+    s.upload(st)
+    s.run(300)
+    s.download(st)
+    assert abs(st.H.sum() - v0) / v0 < 1e-12
+
+
+# ------------------------------------------------------------- error paths
+
+def _cfl_case():
+    """A drain that empties a moving cell to ~1 mm within the half step makes
+    u_1/2 = q/H_1/2 explode, so |dr| >= h/2 (stepper.cpp:378-380)."""
+    from paper_1705_00614_b200.types import CellRect, HydrographSample, SourceKind, SourceSpec
+    sc = S.dam_break_1d(True, 0.0, nx=64, ny=16)
+    sc.state.H[:] = 1.0
+    sc.state.HUx[:] = 1.0
+    sig = -2.0 * (1.0 - 1e-3) / 0.1
+    sc.sources = [SourceSpec(SourceKind.Discharge, "drain", CellRect(40, 5, 40, 5),
+                             [HydrographSample(0.0, sig)])]
+    return sc
+
+
+def test_cfl_abort_leaves_state_untouched(gpu_cls, oracle_built):
+    from paper_1705_00614_b200 import NumericalError
+    sc = _cfl_case()
+    for mode in (0, 1):
+        s = make(gpu_cls, sc, mode=mode)
+        o = make(oracle_built.OracleStepper, sc, kind="orc")
+        st, so = sc.state.copy(), sc.state.copy()
+        with pytest.raises(NumericalError) as eo:
+            o.step(so, 0.1)
+        before = st.copy()
+        with pytest.raises(NumericalError) as eg:
+            s.step(st, 0.1)
+        assert str(eg.value) == str(eo.value)
+        assert "particle displacement reached h/2 at cell (40,5)" in str(eg.value)
+        assert_state_bitwise(st, before, "state changed on abort")
+
+
+def test_dt_floor_abort(gpu_cls):
+    from paper_1705_00614_b200 import NumericalError
+    sc = S.dam_break_1d(False, 0.0, nx=64, ny=8)
+    sc.control.dt_min = 5.0
+    sc.control.dt_max = 10.0
+    s = make(gpu_cls, sc)
+    st = sc.state.copy()
+    before = st.copy()
+    with pytest.raises(NumericalError, match="fell below the abort floor"):
+        s.step(st)
+    assert_state_bitwise(st, before)
+
+
+def test_run_stops_at_failure(gpu_cls):
+    from paper_1705_00614_b200 import NumericalError
+    sc = _cfl_case()
+    sc.sources[0].hydrograph = [HS(0.0, 0.0), HS(2.0, 0.0), HS(2.05, -19.98)]
+    a = make(gpu_cls, sc)
+    st = sc.state.copy()
+    n_ok = 0
+    for _ in range(200):
+        try:
+            a.step(st, 0.1)
+            n_ok += 1
+        except NumericalError:
+            break
+    assert 0 < n_ok < 200
+    b = make(gpu_cls, sc)
+    sb = sc.state.copy()
+    b.upload(sb)
+    with pytest.raises(NumericalError):
+        b.run(200, 0.1)
+    b.download(sb)
+    assert_state_bitwise(sb, st, "run() state after failure")
