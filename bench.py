@@ -1,0 +1,338 @@
+#!/usr/bin/env python
+"""Benchmark of the CSPH-TVD time step (BASELINE.json metric: cell-updates/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--config C3|C2|C5|C1] [--no-skip]
+
+N=1 runs configs[2] (C3: 16384^2 synthetic Volga-Akhtuba-like floodplain,
+all physics) — the largest configuration BASELINE.json names that fits one
+B200 — on one context; N>1 (torchrun, one rank per GPU) splits it into
+B-aligned row strips with an NCCL halo exchange and an exact allreduce-max of
+the CFL speed each step (multigpu.py).  One JSON line is printed by rank 0.
+
+--impl reference times the reference's own CPU implementation (the compiled
+reference in oracle/_ref, all host threads; the C restatement oracle/liborc.so
+as a single-thread port when the reference was not compiled) on a bounded
+crop of the same workload.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+GB = 1e9
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=30)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--config", default="C3")
+    p.add_argument("--no-skip", action="store_true", help="disable dry-block skipping")
+    p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=15.0)
+    return p.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), \
+        int(os.environ.get("LOCAL_RANK", "0"))
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = [r for r in self.rows if len(r) >= 8]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        sm = sorted(float(r[0]) for r in rows if r[0].replace(".", "").isdigit())
+        mx = max(float(r[1]) for r in rows if r[1].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower() == "active"})
+        pw = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(pw) if pw else None}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(kernel="k_step"):
+    """DRAM bytes per launch of the kernel from the committed ncu --set full
+    capture summary (profiles/), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        k = d["kernels"][kernel]
+        return {"bytes_per_launch": k["dram_bytes"], "source": d.get("source", p),
+                "cells_per_launch": k.get("cells")}
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# reference CPU arm (and cpu_baseline)
+# ---------------------------------------------------------------------------
+def cpu_reference(config, seconds, threads=None):
+    """Time the reference's CPU implementation on a bounded crop of the
+    workload; returns (mcells_per_s, cores, kind, sample description)."""
+    from oracle import pyorc
+    from paper_1705_00614_b200 import scenarios as S
+    kind = "reference" if pyorc.available("ref") else "port"
+    if not pyorc.available(kind if kind == "ref" else "orc"):
+        try:
+            pyorc.build(ref=False)
+        except Exception:
+            pass
+    cores = threads or os.cpu_count() or 1
+    if kind != "reference":
+        cores = 1
+    n_full = {"C3": 16384, "C5": 32768}.get(config, 0)
+    if n_full:
+        # 8 crops of 1024^2 on the diagonal: the wet/dry mix of the full domain
+        # (~35% wet) is spatially correlated, so one crop is not representative
+        crop = 1024
+        wins = [(k * (n_full // 8) + (n_full // 16) - crop // 2,) * 2 + (crop, crop) for k in range(8)]
+        scs = [S.build(config, window=w) for w in wins]
+    else:
+        scs = [S.build(config)]
+    cell_updates, el_total, steps_total = 0, 0.0, 0
+    for sc in scs:
+        sc.options.workers = cores
+        o = pyorc.OracleStepper(sc.terrain, sc.params, sc.control, sc.options,
+                                kind="ref" if kind == "reference" else "orc")
+        if sc.wind.any():
+            o.set_wind(sc.wind)
+        if sc.sources:
+            o.set_sources(sc.sources)
+        o.upload(sc.state)
+        o.run(1)  # warm-up
+        steps, t0 = 0, time.perf_counter()
+        while True:
+            o.run(1)
+            steps += 1
+            el = time.perf_counter() - t0
+            if el >= seconds / len(scs) or steps >= 500:
+                break
+        cell_updates += sc.cells() * steps
+        el_total += el
+        steps_total += steps
+        o.close()
+    v = cell_updates / el_total / 1e6
+    what = (f"8 diagonal 1024x1024 crops of {config}" if n_full else f"{config} full grid")
+    sample = (f"{what} (same generator), {steps_total} crop-steps after 1 warm-up each, "
+              f"{el_total:.1f} s, {cores} thread(s)")
+    return v, cores, ("reference" if kind == "reference" else "port"), sample
+
+
+def reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    per_step = []
+    cores = kind = sample = None
+    for _ in range(args.warmup):
+        cpu_reference(args.config, seconds=min(3.0, args.cpu_seconds / 4))
+    for _ in range(args.steps):
+        v, cores, kind, sample = cpu_reference(args.config, seconds=max(2.0, args.cpu_seconds / args.steps))
+        per_step.append(v)
+    v = sum(per_step) / len(per_step)
+    line = {"metric": "cell-updates/sec (Mcells/s)", "value": round(v, 3), "unit": "Mcells/s",
+            "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config} (bounded crop on host CPU)", "grid": args.config},
+            "cpu_baseline": {"value": round(v, 3), "unit": "Mcells/s", "cores": cores,
+                             "kind": kind, "sample": sample},
+            "e2e": {"value": round(v, 3), "unit": "Mcells/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+def b200_single(args):
+    import numpy as np
+    import torch
+    from paper_1705_00614_b200 import CsphTvdStepper, scenarios as S
+
+    torch.cuda.set_device(0)
+    t_gen = time.perf_counter()
+    sc = S.build(args.config, device="cuda")
+    if args.no_skip:
+        sc.options.skip_dry_blocks = False
+    gen_s = time.perf_counter() - t_gen
+    N = sc.cells()
+    st = CsphTvdStepper(sc.terrain, sc.params, sc.control, sc.options)
+    if sc.wind.any():
+        st.set_wind(sc.wind)
+    if sc.sources:
+        st.set_sources(sc.sources)
+    st.upload(sc.state)
+    stream = torch.cuda.ExternalStream(st.stream_handle())
+
+    # warm-up (CUDA-graph replay path)
+    st.run(args.warmup)
+    info = st.step_resident()  # one synchronised step: StepInfo with block counts
+    K = args.steps
+    st.set_timing(K)
+    clocks = ClockSampler(0)
+    clocks.start()
+    time.sleep(0.3)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    done, last = st.run(K)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    assert done == K
+    tk = st.timing_read(K)  # (K, 8) seconds per bucket
+    st.set_timing(0)
+    t_step_kernel = float(tk[:, 6].mean())
+    t_forces_kernel = float(tk[:, 1].mean())
+
+    # active cells (flux-active blocks at B=16)
+    bs = sc.options.block_size
+    n_act = min(N, last.flux_blocks * bs * bs) if sc.options.skip_dry_blocks else N
+    has_nf = sc.params.n_field is not None
+    per_act = 56 + (8 if has_nf else 0)
+    alg_bytes = per_act * n_act + 8 * (N - n_act)
+    hbm_peak, peak_src = peaks()
+    achieved = alg_bytes / t_step_kernel / GB
+    traffic = ncu_traffic("k_step")
+    value = N * K / (ms * 1e-3) / 1e6
+
+    # ---- end to end through the drop-in host-buffer step() ----
+    E = max(1, args.e2e_steps)
+    pin = lambda a: torch.from_numpy(a).pin_memory().numpy()
+    from paper_1705_00614_b200.types import FlowState
+    hs = FlowState(sc.terrain.nx, sc.terrain.ny, 0.0, pin(sc.state.H), pin(sc.state.HUx),
+                   pin(sc.state.HUy))
+    st.download(hs)  # continue from the current device state
+    st.step(hs)  # warm-up of the host path
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(E):
+        st.step(hs)
+    e2e_s = time.perf_counter() - t0
+    e2e_value = N * E / e2e_s / 1e6
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        try:
+            v, cores, kind, sample = cpu_reference(args.config, args.cpu_seconds)
+            cpu = {"value": round(v, 3), "unit": "Mcells/s", "cores": cores, "kind": kind,
+                   "sample": sample}
+        except Exception as e:  # reported, not fatal
+            cpu = {"value": None, "unit": "Mcells/s", "cores": None, "kind": None,
+                   "sample": f"unavailable: {e}"}
+
+    line = {
+        "metric": "cell-updates/sec (Mcells/s)", "value": round(value, 3), "unit": "Mcells/s",
+        "n_gpus": 1, "steps": K, "warmup": args.warmup, "ms_per_step": round(ms / K, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator, scenarios.py)",
+        "config": {"workload": f"{sc.name} {sc.terrain.nx}x{sc.terrain.ny} h={sc.terrain.h} m, all "
+                               "physics (Manning field, wind, Coriolis, viscosity, 3 sources, open east edge)",
+                   "cells": N, "active_fraction": round(last.active_fraction, 4),
+                   "skip_dry_blocks": bool(sc.options.skip_dry_blocks),
+                   "parallelism": "single GPU, fused tile kernels",
+                   "l2": "inputs larger than L2 (2 GiB per field vs 126 MB L2)",
+                   "parity": "bit-exact vs the reference CPU path (tests/test_gpu_parity.py)",
+                   "generation_s": round(gen_s, 1)},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
+                     "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
+                     "traffic": traffic["bytes_per_launch"] if traffic else None,
+                     "kernel": "k_step (fused K4..K8)",
+                     "algorithmic_bytes_per_launch": alg_bytes,
+                     "bytes_per_active_cell": per_act, "active_cells": n_act,
+                     "kernel_ms": round(t_step_kernel * 1e3, 4),
+                     "forces_kernel_ms": round(t_forces_kernel * 1e3, 4),
+                     "kernel_share_of_step": round(t_step_kernel / (ms * 1e-3 / K), 4),
+                     "peak_source": peak_src,
+                     "step_frac_of_hbm": round(alg_bytes / (ms * 1e-3 / K) / GB / hbm_peak, 4)},
+        "e2e": {"value": round(e2e_value, 3), "unit": "Mcells/s",
+                "h2d_bytes_per_step": 3 * 8 * N, "d2h_bytes_per_step": 3 * 8 * N,
+                "how": "CsphTvdStepper.step(FlowState) on pinned host buffers: upload H,HUx,HUy, "
+                       "one fused step, download; host-timed, synchronised"},
+        "gpu_launches": 7 * K,
+        "clocks": clk,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def b200_multi(args):
+    from paper_1705_00614_b200 import multigpu
+    line = multigpu.bench_strips(args)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        reference_arm(args)
+        return
+    if world > 1 or args.gpus > 1:
+        b200_multi(args)
+    else:
+        b200_single(args)
+
+
+if __name__ == "__main__":
+    main()

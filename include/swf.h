@@ -167,8 +167,15 @@ int swf_run(swf_ctx* ctx, int n, double dt_cap, int* done,
             swf_step_info* last);
 /* Synchronise the context's stream and report a pending device error. */
 int swf_sync(swf_ctx* ctx);
-/* Enable per-stage device timing in swf_step_info.timings (adds events). */
-int swf_set_timing(swf_ctx* ctx, int enabled);
+/* Device timing with CUDA events on the context's stream.  slots == 0: off;
+ * 1: swf_step_info.timings of the last step; > 1: a ring of `slots` per-step
+ * event sets readable with swf_timing_read (swf_run then launches directly
+ * instead of replaying its CUDA graph).  Fused-path buckets: mask = begin +
+ * K1, forces = K2+K3 kernel, dt = tau kernel, flux = fused K4..K8 kernel,
+ * finalize = diagnostics/commit; predictor/mid_forces/corrector are 0. */
+int swf_set_timing(swf_ctx* ctx, int slots);
+/* Per-step bucket seconds of the last nsteps fused steps: out[nsteps*8]. */
+int swf_timing_read(swf_ctx* ctx, int nsteps, double* out);
 /* The CUDA stream (cudaStream_t) of the context, for interop. */
 void* swf_stream(swf_ctx* ctx);
 /* Execution path of swf_step / swf_run: 0 = fused tile kernels (default),

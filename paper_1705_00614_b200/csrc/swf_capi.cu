@@ -108,14 +108,12 @@ int validate_control(swf_ctx* c, const swf_control* k) {
   return SWF_OK;
 }
 
-int validate_setup(const swf_terrain* T, const swf_params* P) {
-  if (!T || !P) return set_err(nullptr, SWF_ECONFIG, "null argument");
+int validate_setup(const swf_terrain* T, const swf_params* P, size_t n) {
   if (T->nx < 1 || T->ny < 1) return set_err(nullptr, SWF_ECONFIG, "terrain: nx and ny must be >= 1");
   if (!(T->h > 0.0)) return set_err(nullptr, SWF_ECONFIG, "terrain: cell size must be positive");
   if (!T->b) return set_err(nullptr, SWF_ECONFIG, "terrain: bed array size mismatch");
   if ((long long)T->nx * T->ny > 2147483647LL)
     return set_err(nullptr, SWF_ECONFIG, "terrain: more than 2^31-1 cells");
-  size_t n = (size_t)T->nx * T->ny;
   for (size_t k = 0; k < n; ++k)
     if (!std::isfinite(T->b[k]))
       return set_err(nullptr, SWF_ECONFIG,
@@ -186,13 +184,18 @@ void apply_control(swf_ctx* c, const swf_control* k) {
 int create_impl(const swf_terrain* T, const swf_params* P, const swf_control* K,
                 const swf_options* O, int j0, int j1, int device, swf_ctx** out) {
   *out = nullptr;
-  int rc = validate_setup(T, P);
+  if (!T || !P || !K || !O) return set_err(nullptr, SWF_ECONFIG, "null argument");
+  if (T->ny >= 1 && (j0 < 0 || j1 > T->ny || j0 >= j1))
+    return set_err(nullptr, SWF_ECONFIG, "strip rows out of range");
+  // host arrays cover the local window: global rows [j0 - glo, j1 + ghi)
+  int glo = j0 > 0 ? SWF_HALO : 0, ghi = j1 < T->ny ? SWF_HALO : 0;
+  if (j0 - glo < 0) glo = j0;
+  if (j1 + ghi > T->ny) ghi = T->ny - j1;
+  int rc = validate_setup(T, P, (size_t)(T->nx > 0 ? T->nx : 0) * (size_t)((j1 - j0) + glo + ghi));
   if (rc) return rc;
-  if (!K || !O) return set_err(nullptr, SWF_ECONFIG, "null argument");
   rc = validate_control(nullptr, K);
   if (rc) return rc;
   if (O->block_size < 1) return set_err(nullptr, SWF_ECONFIG, "stepper: block size must be >= 1");
-  if (j0 < 0 || j1 > T->ny || j0 >= j1) return set_err(nullptr, SWF_ECONFIG, "strip rows out of range");
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
   if (e != cudaSuccess || ndev == 0)
@@ -213,9 +216,6 @@ int create_impl(const swf_terrain* T, const swf_params* P, const swf_control* K,
   Geo& G = c->geo;
   G.nx = T->nx;
   G.ny = T->ny;
-  int glo = j0 > 0 ? SWF_HALO : 0, ghi = j1 < T->ny ? SWF_HALO : 0;
-  if (j0 - glo < 0) glo = j0;
-  if (j1 + ghi > T->ny) ghi = T->ny - j1;
   G.jg0 = j0 - glo;
   G.rows = (j1 - j0) + glo + ghi;
   G.r0 = glo;
@@ -243,14 +243,14 @@ int create_impl(const swf_terrain* T, const swf_params* P, const swf_control* K,
   }
   size_t n = local_cells(c);
   size_t bytes = n * sizeof(double);
-  const double* bsrc = T->b + (size_t)G.jg0 * G.nx;
+  const double* bsrc = T->b;  // window rows [jg0, jg0 + rows)
   e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaMalloc(&c->b, bytes);
   if (e == cudaSuccess) e = cudaMemcpy(c->b, bsrc, bytes, cudaMemcpyHostToDevice);
   if (e == cudaSuccess && P->n_field) {
     e = cudaMalloc(&c->nf, bytes);
     if (e == cudaSuccess)
-      e = cudaMemcpy(c->nf, P->n_field + (size_t)G.jg0 * G.nx, bytes, cudaMemcpyHostToDevice);
+      e = cudaMemcpy(c->nf, P->n_field, bytes, cudaMemcpyHostToDevice);
   }
   for (int s = 0; s < 2 && e == cudaSuccess; ++s) {
     e = cudaMalloc(&c->H[s], bytes);
@@ -314,8 +314,10 @@ void fill_fused_info(swf_ctx* c, swf_step_info* info) {
     float ms;
     // buckets: mask (begin+K1), forces (K2), dt (K3 tail), flux (K4..K8 fused), finalize
     int map[5][2] = {{0, 0}, {1, 1}, {2, 2}, {3, 6}, {4, 7}};
+    const cudaEvent_t* E = c->ev;
+    if (c->tslots > 0 && c->tstep > 0) E = &c->tev[(size_t)((c->tstep - 1) % c->tslots) * 6];
     for (auto& m : map) {
-      if (cudaEventElapsedTime(&ms, c->ev[m[0]], c->ev[m[0] + 1]) == cudaSuccess)
+      if (cudaEventElapsedTime(&ms, E[m[0]], E[m[0] + 1]) == cudaSuccess)
         info->timings[m[1]] = ms * 1e-3;
     }
   }
@@ -364,6 +366,7 @@ void swf_destroy(swf_ctx* c) {
   if (c->h_sc) cudaFreeHost(c->h_sc);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->tev) cudaEventDestroy(e);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -488,7 +491,7 @@ int swf_get_options(const swf_ctx* c, swf_options* o) {
 int swf_upload_state(swf_ctx* c, const double* H, const double* HUx, const double* HUy, double t) {
   cudaSetDevice(c->device);
   size_t n = local_cells(c), bytes = n * sizeof(double);
-  size_t off = (size_t)c->geo.jg0 * c->geo.nx;  // strips: rows of a global array
+  size_t off = 0;  // host arrays cover the local window
   cudaError_t e = cudaMemcpyAsync(c->H[c->cur], H + off, bytes, cudaMemcpyHostToDevice, c->stream);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(c->HUx[c->cur], HUx + off, bytes, cudaMemcpyHostToDevice, c->stream);
@@ -507,7 +510,7 @@ int swf_download_state(swf_ctx* c, double* H, double* HUx, double* HUy, double* 
   cudaSetDevice(c->device);
   const Geo& G = c->geo;
   size_t off = (size_t)G.r0 * G.nx, n = (size_t)(G.r1 - G.r0) * G.nx, bytes = n * sizeof(double);
-  size_t hoff = (size_t)(G.jg0 + G.r0) * G.nx;  // owned rows into a global-shaped array
+  size_t hoff = off;  // owned rows at their window position
   cudaError_t e = cudaMemcpyAsync(H + hoff, c->H[c->cur] + off, bytes, cudaMemcpyDeviceToHost, c->stream);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(HUx + hoff, c->HUx[c->cur] + off, bytes, cudaMemcpyDeviceToHost, c->stream);
@@ -527,6 +530,7 @@ int swf_device_state(swf_ctx* c, double** H, double** HUx, double** HUy) {
 
 int swf_step(swf_ctx* c, double dt_cap, swf_step_info* info) {
   cudaSetDevice(c->device);
+  c->last_staged = c->mode == 1;
   if (c->mode == 1) {
     int rc = reset_counters(c);
     if (rc) return rc;
@@ -564,6 +568,7 @@ int swf_run(swf_ctx* c, int n, double dt_cap, int* done, swf_step_info* last) {
   cudaSetDevice(c->device);
   if (done) *done = 0;
   if (n <= 0) return SWF_OK;
+  c->last_staged = c->mode == 1;
   if (c->mode == 1) {
     for (int k = 0; k < n; ++k) {
       swf_step_info tmp;
@@ -584,7 +589,10 @@ int swf_run(swf_ctx* c, int n, double dt_cap, int* done, swf_step_info* last) {
   }
   int pairs = (n - enq) / 2;
   if (pairs > 0) {
-    if (!c->graph || c->graph_dt_cap != dt_cap || c->timing) {
+    if (c->timing) {
+      for (int p = 0; p < 2 * pairs; ++p)
+        if ((rc = fused_enqueue_step(c, dt_cap))) return rc;
+    } else if (!c->graph || c->graph_dt_cap != dt_cap) {
       drop_graph(c);
       cudaGraph_t g;
       cudaError_t e = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal);
@@ -627,9 +635,46 @@ int swf_sync(swf_ctx* c) {
   return check_device_error(c);
 }
 
-int swf_set_timing(swf_ctx* c, int enabled) {
-  c->timing = enabled != 0;
+int swf_set_timing(swf_ctx* c, int slots) {
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (cudaEvent_t e : c->tev) cudaEventDestroy(e);
+  c->tev.clear();
+  c->tslots = 0;
+  c->tstep = 0;
+  c->timing = slots != 0;
+  if (slots > 1) {
+    c->tev.resize((size_t)slots * 6);
+    for (auto& e : c->tev) {
+      cudaError_t r = cudaEventCreate(&e);
+      if (r != cudaSuccess) return cuda_check(c, r, "timing events");
+    }
+    c->tslots = slots;
+  }
   drop_graph(c);
+  return SWF_OK;
+}
+
+int swf_timing_read(swf_ctx* c, int nsteps, double* out) {
+  cudaSetDevice(c->device);
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return cuda_check(c, e, "timing read");
+  if (c->tslots <= 0) return set_err(c, SWF_ECONFIG, "per-step timing needs swf_set_timing(ctx, slots > 1)");
+  if (nsteps > c->tslots || nsteps > c->tstep)
+    return set_err(c, SWF_ECONFIG, "fewer timed steps recorded than requested");
+  int map[5][2] = {{0, 0}, {1, 1}, {2, 2}, {3, 6}, {4, 7}};
+  for (int s = 0; s < nsteps; ++s) {
+    long long st = c->tstep - nsteps + s;
+    const cudaEvent_t* E = &c->tev[(size_t)(st % c->tslots) * 6];
+    double* o = out + (size_t)s * 8;
+    for (int q = 0; q < 8; ++q) o[q] = 0.0;
+    for (auto& m : map) {
+      float ms = 0.f;
+      e = cudaEventElapsedTime(&ms, E[m[0]], E[m[0] + 1]);
+      if (e != cudaSuccess) return cuda_check(c, e, "timing elapsed");
+      o[m[1]] = ms * 1e-3;
+    }
+  }
   return SWF_OK;
 }
 
@@ -647,6 +692,7 @@ int swf_stage(swf_ctx* c, int stage, double arg, double* tau_out) {
     int rc = reset_counters(c);
     if (rc) return rc;
   }
+  c->last_staged = 1;
   int rc = stage_run(c, stage, arg, tau_out);
   if (rc) return rc;
   cudaError_t e = cudaStreamSynchronize(c->stream);
@@ -675,11 +721,10 @@ int swf_download_mask(swf_ctx* c, int* interior, int* halo, int* nbx, int* nby) 
 int swf_last_volumes(swf_ctx* c, double* cd, double* sv, double* bo) {
   cudaSetDevice(c->device);
   double v[3] = {0, 0, 0};
-  if (c->mode == 1 || c->scr) {
+  if (c->last_staged) {
     int rc = stage_volumes(c, v);
     if (rc) return rc;
-  }
-  if (c->mode == 0) {
+  } else {
     cudaError_t e = cudaMemcpy(c->h_sc, c->d_sc, sizeof(StepScalars), cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return cuda_check(c, e, "volumes");
     v[0] = c->h_sc->deficit;

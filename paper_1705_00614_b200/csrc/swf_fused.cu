@@ -702,7 +702,11 @@ constexpr size_t step_smem() {
 }
 
 void ev(swf_ctx* c, int i) {
-  if (c->timing) cudaEventRecord(c->ev[i], c->stream);
+  if (!c->timing) return;
+  if (c->tslots > 0)
+    cudaEventRecord(c->tev[(size_t)(c->tstep % c->tslots) * 6 + i], c->stream);
+  else
+    cudaEventRecord(c->ev[i], c->stream);
 }
 
 // rows k_forces must cover: owned rows plus 2 ghost rows on each interior side
@@ -782,6 +786,7 @@ int fused_enqueue_phase2(swf_ctx* c, double dt_cap, double global_speed) {
   ev(c, 4);
   k_finish<<<1, 256, 0, c->stream>>>(G, c->d_part, nt, c->d_sc, c->h * c->h, c->h);
   ev(c, 5);
+  if (c->timing && c->tslots > 0) ++c->tstep;
   c->cur = 1 - c->cur;  // optimistic; rolled back by the caller on failure
   return cuda_check(c, cudaGetLastError(), "k_step");
 }

@@ -106,9 +106,14 @@ struct swf_ctx {
   // stage path
   swf::Scratch* scr = nullptr;
   int mode = 0;  // 0 fused, 1 staged
+  int last_staged = 0;  // which path produced the last diagnostics
   // timing
   bool timing = false;
   cudaEvent_t ev[10] = {};
+  // per-step event ring of the fused path (swf_set_timing(ctx, slots))
+  std::vector<cudaEvent_t> tev;  // 6 per slot
+  int tslots = 0;
+  long long tstep = 0;
   // CUDA graph of one fused step (captured lazily, invalidated on config change)
   cudaGraphExec_t graph = nullptr;
   double graph_dt_cap = -1.0;

@@ -127,8 +127,15 @@ class CsphTvdStepper:
         """0 = fused tile kernels (default), 1 = unfused stage kernels."""
         self._rc(self._lib.swf_set_mode(self._ctx, int(mode)))
 
-    def set_timing(self, enabled: bool) -> None:
-        self._rc(self._lib.swf_set_timing(self._ctx, int(bool(enabled))))
+    def set_timing(self, slots) -> None:
+        """0/False: off; 1/True: timings of the last step; n > 1: per-step ring."""
+        self._rc(self._lib.swf_set_timing(self._ctx, int(slots)))
+
+    def timing_read(self, nsteps: int) -> np.ndarray:
+        """(nsteps, 8) device seconds per bucket of the last nsteps fused steps."""
+        out = np.zeros((nsteps, 8))
+        self._rc(self._lib.swf_timing_read(self._ctx, int(nsteps), A.dptr(out)))
+        return out
 
     def _push_control(self):
         k = Marshalled.control(self._control)
