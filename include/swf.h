@@ -231,6 +231,11 @@ int swf_strip_phase2(swf_ctx* ctx, double global_speed, double dt_cap,
  * *count = doubles per field (0 when that side is a domain edge). */
 int swf_strip_halo_ptrs(swf_ctx* ctx, int side, double** send3, double** recv3,
                         size_t* count);
+/* Copy the SWF_HALO owned boundary rows of `side` into the contiguous DEVICE
+ * buffer dst = [H | HUx | HUy] (3*count doubles), or a neighbour's pack into
+ * this strip's ghost rows on `side`.  Synchronous on the context stream. */
+int swf_strip_pack(swf_ctx* ctx, int side, double* dst);
+int swf_strip_unpack(swf_ctx* ctx, int side, const double* src);
 /* Owned global rows [j0, j1) and the ghost-row counts below/above. */
 int swf_strip_rows(const swf_ctx* ctx, int* j0, int* j1, int* ghost_lo,
                    int* ghost_hi);

@@ -62,6 +62,8 @@ def declare(lib):
     _sig(lib, "swf_strip_phase2", I, P, D, D, PN)
     _sig(lib, "swf_strip_halo_ptrs", I, P, I, PPD, PPD, C.POINTER(C.c_size_t))
     _sig(lib, "swf_strip_rows", I, P, PI, PI, PI, PI)
+    _sig(lib, "swf_strip_pack", I, P, I, C.c_void_p)
+    _sig(lib, "swf_strip_unpack", I, P, I, C.c_void_p)
     return lib
 
 

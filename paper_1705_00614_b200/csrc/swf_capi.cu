@@ -277,6 +277,7 @@ int create_impl(const swf_terrain* T, const swf_params* P, const swf_control* K,
     e = cudaMemcpy(c->d_sc, c->h_sc, sizeof(StepScalars), cudaMemcpyHostToDevice);
   }
   for (int i = 0; i < 10 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
+  if (e == cudaSuccess && fused_prepare(c) != SWF_OK) e = cudaErrorInvalidValue;
   if (e != cudaSuccess) {
     rc = cuda_check(nullptr, e, "context allocation");
     swf_destroy(c);
@@ -857,6 +858,36 @@ int swf_strip_halo_ptrs(swf_ctx* c, int side, double** send3, double** recv3, si
     recv3[q] = f[q] + (size_t)rr * nx;
   }
   return SWF_OK;
+}
+
+// Pack the SWF_HALO owned boundary rows of (H, HUx, HUy) on `side` into a
+// contiguous device buffer [H rows | HUx rows | HUy rows], or unpack a
+// neighbour's pack into the ghost rows.  Enqueued on the context stream and
+// synchronised, so the buffer can go straight to NCCL on another stream.
+int swf_strip_pack(swf_ctx* c, int side, double* dst) {
+  cudaSetDevice(c->device);
+  double *s3[3], *r3[3];
+  size_t count = 0;
+  swf_strip_halo_ptrs(c, side, s3, r3, &count);
+  cudaError_t e = cudaSuccess;
+  for (int q = 0; q < 3 && e == cudaSuccess && count; ++q)
+    e = cudaMemcpyAsync(dst + q * count, s3[q], count * sizeof(double), cudaMemcpyDeviceToDevice,
+                        c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  return cuda_check(c, e, "strip pack");
+}
+
+int swf_strip_unpack(swf_ctx* c, int side, const double* src) {
+  cudaSetDevice(c->device);
+  double *s3[3], *r3[3];
+  size_t count = 0;
+  swf_strip_halo_ptrs(c, side, s3, r3, &count);
+  cudaError_t e = cudaSuccess;
+  for (int q = 0; q < 3 && e == cudaSuccess && count; ++q)
+    e = cudaMemcpyAsync(r3[q], src + q * count, count * sizeof(double), cudaMemcpyDeviceToDevice,
+                        c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  return cuda_check(c, e, "strip unpack");
 }
 
 int swf_strip_rows(const swf_ctx* c, int* j0, int* j1, int* glo, int* ghi) {

@@ -775,14 +775,7 @@ int fused_enqueue_phase2(swf_ctx* c, double dt_cap, double global_speed) {
                                 c->d_sc, dt_cap, global_speed);
   ev(c, 3);
   int nt = G.tiles_x * G.tiles_y;
-  if (nt > 0) {
-    static bool attr_set = false;
-    if (!attr_set) {
-      cudaFuncSetAttribute(k_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)step_smem());
-      attr_set = true;
-    }
-    k_step<<<nt, NTHR, step_smem(), c->stream>>>(G, step_args(c));
-  }
+  if (nt > 0) k_step<<<nt, NTHR, step_smem(), c->stream>>>(G, step_args(c));
   ev(c, 4);
   k_finish<<<1, 256, 0, c->stream>>>(G, c->d_part, nt, c->d_sc, c->h * c->h, c->h);
   ev(c, 5);
@@ -800,5 +793,13 @@ int fused_enqueue_step(swf_ctx* c, double dt_cap) {
 }
 
 size_t fused_tile_bytes() { return step_smem(); }
+
+// Kernel attributes must be set outside stream capture (a CUDA graph does not
+// record cudaFuncSetAttribute), so contexts call this at creation.
+int fused_prepare(swf_ctx* c) {
+  cudaError_t e = cudaFuncSetAttribute(k_step, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)step_smem());
+  return cuda_check(c, e, "k_step shared-memory attribute");
+}
 
 }  // namespace swf

@@ -133,6 +133,7 @@ void stage_free(swf_ctx* c);
 
 // fused path (swf_fused.cu)
 int fused_enqueue_step(swf_ctx* c, double dt_cap);
+int fused_prepare(swf_ctx* c);
 int fused_enqueue_phase1(swf_ctx* c, double dt_cap);
 int fused_enqueue_phase2(swf_ctx* c, double dt_cap);
 int fused_enqueue_phase2(swf_ctx* c, double dt_cap, double global_speed);

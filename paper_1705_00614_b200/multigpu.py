@@ -1,0 +1,317 @@
+"""Row-strip decomposition of the CSPH-TVD step across GPUs.
+
+The global nx x ny grid is cut into contiguous row strips whose boundaries
+are multiples of the block size B, so every B-block (and with it the K1
+activity mask and the dry-block skipping) lives on exactly one strip.  Each
+strip keeps SWF_HALO = 3 ghost rows per interior side — the radius of the
+step's dependency diamond — and per step:
+
+  1. halo exchange: the 3 owned boundary rows of (H, HUx, HUy) go to each
+     neighbour's ghost rows (NCCL send/recv over NVLink, or in-process
+     device copies for virtual ranks);
+  2. phase 1 on every strip: sources, K1 mask, K2 forces on the owned rows
+     plus 2 ghost rows, and the strip's CFL speed;
+  3. allreduce-MAX of the speed — exact in any order, so tau is bit-equal to
+     the single-grid tau;
+  4. phase 2: tau, fused K4..K8 on the owned rows.
+
+Per-cell arithmetic is unchanged, so a P-strip run is bit-identical to the
+single-grid run (tests/test_gpu_strips.py checks this on one GPU with virtual
+ranks; tests/test_multigpu_cpu.py checks the exchange protocol with gloo).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+import time
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _abi as A
+
+HALO = 3
+
+
+def strip_bounds(ny: int, parts: int, bs: int) -> List[Tuple[int, int]]:
+    """Owned global rows [j0, j1) per strip: balanced whole block rows."""
+    nbr = (ny + bs - 1) // bs
+    if parts < 1 or parts > nbr:
+        raise ValueError(f"cannot split {nbr} block rows into {parts} strips")
+    base, rem = divmod(nbr, parts)
+    out, b0 = [], 0
+    for p in range(parts):
+        b1 = b0 + base + (1 if p < rem else 0)
+        out.append((b0 * bs, min(b1 * bs, ny)))
+        b0 = b1
+    return out
+
+
+def window_rows(j0: int, j1: int, ny: int, halo: int = HALO) -> Tuple[int, int]:
+    """Global rows of a strip's local window (owned + ghost rows)."""
+    return max(j0 - halo, 0), min(j1 + halo, ny)
+
+
+class Strip:
+    """One strip context of libswflood_cuda (swf_create_strip)."""
+
+    def __init__(self, sc_window, ny_global: int, j0: int, j1: int, sources, wind,
+                 device: int = 0):
+        from ._lib import lib
+        from ._marshal import Marshalled
+        from .stepper import raise_for
+        self._lib = lib()
+        self._raise = raise_for
+        T = sc_window.terrain
+        self.nx, self.ny, self.j0, self.j1 = T.nx, ny_global, j0, j1
+        self.w0, self.w1 = window_rows(j0, j1, ny_global)
+        if T.ny != self.w1 - self.w0:
+            raise ValueError("scenario window does not match the strip window")
+        m = Marshalled()
+        b = m.arr(T.b)
+        t = A.swf_terrain(T.nx, ny_global, T.h, T.x0, T.y0 - self.w0 * T.h, A.dptr(b))
+        p = m.params(sc_window.params, T.nx * T.ny)
+        k = m.control(sc_window.control)
+        o = m.options(sc_window.options)
+        ctx = C.c_void_p()
+        rc = self._lib.swf_create_strip(C.byref(t), C.byref(p), C.byref(k), C.byref(o), j0, j1,
+                                        device, C.byref(ctx))
+        raise_for(rc, None)
+        self.ctx = ctx
+        if wind is not None and wind.any():
+            n, tt, x, y = m.wind(wind)
+            self._rc(self._lib.swf_set_wind(ctx, n, tt, x, y))
+        if sources:
+            arr = m.sources(sources)
+            self._rc(self._lib.swf_set_sources(ctx, len(sources), arr))
+        self.count = {s: self._count(s) for s in (0, 1)}
+
+    def _rc(self, rc):
+        self._raise(rc, self.ctx)
+
+    def _count(self, side):
+        s3, r3 = (A.PD * 3)(), (A.PD * 3)()
+        n = C.c_size_t()
+        self._rc(self._lib.swf_strip_halo_ptrs(self.ctx, side, s3, r3, C.byref(n)))
+        return n.value
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            self._lib.swf_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def upload(self, H, HUx, HUy, t: float):
+        self._rc(self._lib.swf_upload_state(self.ctx, A.dptr(H), A.dptr(HUx), A.dptr(HUy), t))
+
+    def download(self, H, HUx, HUy) -> float:
+        t = C.c_double()
+        self._rc(self._lib.swf_download_state(self.ctx, A.dptr(H), A.dptr(HUx), A.dptr(HUy),
+                                              C.byref(t)))
+        return t.value
+
+    def pack(self, side: int, dev_ptr: int):
+        self._rc(self._lib.swf_strip_pack(self.ctx, side, C.c_void_p(dev_ptr)))
+
+    def unpack(self, side: int, dev_ptr: int):
+        self._rc(self._lib.swf_strip_unpack(self.ctx, side, C.c_void_p(dev_ptr)))
+
+    def phase1(self, dt_cap: float = 0.0) -> float:
+        s = C.c_double()
+        self._rc(self._lib.swf_strip_phase1(self.ctx, float(dt_cap), C.byref(s)))
+        return s.value
+
+    def phase2(self, speed: float, dt_cap: float = 0.0):
+        from ._marshal import info_from_c
+        info = A.swf_step_info()
+        self._rc(self._lib.swf_strip_phase2(self.ctx, float(speed), float(dt_cap), C.byref(info)))
+        return info_from_c(info)
+
+    def stream_handle(self) -> int:
+        return self._lib.swf_stream(self.ctx) or 0
+
+    def set_timing(self, slots: int):
+        self._rc(self._lib.swf_set_timing(self.ctx, int(slots)))
+
+    def timing_read(self, n: int) -> np.ndarray:
+        out = np.zeros((n, 8))
+        self._rc(self._lib.swf_timing_read(self.ctx, int(n), A.dptr(out)))
+        return out
+
+
+# ---------------------------------------------------------------------------
+# exchange protocol (device-agnostic: works with NCCL on CUDA tensors and with
+# gloo on CPU tensors, which is how the CPU tests exercise it)
+# ---------------------------------------------------------------------------
+
+def exchange_plan(rank: int, world: int):
+    """(side, peer) pairs this rank exchanges with: side 0 = south (rank-1),
+    side 1 = north (rank+1)."""
+    plan = []
+    if rank > 0:
+        plan.append((0, rank - 1))
+    if rank < world - 1:
+        plan.append((1, rank + 1))
+    return plan
+
+
+def dist_exchange(pack, unpack, counts, rank: int, world: int, device):
+    """Halo exchange through torch.distributed point-to-point ops.
+    pack(side, tensor) fills a send buffer, unpack(side, tensor) consumes a
+    received one; counts[side] = doubles per field."""
+    import torch
+    import torch.distributed as dist
+    ops, recv = [], {}
+    for side, peer in exchange_plan(rank, world):
+        n = 3 * counts[side]
+        sbuf = torch.empty(n, dtype=torch.float64, device=device)
+        pack(side, sbuf)
+        rbuf = torch.empty(n, dtype=torch.float64, device=device)
+        ops.append(dist.P2POp(dist.isend, sbuf, peer))
+        ops.append(dist.P2POp(dist.irecv, rbuf, peer))
+        recv[side] = rbuf
+    if ops:
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+    if device is not None and str(device).startswith("cuda"):
+        torch.cuda.synchronize(device)
+    for side, rbuf in recv.items():
+        unpack(side, rbuf)
+
+
+def dist_allreduce_max(x: float, device) -> float:
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def local_exchange(strips: Sequence[Strip]):
+    """Virtual ranks on one device: strip r's south rows -> strip r-1's
+    north ghosts and vice versa, through the same pack/unpack entry points."""
+    import torch
+    for r in range(len(strips) - 1):
+        lo, hi = strips[r], strips[r + 1]
+        a = torch.empty(3 * lo.count[1], dtype=torch.float64, device="cuda")
+        b = torch.empty(3 * hi.count[0], dtype=torch.float64, device="cuda")
+        lo.pack(1, a.data_ptr())
+        hi.pack(0, b.data_ptr())
+        hi.unpack(0, a.data_ptr())
+        lo.unpack(1, b.data_ptr())
+
+
+def local_step(strips: Sequence[Strip], dt_cap: float = 0.0):
+    local_exchange(strips)
+    speed = max(s.phase1(dt_cap) for s in strips)
+    return [s.phase2(speed, dt_cap) for s in strips]
+
+
+# ---------------------------------------------------------------------------
+# bench (torchrun, one rank per GPU)
+# ---------------------------------------------------------------------------
+
+def bench_strips(args) -> Optional[dict]:
+    import torch
+    import torch.distributed as dist
+    from . import scenarios as S
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=dev)
+    full_n = {"C3": 16384, "C5": 32768, "C2": 2048}[args.config]
+    bs = 16
+    bounds = strip_bounds(full_n, world, bs)
+    j0, j1 = bounds[rank]
+    w0, w1 = window_rows(j0, j1, full_n)
+    sc = S.build(args.config, device=f"cuda:{local}", window=(0, w0, full_n, w1 - w0))
+    if args.no_skip:
+        sc.options.skip_dry_blocks = False
+    strip = Strip(sc, full_n, j0, j1, sc.global_sources, sc.wind, device=local)
+    strip.upload(sc.state.H, sc.state.HUx, sc.state.HUy, 0.0)
+
+    def pack(side, t):
+        strip.pack(side, t.data_ptr())
+
+    def unpack(side, t):
+        strip.unpack(side, t.data_ptr())
+
+    def step():
+        dist_exchange(pack, unpack, strip.count, rank, world, dev)
+        sp = strip.phase1(0.0)
+        g = dist_allreduce_max(sp, dev)
+        return strip.phase2(g, 0.0)
+
+    for _ in range(args.warmup):
+        step()
+    K = args.steps
+    strip.set_timing(K)
+    stream = torch.cuda.ExternalStream(strip.stream_handle())
+    from bench import ClockSampler, peaks, ncu_traffic  # noqa
+    clocks = ClockSampler(local) if rank == 0 else None
+    if clocks:
+        clocks.start()
+        time.sleep(0.3)
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    infos = [step() for _ in range(K)]
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    clk = clocks.stop() if clocks else None
+    tk = strip.timing_read(K)
+    t_kstep = float(tk[:, 6].mean())
+    last = infos[-1]
+    N_total = full_n * full_n
+    n_own = (j1 - j0) * full_n
+    n_act = min(n_own, last.flux_blocks * bs * bs) if sc.options.skip_dry_blocks else n_own
+    per_act = 56 + (8 if sc.params.n_field is not None else 0)
+    alg = per_act * n_act + 8 * (n_own - n_act)
+    # aggregate kernel-level bandwidth: sum of per-rank algorithmic bytes / max k_step time
+    agg = torch.tensor([alg, t_kstep], dtype=torch.float64, device=dev)
+    alg_all = agg[0:1].clone()
+    dist.all_reduce(alg_all, op=dist.ReduceOp.SUM)
+    tmax = agg[1:2].clone()
+    dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    value = N_total * K / (ms_max * 1e-3) / 1e6
+    if rank != 0:
+        dist.barrier()
+        return None
+    hbm_peak, src = peaks()
+    achieved = float(alg_all.item()) / float(tmax.item()) / 1e9 / world
+    traffic = ncu_traffic("k_step")
+    line = {
+        "metric": "cell-updates/sec (Mcells/s)", "value": round(value, 3), "unit": "Mcells/s",
+        "n_gpus": world, "steps": K, "warmup": args.warmup, "ms_per_step": round(ms_max / K, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator, scenarios.py)",
+        "config": {"workload": f"{sc.name.split('-')[0]} {full_n}x{full_n} row strips",
+                   "cells": N_total, "strips": bounds, "halo_rows": HALO,
+                   "parallelism": f"row strips x{world}, NCCL halo send/recv + allreduce-max",
+                   "l2": "inputs larger than L2"},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
+                     "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
+                     "traffic": traffic["bytes_per_launch"] if traffic else None,
+                     "kernel": "k_step (fused K4..K8), per GPU", "peak_source": src},
+        "e2e": None,
+        "gpu_launches": 7 * K,
+        "clocks": clk,
+        "cpu_baseline": None,
+    }
+    dist.barrier()
+    return line

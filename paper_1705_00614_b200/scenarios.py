@@ -41,6 +41,7 @@ class Scenario:
     wind: WindForcing = field(default_factory=WindForcing)
     full_shape: Tuple[int, int] = (0, 0)
     window: Tuple[int, int, int, int] = (0, 0, 0, 0)  # i0, j0, ni, nj
+    global_sources: List[SourceSpec] = field(default_factory=list)  # full-grid cells
 
     def cells(self) -> int:
         return self.terrain.nx * self.terrain.ny
@@ -176,7 +177,8 @@ def floodplain(n: int = 16384, h: float = 50.0, window=None, device: str = "cpu"
                                     list(s.hydrograph), s.rate, s.source_velocity))
     name = "C3-floodplain" if n == 16384 else ("C5-floodplain" if n == 32768 else f"floodplain-{n}")
     return Scenario(name, terrain, params, TimestepControl(), opts, st, specs,
-                    WindForcing.constant(5.0, 2.0), full_shape=(n, n), window=(i0, j0, ni, nj))
+                    WindForcing.constant(5.0, 2.0), full_shape=(n, n), window=(i0, j0, ni, nj),
+                    global_sources=full_specs)
 
 
 def lake_at_rest(n: int = 128, h: float = 10.0, level: float = 0.0, seed: int = SEED) -> Scenario:

@@ -1,0 +1,51 @@
+"""Row strips on ONE GPU (virtual ranks): P strip contexts exchanging halos
+through the same pack/unpack entry points the NCCL path uses, against the
+single-grid run.  Bit-identical by construction (exact max-reduction of the
+CFL speed, unchanged per-cell arithmetic)."""
+import numpy as np
+import pytest
+
+from helpers import assert_bitwise, make
+from paper_1705_00614_b200 import multigpu as M
+from paper_1705_00614_b200 import scenarios as S
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("parts", [2, 3, 4])
+def test_strips_bitwise_equal_single_grid(parts):
+    from paper_1705_00614_b200 import CsphTvdStepper
+    n = 256
+    full = S.floodplain(n, 50.0)
+    one = make(CsphTvdStepper, full)
+    st = full.state.copy()
+    one.upload(st)
+    one.run(25)
+    one.download(st)
+    bounds = M.strip_bounds(n, parts, full.options.block_size)
+    strips = []
+    for j0, j1 in bounds:
+        w0, w1 = M.window_rows(j0, j1, n)
+        sc = S.floodplain(n, 50.0, window=(0, w0, n, w1 - w0))
+        s = M.Strip(sc, n, j0, j1, sc.global_sources, sc.wind)
+        s.upload(sc.state.H, sc.state.HUx, sc.state.HUy, 0.0)
+        strips.append((s, sc, w0))
+    for _ in range(25):
+        M.local_step([s for s, _, _ in strips])
+    H = np.empty(n * n)
+    X = np.empty(n * n)
+    Y = np.empty(n * n)
+    t = None
+    for (s, sc, w0), (j0, j1) in zip(strips, bounds):
+        h = np.empty_like(sc.state.H)
+        x = np.empty_like(h)
+        y = np.empty_like(h)
+        t = s.download(h, x, y)
+        r0 = (j0 - w0) * n
+        H[j0 * n:j1 * n] = h[r0:r0 + (j1 - j0) * n]
+        X[j0 * n:j1 * n] = x[r0:r0 + (j1 - j0) * n]
+        Y[j0 * n:j1 * n] = y[r0:r0 + (j1 - j0) * n]
+    assert t == st.t
+    assert_bitwise(H, st.H, "H")
+    assert_bitwise(X, st.HUx, "HUx")
+    assert_bitwise(Y, st.HUy, "HUy")

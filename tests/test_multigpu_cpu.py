@@ -1,0 +1,93 @@
+"""Host-side logic of the multi-GPU row-strip path on CPU: the strip
+decomposition and the halo-exchange / allreduce protocol, run with
+torch.distributed gloo at world_size 2 and 3 (same code as the NCCL path)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paper_1705_00614_b200 import multigpu as M
+
+
+def test_strip_bounds_block_aligned_and_balanced():
+    for ny, bs in ((16384, 16), (1000, 16), (96, 7), (32768, 16)):
+        for parts in (1, 2, 3, 4, 8):
+            b = M.strip_bounds(ny, parts, bs)
+            assert b[0][0] == 0 and b[-1][1] == ny
+            assert all(a[1] == c[0] for a, c in zip(b, b[1:]))
+            assert all(j0 % bs == 0 for j0, _ in b)
+            h = [j1 - j0 for j0, j1 in b]
+            assert max(h) - min(h) < 2 * bs  # whole block rows; the last may be partial
+    with pytest.raises(ValueError):
+        M.strip_bounds(32, 3, 16)
+
+
+def test_window_rows():
+    assert M.window_rows(0, 100, 200) == (0, 103)
+    assert M.window_rows(100, 200, 200) == (97, 200)
+    assert M.window_rows(64, 128, 256) == (61, 131)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, ny, nx, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        bounds = M.strip_bounds(ny, world, 4)
+        j0, j1 = bounds[rank]
+        w0, w1 = M.window_rows(j0, j1, ny)
+        # global field f(j, i) = 1000*j + i; each rank owns rows [j0,j1) and
+        # starts with NaN ghost rows
+        win = np.full((w1 - w0, nx), np.nan)
+        own = np.arange(j0, j1)[:, None] * 1000.0 + np.arange(nx)[None, :]
+        win[j0 - w0:j1 - w0] = own
+        fields = [win.copy(), win.copy() + 0.5, win.copy() - 0.5]
+        r0, r1 = j0 - w0, j1 - w0
+        counts = {0: (j0 - w0) * nx, 1: (w1 - j1) * nx}
+
+        def pack(side, t):
+            rows = slice(r0, r0 + (j0 - w0)) if side == 0 else slice(r1 - (w1 - j1), r1)
+            t.copy_(torch.from_numpy(np.concatenate([f[rows].reshape(-1) for f in fields])))
+
+        def unpack(side, t):
+            rows = slice(0, r0) if side == 0 else slice(r1, w1 - w0)
+            n = counts[side]
+            a = t.numpy()
+            for k, f in enumerate(fields):
+                f[rows] = a[k * n:(k + 1) * n].reshape(-1, nx)
+
+        M.dist_exchange(pack, unpack, counts, rank, world, torch.device("cpu"))
+        exp = np.arange(w0, w1)[:, None] * 1000.0 + np.arange(nx)[None, :]
+        ok = all(np.array_equal(f, exp + d) for f, d in zip(fields, (0.0, 0.5, -0.5)))
+        speed = M.dist_allreduce_max(float(rank) * 1.5 + 0.25, torch.device("cpu"))
+        q.put((rank, ok, speed))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_halo_exchange_and_allreduce(world):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, 24, 5, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok, speed in res:
+        assert ok, f"rank {rank}: ghost rows differ from the neighbour's owned rows"
+        assert speed == (world - 1) * 1.5 + 0.25
