@@ -611,7 +611,7 @@ int swf_run(swf_ctx* c, int n, double dt_cap, int* done, swf_step_info* last) {
       if (e != cudaSuccess) return cuda_check(c, e, "graph instantiate");
       c->graph_dt_cap = dt_cap;
     }
-    for (int p = 0; p < pairs; ++p) {
+    for (int p = 0; p < pairs && c->graph; ++p) {
       cudaError_t e = cudaGraphLaunch(c->graph, c->stream);
       if (e != cudaSuccess) return cuda_check(c, e, "graph launch");
     }
