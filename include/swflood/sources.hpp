@@ -1,0 +1,4 @@
+// Forwarder: the reference header name (proj/include/swflood/sources.hpp) mapped
+// onto the B200 drop-in API.
+#pragma once
+#include "../swflood_b200.hpp"

@@ -35,14 +35,32 @@ def stale():
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
+HOST_SRC = os.path.join(HERE, "host", "swflood_b200.cpp")
+HOST_OUT = os.path.join(HERE, "libswflood_b200.so")
+INCLUDE = os.path.join(HERE, "..", "include")
+
+
+def build_host(force=False):
+    """The C++ drop-in API (include/swflood_b200.hpp) over the C ABI."""
+    deps = [HOST_SRC, os.path.join(INCLUDE, "swflood_b200.hpp"), os.path.join(INCLUDE, "swf.h"), OUT]
+    if not force and os.path.exists(HOST_OUT) and all(
+            os.path.getmtime(d) <= os.path.getmtime(HOST_OUT) for d in deps):
+        return HOST_OUT
+    cxx = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
+    cmd = [cxx, "-std=c++20", "-O2", "-fPIC", "-shared", "-I", INCLUDE, HOST_SRC, "-o", HOST_OUT,
+           "-L", HERE, "-lswflood_cuda", "-Wl,-rpath,$ORIGIN"]
+    subprocess.run(cmd, check=True)
+    return HOST_OUT
+
+
 def build(force=False, verbose=False):
-    if not force and not stale():
-        return OUT
-    cmd = [nvcc()] + NVCC_FLAGS + ["-shared", "-o", OUT] + [os.path.join(CSRC, s) for s in SOURCES]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True, cwd=CSRC)
+    if force or stale():
+        cmd = [nvcc()] + NVCC_FLAGS + ["-shared", "-o", OUT] + [os.path.join(CSRC, s) for s in SOURCES]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True, cwd=CSRC)
+    build_host(force)
     return OUT
 
 

@@ -1,0 +1,426 @@
+// swflood_b200.cpp — the C++ drop-in API (include/swflood_b200.hpp) over the
+// C ABI of libswflood_cuda.so.  Value-type validation mirrors the reference
+// (grid.cpp:13-121, sources.cpp:10-33, stepper.cpp:31-49); everything that
+// touches cells is a call into the CUDA library.
+#include "swflood_b200.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numbers>
+
+namespace swflood {
+
+namespace {
+
+[[noreturn]] void throw_status(int rc, const char* msg) {
+  std::string m = msg ? msg : "";
+  switch (rc) {
+    case SWF_ECONFIG: throw ConfigError(m);
+    case SWF_ENUMERICAL: throw NumericalError(m);
+    case SWF_ERANGE: throw std::out_of_range(m);
+    default: throw std::runtime_error(m);
+  }
+}
+
+swf_control to_c(const TimestepControl& k) { return swf_control{k.courant, k.dt_max, k.dt_min}; }
+
+swf_options to_c(const StepperOptions& o) {
+  auto e = [](EdgeKind k) { return k == EdgeKind::Open ? SWF_EDGE_OPEN : SWF_EDGE_REFLECTIVE; };
+  return swf_options{o.block_size, o.skip_dry_blocks ? 1 : 0, o.workers,
+                     e(o.boundaries.west), e(o.boundaries.east), e(o.boundaries.south),
+                     e(o.boundaries.north)};
+}
+
+bool same(const TimestepControl& a, const TimestepControl& b) {
+  return a.courant == b.courant && a.dt_max == b.dt_max && a.dt_min == b.dt_min;
+}
+
+bool same(const StepperOptions& a, const StepperOptions& b) {
+  return a.block_size == b.block_size && a.skip_dry_blocks == b.skip_dry_blocks &&
+         a.workers == b.workers && a.boundaries.west == b.boundaries.west &&
+         a.boundaries.east == b.boundaries.east && a.boundaries.south == b.boundaries.south &&
+         a.boundaries.north == b.boundaries.north;
+}
+
+template <class T>
+double interp_series(const std::vector<T>& s, double t, double T::*val) {
+  if (s.empty()) return 0.0;
+  if (s.size() == 1 || t <= s.front().t) return s.front().*val;
+  if (t >= s.back().t) return s.back().*val;
+  auto hi = std::upper_bound(s.begin(), s.end(), t, [](double v, const T& x) { return v < x.t; });
+  const T& H = *hi;
+  const T& L = *(hi - 1);
+  double a = (t - L.t) / (H.t - L.t);
+  return L.*val + a * (H.*val - L.*val);
+}
+
+}  // namespace
+
+// ---- value types ------------------------------------------------------------
+
+void Terrain::validate() const {
+  if (nx < 1 || ny < 1) throw ConfigError("terrain: nx and ny must be >= 1");
+  if (!(h > 0.0)) throw ConfigError("terrain: cell size must be positive");
+  if (b.size() != cells()) throw ConfigError("terrain: bed array size mismatch");
+  for (std::size_t k = 0; k < b.size(); ++k)
+    if (!std::isfinite(b[k]))
+      throw ConfigError("terrain: non-finite bed elevation at cell " + std::to_string(k));
+}
+
+FlowState FlowState::dry(const Terrain& terrain) {
+  FlowState s;
+  s.nx = terrain.nx;
+  s.ny = terrain.ny;
+  s.H.assign(terrain.cells(), 0.0);
+  s.HUx.assign(terrain.cells(), 0.0);
+  s.HUy.assign(terrain.cells(), 0.0);
+  return s;
+}
+
+void FlowState::enforce_dry_rule(double eps_dry) {
+  for (std::size_t k = 0; k < H.size(); ++k)
+    if (H[k] <= eps_dry) HUx[k] = HUy[k] = 0.0;
+}
+
+void PhysicalParams::validate() const {
+  if (!(g > 0.0)) throw ConfigError("params: gravity must be positive");
+  if (n_manning < 0.0) throw ConfigError("params: Manning coefficient must be >= 0");
+  if (std::any_of(n_field.begin(), n_field.end(), [](double n) { return n < 0.0; }))
+    throw ConfigError("params: Manning field must be >= 0");
+  if (nu < 0.0) throw ConfigError("params: viscosity must be >= 0");
+  if (!(rho_water > 0.0)) throw ConfigError("params: water density must be positive");
+  if (rho_air < 0.0) throw ConfigError("params: air density must be >= 0");
+  if (!(eps_dry > 0.0)) throw ConfigError("params: dry threshold must be positive");
+}
+
+double latitude_to_omega_z(double latitude_deg) {
+  return 7.2921159e-5 * std::sin(latitude_deg * std::numbers::pi / 180.0);
+}
+
+Vec2 WindForcing::at(double t) const {
+  return {interp_series(series, t, &WindSample::wx), interp_series(series, t, &WindSample::wy)};
+}
+
+void WindForcing::validate() const {
+  for (std::size_t k = 1; k < series.size(); ++k)
+    if (!(series[k].t > series[k - 1].t))
+      throw ConfigError("wind: sample times must be strictly increasing");
+}
+
+void SourceField::resize(int nx_, int ny_) {
+  nx = nx_;
+  ny = ny_;
+  std::size_t n = std::size_t(nx_) * std::size_t(ny_);
+  sigma.assign(n, 0.0);
+  vx.assign(n, 0.0);
+  vy.assign(n, 0.0);
+  index_q.assign(n, 0);
+}
+
+void SourceField::clear_values() {
+  std::fill(sigma.begin(), sigma.end(), 0.0);
+  std::fill(vx.begin(), vx.end(), 0.0);
+  std::fill(vy.begin(), vy.end(), 0.0);
+  std::fill(index_q.begin(), index_q.end(), 0);
+}
+
+double free_surface(const FlowState& state, const Terrain& terrain, int i, int j) {
+  if (!terrain.contains(i, j))
+    throw std::out_of_range("free_surface: cell (" + std::to_string(i) + "," + std::to_string(j) +
+                            ") outside grid");
+  return state.H[state.idx(i, j)] + terrain.b[terrain.idx(i, j)];
+}
+
+Vec2 velocity(const FlowState& state, const PhysicalParams& params, int i, int j) {
+  if (i < 0 || i >= state.nx || j < 0 || j >= state.ny)
+    throw std::out_of_range("velocity: cell index outside grid");
+  int k = state.idx(i, j);
+  if (state.H[k] <= params.eps_dry) return {};
+  return {state.HUx[k] / state.H[k], state.HUy[k] / state.H[k]};
+}
+
+double total_volume(const FlowState& state, const Terrain& terrain) {
+  double s = 0.0;
+  for (double v : state.H) s += v;
+  return s * terrain.cell_area();
+}
+
+double SourceSpec::discharge_at(double t) const {
+  return interp_series(hydrograph, t, &HydrographSample::q);
+}
+
+void SourceSpec::validate(const Terrain& terrain) const {
+  if (cells.i0 > cells.i1 || cells.j0 > cells.j1)
+    throw ConfigError("source '" + name + "': empty cell rectangle");
+  if (!terrain.contains(cells.i0, cells.j0) || !terrain.contains(cells.i1, cells.j1))
+    throw ConfigError("source '" + name + "': cells outside grid");
+  for (std::size_t k = 1; k < hydrograph.size(); ++k)
+    if (!(hydrograph[k].t > hydrograph[k - 1].t))
+      throw ConfigError("source '" + name + "': hydrograph times must be strictly increasing");
+  if (kind == Kind::Discharge && hydrograph.empty())
+    throw ConfigError("source '" + name + "': discharge source needs a hydrograph");
+}
+
+void ForceField::resize(int nx_, int ny_) {
+  nx = nx_;
+  ny = ny_;
+  std::size_t n = std::size_t(nx_) * std::size_t(ny_);
+  for (auto* v : {&fx, &fy, &fric_x, &fric_y, &sigma_eff}) v->assign(n, 0.0);
+}
+
+void ForceField::clear() {
+  for (auto* v : {&fx, &fy, &fric_x, &fric_y, &sigma_eff}) std::fill(v->begin(), v->end(), 0.0);
+}
+
+Vec2 bottom_friction(Vec2 u, double H, double g, double n_manning) {
+  double in[3] = {u.x, u.y, H}, out[2];
+  int rc = swf_dev_bottom_friction(1, in, g, n_manning, out);
+  if (rc) throw_status(rc, swf_last_error(nullptr));
+  return {out[0], out[1]};
+}
+
+Vec2 bottom_friction(Vec2 u, double H, const PhysicalParams& p) {
+  return bottom_friction(u, H, p.g, p.n_manning);  // scalar n, forcing.cpp:30-32
+}
+
+FaceFlux hll_face_flux(double hL, double unL, double utL, double hR, double unR, double utR,
+                       double g) {
+  double in[6] = {hL, unL, utL, hR, unR, utR}, out[3];
+  int rc = swf_dev_hll_face_flux(1, in, g, out);
+  if (rc) throw_status(rc, swf_last_error(nullptr));
+  return {out[0], out[1], out[2]};
+}
+
+void BlockMask::block_rect(int ib, int& i0, int& j0, int& i1, int& j1) const {
+  i0 = (ib % nbx) * block_size;
+  j0 = (ib / nbx) * block_size;
+  i1 = std::min(i0 + block_size - 1, nx - 1);
+  j1 = std::min(j0 + block_size - 1, ny - 1);
+}
+
+double active_fraction(const BlockMask& m) {
+  if (m.total_blocks() == 0) return 0.0;
+  int n = 0;
+  for (int ib = 0; ib < m.total_blocks(); ++ib) n += m.flux_active(ib);
+  return static_cast<double>(n) / m.total_blocks();
+}
+
+void TimestepControl::validate() const {
+  if (!(courant > 0.0 && courant < 1.0)) throw ConfigError("timestep: Courant number must be in (0,1)");
+  if (!(dt_max > 0.0)) throw ConfigError("timestep: dt_max must be positive");
+  if (!(dt_min > 0.0 && dt_min < dt_max)) throw ConfigError("timestep: need 0 < dt_min < dt_max");
+}
+
+StageTimings& StageTimings::operator+=(const StageTimings& o) {
+  mask += o.mask;
+  forces += o.forces;
+  dt += o.dt;
+  predictor += o.predictor;
+  mid_forces += o.mid_forces;
+  corrector += o.corrector;
+  flux += o.flux;
+  finalize += o.finalize;
+  return *this;
+}
+
+// ---- the stepper --------------------------------------------------------------
+
+CsphTvdStepper::CsphTvdStepper(const Terrain& terrain, PhysicalParams params,
+                               TimestepControl control, StepperOptions options)
+    : terrain_(&terrain), params_(std::move(params)), ctl_(control), opt_(options) {
+  terrain.validate();
+  params_.validate();
+  ctl_.validate();
+  if (opt_.block_size < 1) throw ConfigError("stepper: block size must be >= 1");
+  if (opt_.workers < 1) opt_.workers = 1;
+  if (!params_.n_field.empty() && params_.n_field.size() != terrain.cells())
+    throw ConfigError("stepper: Manning field size mismatch");
+  swf_terrain t{terrain.nx, terrain.ny, terrain.h, terrain.x0, terrain.y0, terrain.b.data()};
+  swf_params p{params_.g,       params_.n_manning, params_.nu,        params_.omega_z,
+               params_.c_a,     params_.rho_air,   params_.rho_water, params_.eps_dry,
+               params_.n_field.empty() ? nullptr : params_.n_field.data()};
+  swf_control k = to_c(ctl_);
+  swf_options o = to_c(opt_);
+  int rc = swf_create(&t, &p, &k, &o, &ctx_);
+  if (rc) throw_status(rc, swf_last_error(nullptr));
+  pushed_ctl_ = ctl_;
+  pushed_opt_ = opt_;
+}
+
+CsphTvdStepper::~CsphTvdStepper() { swf_destroy(ctx_); }
+
+void CsphTvdStepper::check(int rc) const {
+  if (rc) throw_status(rc, swf_last_error(ctx_));
+}
+
+void CsphTvdStepper::sync_config() const {
+  if (!same(ctl_, pushed_ctl_)) {
+    swf_control k = to_c(ctl_);
+    check(swf_set_control(ctx_, &k));
+    pushed_ctl_ = ctl_;
+  }
+  if (!same(opt_, pushed_opt_)) {
+    swf_options o = to_c(opt_);
+    check(swf_set_options(ctx_, &o));
+    pushed_opt_ = opt_;
+  }
+}
+
+void CsphTvdStepper::set_wind(WindForcing wind) {
+  wind.validate();
+  std::vector<double> t, x, y;
+  for (const WindSample& s : wind.series) {
+    t.push_back(s.t);
+    x.push_back(s.wx);
+    y.push_back(s.wy);
+  }
+  check(swf_set_wind(ctx_, (int)t.size(), t.data(), x.data(), y.data()));
+}
+
+void CsphTvdStepper::set_sources(std::vector<SourceSpec> sources) {
+  for (const SourceSpec& s : sources) s.validate(*terrain_);
+  std::vector<swf_source> v;
+  std::vector<std::vector<double>> keep;
+  for (const SourceSpec& s : sources) {
+    keep.emplace_back();
+    keep.emplace_back();
+    auto& ts = keep[keep.size() - 2];
+    auto& qs = keep.back();
+    for (const HydrographSample& h : s.hydrograph) {
+      ts.push_back(h.t);
+      qs.push_back(h.q);
+    }
+    v.push_back(swf_source{s.kind == SourceSpec::Kind::Rain ? SWF_SOURCE_RAIN : SWF_SOURCE_DISCHARGE,
+                           s.cells.i0, s.cells.j0, s.cells.i1, s.cells.j1, (int)ts.size(),
+                           ts.data(), qs.data(), s.rate, s.source_velocity.x,
+                           s.source_velocity.y});
+  }
+  check(swf_set_sources(ctx_, (int)v.size(), v.data()));
+}
+
+StepInfo CsphTvdStepper::step(FlowState& state, double dt_cap) {
+  if (state.nx != terrain_->nx || state.ny != terrain_->ny)
+    throw ConfigError("stepper: state does not match the terrain grid");
+  sync_config();
+  swf_step_info ci{};
+  check(swf_step_host(ctx_, state.H.data(), state.HUx.data(), state.HUy.data(), &state.t, dt_cap,
+                      &ci));
+  StepInfo s;
+  s.tau = ci.tau;
+  s.active_fraction = ci.active_fraction;
+  s.lagrangian_blocks = ci.lagrangian_blocks;
+  s.flux_blocks = ci.flux_blocks;
+  s.total_blocks = ci.total_blocks;
+  double* tm[8] = {&s.timings.mask,       &s.timings.forces,    &s.timings.dt,
+                   &s.timings.predictor,  &s.timings.mid_forces, &s.timings.corrector,
+                   &s.timings.flux,       &s.timings.finalize};
+  for (int q = 0; q < 8; ++q) *tm[q] = ci.timings[q];
+  s.clamp_deficit_volume = ci.clamp_deficit_volume;
+  s.source_volume = ci.source_volume;
+  s.boundary_outflow_volume = ci.boundary_outflow_volume;
+  return s;
+}
+
+void CsphTvdStepper::begin_step(const FlowState& state) {
+  if (state.nx != terrain_->nx || state.ny != terrain_->ny)
+    throw ConfigError("stepper: state does not match the terrain grid");
+  sync_config();
+  check(swf_upload_state(ctx_, state.H.data(), state.HUx.data(), state.HUy.data(), state.t));
+  check(swf_stage(ctx_, SWF_STAGE_BEGIN, 0.0, nullptr));
+}
+
+void CsphTvdStepper::compute_forces(const FlowState&) { check(swf_stage(ctx_, SWF_STAGE_FORCES, 0.0, nullptr)); }
+
+double CsphTvdStepper::compute_dt(const FlowState&, double dt_cap) const {
+  double tau = 0.0;
+  check(swf_stage(ctx_, SWF_STAGE_DT, dt_cap, &tau));
+  return tau;
+}
+
+void CsphTvdStepper::predictor(const FlowState&, double tau) { check(swf_stage(ctx_, SWF_STAGE_PREDICTOR, tau, nullptr)); }
+void CsphTvdStepper::mid_forces(const FlowState&, double tau) { check(swf_stage(ctx_, SWF_STAGE_MID_FORCES, tau, nullptr)); }
+void CsphTvdStepper::corrector(const FlowState&, double tau) { check(swf_stage(ctx_, SWF_STAGE_CORRECTOR, tau, nullptr)); }
+void CsphTvdStepper::flux(const FlowState&, double tau) { check(swf_stage(ctx_, SWF_STAGE_FLUX, tau, nullptr)); }
+
+void CsphTvdStepper::final_update(FlowState& state, double tau) {
+  check(swf_stage(ctx_, SWF_STAGE_FINAL, tau, nullptr));
+  check(swf_download_state(ctx_, state.H.data(), state.HUx.data(), state.HUy.data(), &state.t));
+}
+
+std::span<const double> CsphTvdStepper::scratch(int which, std::vector<double>& buf) const {
+  buf.resize(terrain_->cells());
+  check(swf_download_scratch(ctx_, which, buf.data()));
+  return buf;
+}
+
+const BlockMask& CsphTvdStepper::mask() const {
+  int nbx = 0, nby = 0;
+  check(swf_download_mask(ctx_, nullptr, nullptr, &nbx, &nby));
+  mask_.block_size = opt_.block_size;
+  mask_.nx = terrain_->nx;
+  mask_.ny = terrain_->ny;
+  mask_.nbx = nbx;
+  mask_.nby = nby;
+  mask_.interior_wet.resize(std::size_t(nbx) * nby);
+  mask_.halo_wet.resize(std::size_t(nbx) * nby);
+  check(swf_download_mask(ctx_, mask_.interior_wet.data(), mask_.halo_wet.data(), &nbx, &nby));
+  return mask_;
+}
+
+const SourceField& CsphTvdStepper::step_sources() const {
+  src_.resize(terrain_->nx, terrain_->ny);
+  check(swf_download_scratch(ctx_, SWF_SCR_SIGMA, src_.sigma.data()));
+  check(swf_download_scratch(ctx_, SWF_SCR_SRC_VX, src_.vx.data()));
+  check(swf_download_scratch(ctx_, SWF_SCR_SRC_VY, src_.vy.data()));
+  for (std::size_t k = 0; k < src_.sigma.size(); ++k) src_.index_q[k] = src_.sigma[k] != 0.0;
+  return src_;
+}
+
+const ForceField& CsphTvdStepper::forces_n() const {
+  f_n_.resize(terrain_->nx, terrain_->ny);
+  check(swf_download_scratch(ctx_, SWF_SCR_FN_FX, f_n_.fx.data()));
+  check(swf_download_scratch(ctx_, SWF_SCR_FN_FY, f_n_.fy.data()));
+  check(swf_download_scratch(ctx_, SWF_SCR_FN_FRIC_X, f_n_.fric_x.data()));
+  check(swf_download_scratch(ctx_, SWF_SCR_FN_FRIC_Y, f_n_.fric_y.data()));
+  check(swf_download_scratch(ctx_, SWF_SCR_FN_SIGMA, f_n_.sigma_eff.data()));
+  return f_n_;
+}
+
+const ForceField& CsphTvdStepper::forces_mid() const {
+  f_mid_.resize(terrain_->nx, terrain_->ny);
+  check(swf_download_scratch(ctx_, SWF_SCR_FM_FX, f_mid_.fx.data()));
+  check(swf_download_scratch(ctx_, SWF_SCR_FM_FY, f_mid_.fy.data()));
+  check(swf_download_scratch(ctx_, SWF_SCR_FM_FRIC_X, f_mid_.fric_x.data()));
+  check(swf_download_scratch(ctx_, SWF_SCR_FM_FRIC_Y, f_mid_.fric_y.data()));
+  check(swf_download_scratch(ctx_, SWF_SCR_FM_SIGMA, f_mid_.sigma_eff.data()));
+  return f_mid_;
+}
+
+std::span<const double> CsphTvdStepper::half_depth() const { return scratch(SWF_SCR_HALF_H, buf_[0]); }
+std::span<const double> CsphTvdStepper::lagrangian_depth() const { return scratch(SWF_SCR_HT, buf_[1]); }
+std::span<const double> CsphTvdStepper::lagrangian_momentum_x() const { return scratch(SWF_SCR_HVTX, buf_[2]); }
+std::span<const double> CsphTvdStepper::lagrangian_momentum_y() const { return scratch(SWF_SCR_HVTY, buf_[3]); }
+std::span<const double> CsphTvdStepper::displacement_x() const { return scratch(SWF_SCR_DRX, buf_[4]); }
+std::span<const double> CsphTvdStepper::displacement_y() const { return scratch(SWF_SCR_DRY, buf_[5]); }
+std::span<const double> CsphTvdStepper::flux_mass() const { return scratch(SWF_SCR_FH, buf_[6]); }
+std::span<const double> CsphTvdStepper::flux_momentum_x() const { return scratch(SWF_SCR_FVX, buf_[7]); }
+std::span<const double> CsphTvdStepper::flux_momentum_y() const { return scratch(SWF_SCR_FVY, buf_[8]); }
+
+double CsphTvdStepper::last_clamp_deficit() const {
+  double v = 0.0;
+  check(swf_last_volumes(ctx_, &v, nullptr, nullptr));
+  return v;
+}
+double CsphTvdStepper::last_source_volume() const {
+  double v = 0.0;
+  check(swf_last_volumes(ctx_, nullptr, &v, nullptr));
+  return v;
+}
+double CsphTvdStepper::last_boundary_outflow() const {
+  double v = 0.0;
+  check(swf_last_volumes(ctx_, nullptr, nullptr, &v));
+  return v;
+}
+
+}  // namespace swflood
