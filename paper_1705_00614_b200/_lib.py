@@ -9,7 +9,7 @@ import os
 from . import _abi as A
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libswflood_cuda.so")
+LIB_PATH = os.environ.get("SWF_LIB") or os.path.join(HERE, "libswflood_cuda.so")
 
 _lib = None
 

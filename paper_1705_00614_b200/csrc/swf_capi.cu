@@ -32,6 +32,10 @@ int cuda_check(swf_ctx* c, cudaError_t e, const char* what) {
 
 size_t local_cells(const swf_ctx* c) { return (size_t)c->geo.nx * (size_t)c->geo.rows; }
 
+void invalidate_mask(swf_ctx* c) {
+  if (c->d_sc) cudaMemsetAsync(&c->d_sc->mask_valid, 0, sizeof(int), c->stream);
+}
+
 void fill_block_counts(const swf_ctx* c, const StepScalars* sc, swf_step_info* info) {
   int total = c->geo.nbx * (c->geo.bj1 - c->geo.bj0);
   info->total_blocks = total;
@@ -263,10 +267,13 @@ int create_impl(const swf_terrain* T, const swf_params* P, const swf_control* K,
   if (e == cudaSuccess) e = cudaMalloc(&c->fpx, bytes);
   if (e == cudaSuccess) e = cudaMalloc(&c->fpy, bytes);
   size_t nt = (size_t)G.tiles_x * G.tiles_y;
-  if (e == cudaSuccess) e = cudaMalloc(&c->d_tile_act, nt ? nt : 1);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_tile_act, 2 * (nt ? nt : 1));
+  if (e == cudaSuccess) e = cudaMemset(c->d_tile_act, 0, 2 * (nt ? nt : 1));
   if (e == cudaSuccess) e = cudaMalloc(&c->d_tile_same, nt ? nt : 1);
   if (e == cudaSuccess) e = cudaMemset(c->d_tile_same, 1, nt ? nt : 1);  // both buffers zero
-  if (e == cudaSuccess) e = cudaMalloc(&c->d_part, 3 * (nt ? nt : 1) * sizeof(double));
+  // per-tile diagnostic partials, then the k_reduce partials
+  if (e == cudaSuccess)
+    e = cudaMalloc(&c->d_part, 5 * ((nt ? nt : 1) + (size_t)fused_reduce_ctas()) * sizeof(double));
   if (e == cudaSuccess) e = cudaMalloc(&c->d_sig, 2 * sizeof(double));
   if (e == cudaSuccess) e = cudaMalloc(&c->d_sc, sizeof(StepScalars));
   if (e == cudaSuccess) e = cudaMallocHost(&c->h_sc, sizeof(StepScalars));
@@ -463,6 +470,7 @@ int swf_set_sources(swf_ctx* c, int n, const swf_source* s) {
   }
   c->geo.nsrc = n;
   if (n == 0) stage_clear_sources(c);  // src_.clear_values(), stepper.cpp:169
+  invalidate_mask(c);
   drop_graph(c);
   return cuda_check(c, e, "set_sources");
 }
@@ -481,6 +489,7 @@ int swf_get_control(const swf_ctx* c, swf_control* k) {
 int swf_set_options(swf_ctx* c, const swf_options* o) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
+  invalidate_mask(c);
   return apply_options(c, o);
 }
 
@@ -502,6 +511,7 @@ int swf_upload_state(swf_ctx* c, const double* H, const double* HUx, const doubl
     e = cudaMemcpyAsync(&c->d_sc->t, &t, sizeof(double), cudaMemcpyHostToDevice, c->stream);
   size_t nt = (size_t)c->geo.tiles_x * c->geo.tiles_y;
   if (e == cudaSuccess && nt) e = cudaMemsetAsync(c->d_tile_same, 0, nt, c->stream);
+  if (e == cudaSuccess) invalidate_mask(c);
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
   c->h_t = t;
   return cuda_check(c, e, "upload_state");
@@ -825,7 +835,11 @@ int swf_strip_phase1(swf_ctx* c, double dt_cap, double* speed_out) {
   if (e != cudaSuccess) return cuda_check(c, e, "strip phase 1");
   rc = check_device_error(c);
   if (rc) return rc;
-  if (speed_out) *speed_out = bitsd(c->h_sc->speed_bits);
+  // the strip's CFL speed: max over the per-CTA slots (k_tau folds them
+  // on the device in the single-context path)
+  unsigned long long mb = c->h_sc->speed_bits;
+  for (int q = 0; q < SPEED_SLOTS; ++q) mb = c->h_sc->speed_slots[q] > mb ? c->h_sc->speed_slots[q] : mb;
+  if (speed_out) *speed_out = bitsd(mb);
   return SWF_OK;
 }
 

@@ -1,25 +1,28 @@
 // swf_fused.cu — the FUSED fast path of one CSPH-TVD step on sm_100a.
 //
-// One step = 6 launches on the context's stream (captured in a CUDA graph
+// One step = 5 launches on the context's stream (captured in a CUDA graph
 // for swf_run):
 //   k_begin   1 thread   sources sigma_s(t_n), wind(t_n), counter reset
-//   k_mask    B-blocks   K1: interior / halo-ring activity counts (block.cpp:16-61)
-//   k_tiles   tiles      fused-tile activity from the B-block flags
-//   k_forces  tiles      K2 + K3: forces on wet cells (stores f - f_fric only)
-//                        and the CFL speed (shuffle + one atomicMax per CTA)
+//   k_forces  tiles      K1 + K2 + K3: the block mask of the tile's B-blocks
+//                        (block.cpp:16-61) and the fused-tile activity flags,
+//                        forces on wet cells (stores f - f_fric only) and the
+//                        CFL speed (shuffle + one atomicMax per CTA)
 //   k_tau     1 thread   tau = min(dt_max, K h / speed, dt_cap); t_mid,
 //                        wind(t_mid), sigma_s(t_mid)  (stepper.cpp:256-266, 311-319)
 //   k_step    tiles      K4..K8 fused: predictor on the tile + 2-cell halo,
-//                        mid forces + corrector on owned cells, x- then y-face
-//                        TVD/HLL fluxes in shared memory, accumulate, final
-//                        update into the other state buffer (ping-pong)
-//   k_finish  1 CTA      fixed-order diagnostics, t += tau
+//                        mid forces + corrector on owned cells, minmod slopes
+//                        once per cell and direction, x- then y-face HLL
+//                        fluxes in shared memory, accumulate, final update
+//                        into the other state buffer (ping-pong)
+//   k_reduce  148 CTAs   fixed-order diagnostics partials; k_finish commits t
+// (block sizes that do not divide 16 use a separate k_mask/k_tiles pair).
 //
 // HBM traffic per wet cell-update: k_forces reads H,HUx,HUy,b (+n) and writes
 // 2 doubles; k_step reads H,HUx,HUy,b,f' (+n) and writes H,HUx,HUy — ≈120 B
-// against the 56 B compulsory minimum; the FP64 pipe, not HBM, bounds this
-// path.  Dry tiles cost one read of H in k_forces and, once
-// after they go dry, one copy between the ping-pong buffers.
+// against the 56 B compulsory minimum; the FP64 pipe and its dependency
+// chains, not HBM, bound this path.  Dry tiles cost one read
+// of H in k_forces and, once after they go dry, one copy between the
+// ping-pong buffers.
 #include <cuda_runtime.h>
 
 #include "swf_internal.cuh"
@@ -28,11 +31,19 @@ namespace swf {
 namespace {
 
 // ---- tiles -----------------------------------------------------------------
-constexpr int AX = 32, AY = 16;  // k_forces tile (owned cells)
-constexpr int AREGX = AX + 2, AREGY = AY + 2, AREG = AREGX * AREGY;
-constexpr int BX = 32, BY = 16;  // k_step tile (owned cells)
-constexpr int RX = BX + 4, RY = BY + 4, RREG = RX * RY;  // 2-cell halo region
+constexpr int BX = 32, BY = 16;  // tile of owned cells (k_forces and k_step)
+constexpr int AX = BX, AY = BY;
+constexpr int AREGX = AX + 2, AREGY = AY + 2, AREG = AREGX * AREGY;  // 1-cell halo
+constexpr int RX = BX + 4, RY = BY + 4, RREG = RX * RY;              // 2-cell halo
 constexpr int NTHR = 256;
+constexpr int RED_CTAS = 148;
+constexpr int NPART_ALLOC = 5;  // doubles per tile in d_part (see k_reduce)
+#ifndef SWF_STEP_MINB
+#define SWF_STEP_MINB 3  // CTAs per SM the register budget of k_step targets
+#endif
+#ifndef SWF_FORCES_MINB
+#define SWF_FORCES_MINB 5
+#endif
 
 __device__ __forceinline__ bool stopped(const StepScalars* sc) { return sc->err_key != ERR_NONE; }
 
@@ -55,6 +66,7 @@ __global__ void k_begin(Geo G, const DevSrc* src, const double* ht, const double
   sc->wind_n[0] = series_at(wt, wv, G.nwind, 2, 0, t);
   sc->wind_n[1] = series_at(wt, wv, G.nwind, 2, 1, t);
   sc->speed_bits = 0ull;
+  for (int q = 0; q < SPEED_SLOTS; ++q) sc->speed_slots[q] = 0ull;
   sc->lag_act = 0;
   sc->flux_act = 0;
   sc->dt_cap = dt_cap;
@@ -83,7 +95,10 @@ __global__ void k_tau(Geo G, const DevSrc* src, const double* ht, const double* 
                       const double* wt, const double* wv, double* sig, StepScalars* sc,
                       double dt_cap, double global_speed) {
   if (stopped(sc)) return;
-  double speed = global_speed >= 0.0 ? global_speed : bitsd(sc->speed_bits);
+  unsigned long long mb = sc->speed_bits;
+  for (int q = 0; q < SPEED_SLOTS; ++q) mb = sc->speed_slots[q] > mb ? sc->speed_slots[q] : mb;
+  sc->speed_bits = mb;
+  double speed = global_speed >= 0.0 ? global_speed : bitsd(mb);
   double tau = G.dt_max;
   if (speed > 0.0) {
     double cfl = (G.courant * G.P.h) / speed;
@@ -169,61 +184,231 @@ __global__ void k_tiles(Geo G, const unsigned char* bflag, unsigned char* tile_a
   tile_act[t] = f;
 }
 
+
+// Bitmask of the source specs whose rectangle meets the global cell box
+// [ci0, ci1] x [cj0, cj1] (at most 32 specs; more -> all bits).  Cells outside
+// a spec's rectangle get nothing from it, so evaluating only the masked
+// specs, in spec order, reproduces the full per-cell sums exactly.
+__device__ __forceinline__ unsigned src_mask_for(const Geo& G, const DevSrc* src, int ci0, int ci1,
+                                                 int cj0, int cj1) {
+  if (G.nsrc > 32) return 0xffffffffu;
+  unsigned m = 0;
+  for (int s = 0; s < G.nsrc; ++s) {
+    const DevSrc& d = src[s];
+    if (d.i0 <= ci1 && d.i1 >= ci0 && d.j0 <= cj1 && d.j1 >= cj0) m |= 1u << s;
+  }
+  return m;
+}
+
+__device__ __forceinline__ double msrc(const Geo& G, const DevSrc* src, const double* sig,
+                                       unsigned mask, int i, int jg, double& vx, double& vy) {
+  double s = 0.0;
+  if (!mask) return s;
+  for (int m = 0; m < G.nsrc; ++m) {
+    if (G.nsrc <= 32 && !((mask >> m) & 1u)) continue;
+    const DevSrc& d = src[m];
+    if (i >= d.i0 && i <= d.i1 && jg >= d.j0 && jg <= d.j1) {
+      s += sig[m];
+      vx = d.vx;
+      vy = d.vy;
+    }
+  }
+  return s;
+}
+
+__device__ __forceinline__ double msig(const Geo& G, const DevSrc* src, const double* sig,
+                                       unsigned mask, int i, int jg) {
+  double vx, vy;
+  return msrc(G, src, sig, mask, i, jg, vx, vy);
+}
+
 // ---------------------------------------------------------------------------
-// k_forces: K2 + K3.  Tile AX x AY owned cells + 1-cell halo in shared memory.
-// Writes f' = (fx - fric_x, fy - fric_y) for wet cells (the only K2 output
-// the predictor needs, stepper.cpp:283-284) and reduces the CFL speed of
-// K3 (stepper.cpp:233-254) with warp shuffles and one atomicMax per CTA.
-// Rows [ra0, ra1) (local): owned rows plus, for strips, 2 ghost rows each
-// side so k_step can run its predictor on its 2-cell halo.
+// k_forces: K1 + K2 + K3 on a BX x BY tile with a 1-cell halo.
+//  * K1 (fused when the block size divides 16): interior / clamped-ring wet
+//    counts of the tile's B-blocks (block.cpp:16-61), block flags, tile flags.
+//  * K2: forces on wet cells; stores f' = (fx - fric_x, fy - fric_y), the only
+//    K2 output the predictor needs (stepper.cpp:283-284).
+//  * K3: the CFL speed of wet cells (stepper.cpp:233-254), shuffle max and
+//    one atomicMax per CTA.
+// Tile rows tr in [tr_lo, tr_hi) relative to the owned rows; forces cover
+// local rows [ra0, ra1) (owned + 2 ghost rows per interior strip side).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(NTHR) k_forces(Geo G, int ra0, int ra1, int tiles_xa,
-                                                 const double* __restrict__ H,
-                                                 const double* __restrict__ HUx,
-                                                 const double* __restrict__ HUy,
-                                                 const double* __restrict__ b,
-                                                 const double* __restrict__ nf,
-                                                 const DevSrc* src, const double* sig,
-                                                 double* __restrict__ fpx,
-                                                 double* __restrict__ fpy, StepScalars* sc) {
+struct ForcesArgs {
+  const double* __restrict__ H;
+  const double* __restrict__ HUx;
+  const double* __restrict__ HUy;
+  const double* __restrict__ b;
+  const double* __restrict__ nf;
+  const DevSrc* src;
+  const double* sig;
+  double* __restrict__ fpx;
+  double* __restrict__ fpy;
+  int* interior;
+  int* halo;
+  unsigned char* bflag;
+  unsigned char* tile_act;
+  StepScalars* sc;
+  double* cnt_part;  // per-tile diagnostics partials: slots 3, 4 = block counts
+  const unsigned char* tile_prev;  // tile flags of the previous step
+  int ra0, ra1, tr_lo, do_mask;
+};
+
+__global__ void __launch_bounds__(NTHR, SWF_FORCES_MINB) k_forces(Geo G, ForcesArgs A) {
   __shared__ double s_d[AREG], s_e[AREG], s_u[AREG], s_v[AREG];
+  __shared__ unsigned char s_w[AREG];
+  __shared__ int s_cnt[3];
+  __shared__ unsigned s_srcm;
+  __shared__ unsigned long long s_max[NTHR / 32];
+  StepScalars* sc = A.sc;
   if (stopped(sc)) return;
   const PhysConst& P = G.P;
-  int tx = blockIdx.x % tiles_xa, ty = blockIdx.x / tiles_xa;
-  int i0 = tx * AX, rr0 = ra0 + ty * AY;
-  int tid = threadIdx.x;
-  // activity: any wet owned cell in the tile?
-  bool anywet = false;
-  for (int c = tid; c < AX * AY; c += NTHR) {
-    int i = i0 + c % AX, r = rr0 + c / AX;
-    if (i < G.nx && r < ra1) anywet |= H[(size_t)i + (size_t)r * G.nx] > P.eps;
+  const int tid = threadIdx.x;
+  const int tx = blockIdx.x % G.tiles_x, tr = (int)(blockIdx.x / G.tiles_x) + A.tr_lo;
+  const int i0 = tx * BX, rr0 = G.r0 + tr * BY;
+  const size_t nx = G.nx;
+  // mask rows (owned rows only)
+  const bool mask_tile = A.do_mask && tr >= 0 && tr < G.tiles_y;
+  if (tid == 0) {
+    unsigned m = src_mask_for(G, A.src, i0 - 1, i0 + BX, G.jg0 + rr0 - 1, G.jg0 + rr0 + BY);
+    s_srcm = m;
+    // Dry neighbourhood: if this tile and its 8 neighbours had no flux-active
+    // block in the previous step, k_step left all their cells untouched, so
+    // this tile's block counts, flags and (empty) forces are unchanged: skip.
+    // Not across a strip boundary (ghost rows change by exchange) and not
+    // near a source (sigma(t) can switch a marker on).
+    int skip = 0;
+    if (mask_tile && G.skip && !m && sc->mask_valid && (tr > 0 || G.r0 == 0) &&
+        (tr < G.tiles_y - 1 || G.r1 == G.rows)) {
+      skip = 1;
+      for (int dy = -1; dy <= 1 && skip; ++dy)
+        for (int dx = -1; dx <= 1; ++dx) {
+          int x2 = tx + dx, y2 = tr + dy;
+          if (x2 < 0 || x2 >= G.tiles_x || y2 < 0 || y2 >= G.tiles_y) continue;
+          if (A.tile_prev[x2 + y2 * G.tiles_x]) {
+            skip = 0;
+            break;
+          }
+        }
+      if (skip) A.tile_act[tx + tr * G.tiles_x] = 0;
+    }
+    s_cnt[2] = skip;
   }
-  if (!__syncthreads_or(anywet)) return;
+  __syncthreads();
+  if (s_cnt[2]) return;
+  const unsigned srcm = s_srcm;
+  // forces rows of this tile
+  const int fa = max(rr0, A.ra0), fb = min(rr0 + BY, A.ra1);
+
+  // ---- region H + wet flags (wet = H > eps or an active source, K1) ---------
+  bool anywet = false;
   for (int c = tid; c < AREG; c += NTHR) {
     int i = i0 - 1 + c % AREGX, r = rr0 - 1 + c / AREGX;
-    double d = 0.0, e = 0.0, u = 0.0, v = 0.0;
+    double d = 0.0;
+    unsigned char w = 0;
     if (i >= 0 && i < G.nx && r >= 0 && r < G.rows) {
-      size_t k = (size_t)i + (size_t)r * G.nx;
-      d = H[k];
-      e = d + b[k];
-      if (d > P.eps) {
-        u = HUx[k] / d;
-        v = HUy[k] / d;
-      }
+      d = A.H[(size_t)i + (size_t)r * nx];
+      bool wet = d > P.eps;
+      w = wet || (srcm && msig(G, A.src, A.sig, srcm, i, G.jg0 + r) != 0.0);
+      int x = c % AREGX - 1, y = c / AREGX - 1;
+      if (wet && x >= 0 && x < BX && y >= 0 && y < BY && r >= fa && r < fb) anywet = true;
     }
     s_d[c] = d;
+    s_w[c] = w;
+  }
+  if (tid < 3) s_cnt[tid] = 0;
+  anywet = __syncthreads_or(anywet);
+
+  // ---- K1: block counts of the tile's B-blocks ------------------------------
+  // One warp per block: interior cells and the clamped one-cell ring
+  // (corners included, block.cpp:36-56) counted with ballots; no atomics on
+  // global counters — the per-tile counts go to the diagnostics partials.
+  if (mask_tile) {
+    const int bs = G.bs, nbxt = BX / bs, nbyt = BY / bs, nbt = nbxt * nbyt;
+    const int rend = min(rr0 + BY, G.r1);
+    const int lane = tid & 31, warp = tid >> 5;
+    for (int blk = warp; blk < nbt; blk += NTHR / 32) {
+      int bx = blk % nbxt, by = blk / nbxt;
+      int bi0 = i0 + bx * bs, br0 = rr0 + by * bs;  // block origin (global col, local row)
+      if (bi0 >= G.nx || br0 >= rend) continue;
+      int bi1 = min(bi0 + bs - 1, G.nx - 1), br1 = min(br0 + bs - 1, rend - 1);
+      int wdt = bi1 - bi0 + 1, hgt = br1 - br0 + 1;
+      int in = 0, ring = 0;
+      // bs is a power of two (it divides 16): shifts instead of divisions
+      const int lg = __ffs(bs) - 1;
+      for (int p = lane; p < bs * bs; p += 32) {
+        int px = p & (bs - 1), py = p >> lg;
+        if (px < wdt && py < hgt)
+          in += s_w[(bi0 + px - (i0 - 1)) + (br0 + py - (rr0 - 1)) * AREGX];
+      }
+      const int top = wdt + 2, per = 2 * top + 2 * hgt;
+      for (int q = lane; q < per; q += 32) {
+        int ci, cj;  // global, then clamped into the domain
+        if (q < top) {
+          ci = bi0 - 1 + q;
+          cj = G.jg0 + br0 - 1;
+        } else if (q < 2 * top) {
+          ci = bi0 - 1 + (q - top);
+          cj = G.jg0 + br1 + 1;
+        } else {
+          int qq = q - 2 * top;
+          cj = G.jg0 + br0 + (qq >> 1);
+          ci = (qq & 1) ? bi1 + 1 : bi0 - 1;
+        }
+        ci = min(max(ci, 0), G.nx - 1);
+        cj = min(max(cj, 0), G.ny - 1);
+        ring += s_w[(ci - (i0 - 1)) + ((cj - G.jg0) - (rr0 - 1)) * AREGX];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        in += __shfl_xor_sync(0xffffffffu, in, o);
+        ring += __shfl_xor_sync(0xffffffffu, ring, o);
+      }
+      if (lane == 0) {
+        int lb = (bi0 / bs) + ((G.jg0 + br0) / bs - G.bj0) * G.nbx;
+        A.interior[lb] = in;
+        A.halo[lb] = ring;
+        bool l = in > 0, f = l || ring > 0;
+        A.bflag[lb] = (l ? 1 : 0) | (f ? 2 : 0);
+        if (l) atomicAdd(&s_cnt[0], 1);
+        if (f) atomicAdd(&s_cnt[1], 1);
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int t = tx + tr * G.tiles_x;
+      A.tile_act[t] = G.skip ? ((s_cnt[0] ? 1 : 0) | (s_cnt[1] ? 2 : 0)) : 3;
+      A.cnt_part[5 * (size_t)t + 3] = s_cnt[0];
+      A.cnt_part[5 * (size_t)t + 4] = s_cnt[1];
+    }
+  }
+  if (!anywet) return;
+
+  // ---- region momentum -> eta, velocity ---------------------------------------
+  for (int c = tid; c < AREG; c += NTHR) {
+    int i = i0 - 1 + c % AREGX, r = rr0 - 1 + c / AREGX;
+    double e = 0.0, u = 0.0, v = 0.0;
+    if (i >= 0 && i < G.nx && r >= 0 && r < G.rows) {
+      size_t k = (size_t)i + (size_t)r * nx;
+      double d = s_d[c];
+      e = d + A.b[k];
+      if (d > P.eps) {
+        u = A.HUx[k] / d;
+        v = A.HUy[k] / d;
+      }
+    }
     s_e[c] = e;
     s_u[c] = u;
     s_v[c] = v;
   }
   __syncthreads();
+
+  // ---- K2 forces + K3 speed on wet cells ------------------------------------
   double m = 0.0;
-  double wx = sc->wind_n[0], wy = sc->wind_n[1];
-  const double* sig_n = sig;
+  const double wx = sc->wind_n[0], wy = sc->wind_n[1];
   for (int c = tid; c < AX * AY; c += NTHR) {
     int x = c % AX, y = c / AX;
     int i = i0 + x, r = rr0 + y;
-    if (i >= G.nx || r >= ra1) continue;
+    if (i >= G.nx || r < fa || r >= fb) continue;
     int s = (x + 1) + (y + 1) * AREGX;
     double d = s_d[s];
     if (!(d > P.eps)) continue;
@@ -240,14 +425,14 @@ __global__ void __launch_bounds__(NTHR) k_forces(Geo G, int ra0, int ra1, int ti
     Nbr W = nb(i > 0, s - 1), E = nb(i + 1 < G.nx, s + 1);
     Nbr S = nb(jg > 0, s - AREGX), N = nb(jg + 1 < G.ny, s + AREGX);
     double sg = 0.0, svx = 0.0, svy = 0.0;
-    if (G.nsrc > 0) sg = cell_source(src, sig_n, G.nsrc, i, jg, svx, svy);
-    size_t k = (size_t)i + (size_t)r * G.nx;
-    double n = G.has_nfield ? nf[k] : G.n_manning;
+    if (srcm) sg = msrc(G, A.src, A.sig, srcm, i, jg, svx, svy);
+    size_t k = (size_t)i + (size_t)r * nx;
+    double n = G.has_nfield ? A.nf[k] : G.n_manning;
     double ux = s_u[s], uy = s_v[s];
     ForceOut o = cell_forces(d, ux, uy, s_e[s], W, E, S, N, n, P, G.nwind > 0, wx, wy, sg, svx,
                              svy);
-    fpx[k] = o.fx - o.frx;
-    fpy[k] = o.fy - o.fry;
+    A.fpx[k] = o.fx - o.frx;
+    A.fpy[k] = o.fy - o.fry;
     m = cfl_speed(m, d, ux, uy, o.fx, o.fy, P.g, P.h);
   }
   unsigned long long bits = dbits(m);
@@ -256,13 +441,13 @@ __global__ void __launch_bounds__(NTHR) k_forces(Geo G, int ra0, int ra1, int ti
     unsigned long long ob = __shfl_xor_sync(0xffffffffu, bits, o);
     bits = ob > bits ? ob : bits;
   }
-  __shared__ unsigned long long s_max[NTHR / 32];
   if ((tid & 31) == 0) s_max[tid >> 5] = bits;
   __syncthreads();
   if (tid == 0) {
     unsigned long long mb = 0;
     for (int w = 0; w < NTHR / 32; ++w) mb = s_max[w] > mb ? s_max[w] : mb;
-    if (mb) atomicMax(&sc->speed_bits, mb);
+    // spread over SPEED_SLOTS addresses to avoid one contended L2 atomic
+    if (mb) atomicMax(&sc->speed_slots[blockIdx.x % SPEED_SLOTS], mb);
   }
 }
 
@@ -270,8 +455,10 @@ __global__ void __launch_bounds__(NTHR) k_forces(Geo G, int ra0, int ra1, int ti
 // k_step: K4..K8 fused over a BX x BY tile.
 // ---------------------------------------------------------------------------
 
-// shared-memory layout of the 2-cell-halo region (RX x RY), half-step view
-enum { F_D = 0, F_E, F_U, F_V, F_SX, F_SY, F_B, F_HN, F_QX, F_QY, F_NUM };
+// shared-memory fields of the 2-cell-halo region (RX x RY), half-step view
+enum { F_D = 0, F_E, F_U, F_V, F_SX, F_SY, F_B, F_NUM };
+constexpr int NSL = (BX + 2) * BY > BX * (BY + 2) ? (BX + 2) * BY : BX * (BY + 2);  // slopes
+constexpr int NFC = (BX + 1) * BY > BX * (BY + 1) ? (BX + 1) * BY : BX * (BY + 1);  // faces
 
 struct StepArgs {
   const double* __restrict__ H;
@@ -323,19 +510,81 @@ __device__ __forceinline__ unsigned long long fused_flux_key(const Geo& G,
   return (ERR_FLUX << 58) | ((unsigned long long)ib << 24) | (pmax - (unsigned long long)p);
 }
 
-__global__ void __launch_bounds__(NTHR, 2) k_step(Geo G, StepArgs A) {
+// Minmod slopes of one wet cell along one direction.  reconstruct_side
+// (stepper.cpp:95-111) computes, for the face on the cell's + side,
+// minmod((X[k+1]-X[k])/d_in, (X[k]-X[k-1])/d_out) and for the face on its
+// - side the same two quotients negated in numerator and denominator and in
+// swapped order; IEEE division is sign-symmetric and minmod is symmetric, so
+// both faces use identical slopes and each cell computes them once.
+struct Slopes {
+  double eta, un, ut;
+};
+
+__device__ __forceinline__ Slopes cell_slopes(double em, double um, double tm, double sm, double ec,
+                                              double uc, double tc, double sc_, double ep, double up,
+                                              double tp, double sp, double h) {
+  // the + side face: in = +1 neighbour, out = -1 neighbour, sgn = +1
+  double p_in = 1.0 * h + sp;
+  double p_out = -1.0 * h + sm;
+  double d_in = p_in - sc_;
+  double d_out = sc_ - p_out;
+  Slopes s;
+  s.eta = minmod((ep - ec) / d_in, (ec - em) / d_out);
+  s.un = minmod((up - uc) / d_in, (uc - um) / d_out);
+  s.ut = minmod((tp - tc) / d_in, (tc - tm) / d_out);
+  return s;
+}
+
+// One side of a face from the cell's slopes (stepper.cpp:112-122).
+__device__ __forceinline__ SideState side_from_slopes(double eta, double un, double ut, double sh,
+                                                      double b_k, const Slopes& s, double face,
+                                                      double b_face) {
+  SideState r;
+  r.hs = 0.0;
+  r.hcell = 0.0;
+  r.un = 0.0;
+  r.ut = 0.0;
+  double off = face - sh;
+  double eta_f = eta + s.eta * off;
+  r.hcell = smax(0.0, eta_f - b_k);
+  if (r.hcell <= 0.0) {
+    r.hcell = 0.0;
+    return r;
+  }
+  r.hs = smax(0.0, eta_f - b_face);
+  r.un = un + s.un * off;
+  r.ut = ut + s.ut * off;
+  return r;
+}
+
+__device__ __forceinline__ FaceRec face_from_sides(bool wetA, bool wetB, const SideState& L,
+                                                   const SideState& R, double g) {
+  FaceRec rec;
+  rec.fm = rec.fnl = rec.fnr = rec.ft = 0.0;
+  if (!wetA && !wetB) return rec;
+  FaceFlux F = hll_face_flux(L.hs, L.un, L.ut, R.hs, R.un, R.ut, g);
+  rec.fm = F.fm;
+  rec.ft = F.ft;
+  rec.fnl = (F.fn - ((0.5 * g) * L.hs) * L.hs) + ((0.5 * g) * L.hcell) * L.hcell;
+  rec.fnr = (F.fn - ((0.5 * g) * R.hs) * R.hs) + ((0.5 * g) * R.hcell) * R.hcell;
+  return rec;
+}
+
+__global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A) {
   extern __shared__ double smem[];
-  double* R = smem;                  // F_NUM x RREG
-  double* FB = smem + F_NUM * RREG;  // face buffer: 4 x 544
-  constexpr int NF = (BX + 1) * BY > BX * (BY + 1) ? (BX + 1) * BY : BX * (BY + 1);
+  double* R = smem;                       // F_NUM x RREG
+  double* SL = smem + F_NUM * RREG;       // 3 x NSL slopes (eta, un, ut)
+  double* FB = SL + 3 * NSL;              // 4 x NFC faces (fm, fnl, fnr, ft)
+  __shared__ unsigned s_srcm;
+  __shared__ double s_red[3][NTHR / 32];
   const PhysConst& P = G.P;
   StepScalars* sc = A.sc;
   if (stopped(sc)) return;
   const int tid = threadIdx.x;
   const int tile = blockIdx.x;
   const int tx = tile % G.tiles_x, ty = tile / G.tiles_x;
-  const int i0 = tx * BX;        // first owned column
-  const int r0 = G.r0 + ty * BY; // first owned local row
+  const int i0 = tx * BX;         // first owned column
+  const int r0 = G.r0 + ty * BY;  // first owned local row
   const size_t nx = G.nx;
 
   // ---- inactive tile: keep the step-start state (skip semantics) ----------
@@ -352,14 +601,14 @@ __global__ void __launch_bounds__(NTHR, 2) k_step(Geo G, StepArgs A) {
       }
       if (tid == 0) A.tile_same[tile] = 1;
     }
-    if (tid == 0) {
-      A.part[3 * tile + 0] = 0.0;
-      A.part[3 * tile + 1] = 0.0;
-      A.part[3 * tile + 2] = 0.0;
-    }
+    if (tid < 3) A.part[5 * (size_t)tile + tid] = 0.0;
     return;
   }
 
+  if (tid == 0)
+    s_srcm = src_mask_for(G, A.src, i0 - 2, i0 + BX + 1, G.jg0 + r0 - 2, G.jg0 + r0 + BY + 1);
+  __syncthreads();
+  const unsigned srcm = s_srcm;
   const double tau = sc->tau;
   const double half_tau = 0.5 * tau;
   const int nsrc = G.nsrc;
@@ -370,23 +619,19 @@ __global__ void __launch_bounds__(NTHR, 2) k_step(Geo G, StepArgs A) {
   for (int c = tid; c < RREG; c += NTHR) {
     int i = i0 - 2 + c % RX, r = r0 - 2 + c / RX;
     double d = 0.0, e = 0.0, u = 0.0, v = 0.0, sx = 0.0, sy = 0.0, bb = 0.0;
-    double Hn = 0.0, qxn = 0.0, qyn = 0.0;
     if (i >= 0 && i < G.nx && r >= 0 && r < G.rows) {
       size_t k = (size_t)i + (size_t)r * nx;
-      Hn = A.H[k];
-      qxn = A.HUx[k];
-      qyn = A.HUy[k];
+      double Hn = A.H[k];
+      double mx = A.HUx[k], my = A.HUy[k];
       bb = A.b[k];
-      double sg = 0.0;
-      if (nsrc > 0) sg = cell_sigma_only(A.src, sig_n, nsrc, i, G.jg0 + r);
+      double sg = srcm ? msig(G, A.src, sig_n, srcm, i, G.jg0 + r) : 0.0;
       bool act = Hn > P.eps || sg != 0.0;
       d = Hn;
-      double mx = qxn, my = qyn;
       if (act) {
         bool wet = Hn > P.eps;
         double fx = wet ? A.fpx[k] : 0.0, fy = wet ? A.fpy[k] : 0.0;
         double n = G.has_nfield ? A.nf[k] : G.n_manning;
-        predict_cell(Hn, qxn, qyn, sg, fx, fy, n, half_tau, P.eps, P.g, d, mx, my);
+        predict_cell(Hn, mx, my, sg, fx, fy, n, half_tau, P.eps, P.g, d, mx, my);
       }
       e = d + bb;
       if (d > P.eps) {
@@ -407,15 +652,13 @@ __global__ void __launch_bounds__(NTHR, 2) k_step(Geo G, StepArgs A) {
     R[F_SX * RREG + c] = sx;
     R[F_SY * RREG + c] = sy;
     R[F_B * RREG + c] = bb;
-    R[F_HN * RREG + c] = Hn;
-    R[F_QX * RREG + c] = qxn;
-    R[F_QY * RREG + c] = qyn;
   }
   __syncthreads();
 
   // ---- phase 2: K5 mid forces + K6 corrector on owned active cells ---------
   constexpr int PER = BX * BY / NTHR;  // owned cells per thread (2)
   double Ht[PER], Qx[PER], Qy[PER];
+  unsigned actbits = 0;
   double srcvol = 0.0;
   const double wmx = sc->wind_mid[0], wmy = sc->wind_mid[1];
 #pragma unroll
@@ -429,15 +672,16 @@ __global__ void __launch_bounds__(NTHR, 2) k_step(Geo G, StepArgs A) {
     if (i >= G.nx || r >= G.r1) continue;
     int s = (x + 2) + (y + 2) * RX;
     int jg = G.jg0 + r;
-    double Hn = R[F_HN * RREG + s];
+    size_t k = (size_t)i + (size_t)r * nx;
+    double Hn = A.H[k];
     double sgn_ = 0.0, svx = 0.0, svy = 0.0, sgm = 0.0;
-    if (nsrc > 0) {
-      sgn_ = cell_source(A.src, sig_n, nsrc, i, jg, svx, svy);
-      sgm = cell_sigma_only(A.src, sig_m, nsrc, i, jg);
+    if (srcm) {
+      sgn_ = msrc(G, A.src, sig_n, srcm, i, jg, svx, svy);
+      sgm = msig(G, A.src, sig_m, srcm, i, jg);
     }
     bool act = Hn > P.eps || sgn_ != 0.0;
     if (!act) continue;
-    size_t k = (size_t)i + (size_t)r * nx;
+    actbits |= 1u << m;
     double n = G.has_nfield ? A.nf[k] : G.n_manning;
     double d = R[F_D * RREG + s];  // H12
     double fmx = 0.0, fmy = 0.0;
@@ -460,8 +704,8 @@ __global__ void __launch_bounds__(NTHR, 2) k_step(Geo G, StepArgs A) {
       fmy = o.fy - o.fry;
     }
     double ht, qx, qy, sv;
-    correct_cell(Hn, R[F_QX * RREG + s], R[F_QY * RREG + s], nsrc > 0, sgm, d, fmx, fmy, n, tau,
-                 P.eps, P.g, ht, qx, qy, sv);
+    correct_cell(Hn, A.HUx[k], A.HUy[k], nsrc > 0, sgm, d, fmx, fmy, n, tau, P.eps, P.g, ht, qx,
+                 qy, sv);
     srcvol += sv;
     // CFL abort (stepper.cpp:378-380, 391-399): dr = tau * u12
     double dx = tau * R[F_U * RREG + s], dy = tau * R[F_V * RREG + s];
@@ -476,18 +720,31 @@ __global__ void __launch_bounds__(NTHR, 2) k_step(Geo G, StepArgs A) {
     Qy[m] = qy;
   }
 
-  // ---- phase 3: x faces (stepper.cpp:402-447, 496-516) -----------------------
-  double px_m[PER], px_a[PER], px_c[PER];  // (W.fm-E.fm), (W.fnr-E.fnl), (W.ft-E.ft)
+  // ---- phase 3x: x slopes of columns -1..BX (rows of the tile) -------------
+  for (int c = tid; c < (BX + 2) * BY; c += NTHR) {
+    int xx = c % (BX + 2), y = c / (BX + 2);
+    int i = i0 - 1 + xx;
+    int s = (xx + 1) + (y + 2) * RX;
+    double se = 0.0, su = 0.0, st = 0.0;
+    if (i > 0 && i + 1 < G.nx && R[F_D * RREG + s] > P.eps) {
+      Slopes q = cell_slopes(R[F_E * RREG + s - 1], R[F_U * RREG + s - 1], R[F_V * RREG + s - 1],
+                             R[F_SX * RREG + s - 1], R[F_E * RREG + s], R[F_U * RREG + s],
+                             R[F_V * RREG + s], R[F_SX * RREG + s], R[F_E * RREG + s + 1],
+                             R[F_U * RREG + s + 1], R[F_V * RREG + s + 1], R[F_SX * RREG + s + 1],
+                             P.h);
+      se = q.eta;
+      su = q.un;
+      st = q.ut;
+    }
+    SL[0 * NSL + c] = se;
+    SL[1 * NSL + c] = su;
+    SL[2 * NSL + c] = st;
+  }
+  __syncthreads();
+
+  // ---- phase 4x: x faces (stepper.cpp:402-447, 496-516) ----------------------
   double outflow = 0.0;
-  auto lc = [&](int s, int dir) {
-    LineCell L;
-    L.depth = R[F_D * RREG + s];
-    L.eta = R[F_E * RREG + s];
-    L.un = R[(dir == 0 ? F_U : F_V) * RREG + s];
-    L.ut = R[(dir == 0 ? F_V : F_U) * RREG + s];
-    L.sh = R[(dir == 0 ? F_SX : F_SY) * RREG + s];
-    return L;
-  };
+  const double face_p = (1.0 * 0.5) * P.h, face_m = (-1.0 * 0.5) * P.h;
   for (int c = tid; c < (BX + 1) * BY; c += NTHR) {
     int fx = c % (BX + 1), y = c / (BX + 1);
     int f = i0 + fx, r = r0 + y;
@@ -505,38 +762,78 @@ __global__ void __launch_bounds__(NTHR, 2) k_step(Geo G, StepArgs A) {
                             lo ? G.west_refl : G.east_refl, P.g);
         outflow += lo ? -rec.fm : rec.fm;
       } else {
-        bool has_m = f - 2 >= 0, has_p = f + 1 < G.nx;
-        rec = interior_face(lc(sa - 1, 0), has_m, lc(sa, 0), R[F_B * RREG + sa], lc(sa + 1, 0),
-                            R[F_B * RREG + sa + 1], lc(sa + 2, 0), has_p, P.eps, P.g, P.h);
-        if (!face_finite(rec)) atomicMin(&sc->err_key, fused_flux_key(G, A.bflag, 0, jg, f));
+        int la = fx + y * (BX + 2), lb = la + 1;  // slope slots of cells f-1, f
+        double dA = R[F_D * RREG + sa], dB = R[F_D * RREG + sa + 1];
+        bool wetA = dA > P.eps, wetB = dB > P.eps;
+        if (wetA || wetB) {
+          double bA = R[F_B * RREG + sa], bB = R[F_B * RREG + sa + 1];
+          double bf = smax(bA, bB);
+          SideState L, Rr;
+          L.hs = L.hcell = L.un = L.ut = 0.0;
+          Rr = L;
+          if (wetA) {
+            Slopes q = {SL[la], SL[NSL + la], SL[2 * NSL + la]};
+            L = side_from_slopes(R[F_E * RREG + sa], R[F_U * RREG + sa], R[F_V * RREG + sa],
+                                 R[F_SX * RREG + sa], bA, q, face_p, bf);
+          }
+          if (wetB) {
+            Slopes q = {SL[lb], SL[NSL + lb], SL[2 * NSL + lb]};
+            Rr = side_from_slopes(R[F_E * RREG + sa + 1], R[F_U * RREG + sa + 1],
+                                  R[F_V * RREG + sa + 1], R[F_SX * RREG + sa + 1], bB, q, face_m,
+                                  bf);
+          }
+          rec = face_from_sides(wetA, wetB, L, Rr, P.g);
+          if (!face_finite(rec)) atomicMin(&sc->err_key, fused_flux_key(G, A.bflag, 0, jg, f));
+        }
       }
     }
-    FB[0 * NF + c] = rec.fm;
-    FB[1 * NF + c] = rec.fnl;
-    FB[2 * NF + c] = rec.fnr;
-    FB[3 * NF + c] = rec.ft;
+    FB[0 * NFC + c] = rec.fm;
+    FB[1 * NFC + c] = rec.fnl;
+    FB[2 * NFC + c] = rec.fnr;
+    FB[3 * NFC + c] = rec.ft;
   }
   __syncthreads();
+  double px_m[PER], px_a[PER], px_c[PER];  // (W.fm-E.fm), (W.fnr-E.fnl), (W.ft-E.ft)
 #pragma unroll
   for (int m = 0; m < PER; ++m) {
     int c = tid + m * NTHR;
     int x = c % BX, y = c / BX;
     int w = x + y * (BX + 1), e = w + 1;
-    px_m[m] = FB[0 * NF + w] - FB[0 * NF + e];
-    px_a[m] = FB[2 * NF + w] - FB[1 * NF + e];
-    px_c[m] = FB[3 * NF + w] - FB[3 * NF + e];
+    px_m[m] = FB[0 * NFC + w] - FB[0 * NFC + e];
+    px_a[m] = FB[2 * NFC + w] - FB[1 * NFC + e];
+    px_c[m] = FB[3 * NFC + w] - FB[3 * NFC + e];
+  }
+
+  // ---- phase 3y: y slopes of rows -1..BY (columns of the tile) -------------
+  for (int c = tid; c < BX * (BY + 2); c += NTHR) {
+    int x = c % BX, yy = c / BX;
+    int r = r0 - 1 + yy, jg = G.jg0 + r;
+    int s = (x + 2) + (yy + 1) * RX;
+    double se = 0.0, su = 0.0, st = 0.0;
+    if (jg > 0 && jg + 1 < G.ny && i0 + x < G.nx && R[F_D * RREG + s] > P.eps) {
+      Slopes q = cell_slopes(R[F_E * RREG + s - RX], R[F_V * RREG + s - RX],
+                             R[F_U * RREG + s - RX], R[F_SY * RREG + s - RX], R[F_E * RREG + s],
+                             R[F_V * RREG + s], R[F_U * RREG + s], R[F_SY * RREG + s],
+                             R[F_E * RREG + s + RX], R[F_V * RREG + s + RX],
+                             R[F_U * RREG + s + RX], R[F_SY * RREG + s + RX], P.h);
+      se = q.eta;
+      su = q.un;
+      st = q.ut;
+    }
+    SL[0 * NSL + c] = se;
+    SL[1 * NSL + c] = su;
+    SL[2 * NSL + c] = st;
   }
   __syncthreads();
 
-  // ---- phase 4: y faces (stepper.cpp:449-494, 518-538) -----------------------
+  // ---- phase 4y: y faces (stepper.cpp:449-494, 518-538) ----------------------
   for (int c = tid; c < BX * (BY + 1); c += NTHR) {
     int x = c % BX, fy = c / BX;
     int i = i0 + x, rf = r0 + fy;  // face between local rows rf-1 and rf
     int jf = G.jg0 + rf;           // global face index
     FaceRec rec;
     rec.fm = rec.fnl = rec.fnr = rec.ft = 0.0;
-    bool owned_face = i < G.nx && (rf < G.r1 || (rf == G.r1 && fy <= BY));
-    if (owned_face && rf <= G.r1) {
+    if (i < G.nx && rf <= G.r1) {
       int sa = (x + 2) + (fy + 1) * RX;  // cell rf-1
       if (jf == 0 || jf == G.ny) {
         bool lo = jf == 0;
@@ -547,17 +844,35 @@ __global__ void __launch_bounds__(NTHR, 2) k_step(Geo G, StepArgs A) {
                             lo ? G.south_refl : G.north_refl, P.g);
         outflow += lo ? -rec.fm : rec.fm;
       } else {
-        bool has_m = jf - 2 >= 0, has_p = jf + 1 < G.ny;
-        rec = interior_face(lc(sa - RX, 1), has_m, lc(sa, 1), R[F_B * RREG + sa],
-                            lc(sa + RX, 1), R[F_B * RREG + sa + RX], lc(sa + 2 * RX, 1), has_p,
-                            P.eps, P.g, P.h);
-        if (!face_finite(rec)) atomicMin(&sc->err_key, fused_flux_key(G, A.bflag, 1, i, jf));
+        int la = x + fy * BX, lb = la + BX;  // slope slots of rows rf-1, rf
+        double dA = R[F_D * RREG + sa], dB = R[F_D * RREG + sa + RX];
+        bool wetA = dA > P.eps, wetB = dB > P.eps;
+        if (wetA || wetB) {
+          double bA = R[F_B * RREG + sa], bB = R[F_B * RREG + sa + RX];
+          double bf = smax(bA, bB);
+          SideState L, Rr;
+          L.hs = L.hcell = L.un = L.ut = 0.0;
+          Rr = L;
+          if (wetA) {
+            Slopes q = {SL[la], SL[NSL + la], SL[2 * NSL + la]};
+            L = side_from_slopes(R[F_E * RREG + sa], R[F_V * RREG + sa], R[F_U * RREG + sa],
+                                 R[F_SY * RREG + sa], bA, q, face_p, bf);
+          }
+          if (wetB) {
+            Slopes q = {SL[lb], SL[NSL + lb], SL[2 * NSL + lb]};
+            Rr = side_from_slopes(R[F_E * RREG + sa + RX], R[F_V * RREG + sa + RX],
+                                  R[F_U * RREG + sa + RX], R[F_SY * RREG + sa + RX], bB, q,
+                                  face_m, bf);
+          }
+          rec = face_from_sides(wetA, wetB, L, Rr, P.g);
+          if (!face_finite(rec)) atomicMin(&sc->err_key, fused_flux_key(G, A.bflag, 1, i, jf));
+        }
       }
     }
-    FB[0 * NF + c] = rec.fm;
-    FB[1 * NF + c] = rec.fnl;
-    FB[2 * NF + c] = rec.fnr;
-    FB[3 * NF + c] = rec.ft;
+    FB[0 * NFC + c] = rec.fm;
+    FB[1 * NFC + c] = rec.fnl;
+    FB[2 * NFC + c] = rec.fnr;
+    FB[3 * NFC + c] = rec.ft;
   }
   __syncthreads();
 
@@ -573,19 +888,18 @@ __global__ void __launch_bounds__(NTHR, 2) k_step(Geo G, StepArgs A) {
     int jg = G.jg0 + r;
     int s = (x + 2) + (y + 2) * RX;
     size_t k = (size_t)i + (size_t)r * nx;
-    double Hn = R[F_HN * RREG + s], qxn = R[F_QX * RREG + s], qyn = R[F_QY * RREG + s];
     int lb = i / G.bs + (jg / G.bs - G.bj0) * G.nbx;
     bool flux_on = !G.skip || (A.bflag[lb] & 2);
     if (!flux_on) {  // block skipped by the reference: state unchanged
-      A.Ho[k] = Hn;
-      A.HUxo[k] = qxn;
-      A.HUyo[k] = qyn;
+      A.Ho[k] = A.H[k];
+      A.HUxo[k] = A.HUx[k];
+      A.HUyo[k] = A.HUy[k];
       continue;
     }
     int sf = x + y * BX, nf_ = sf + BX;  // S and N face of the cell
-    double py_m = FB[0 * NF + sf] - FB[0 * NF + nf_];
-    double py_a = FB[2 * NF + sf] - FB[1 * NF + nf_];  // S.fnr - N.fnl
-    double py_c = FB[3 * NF + sf] - FB[3 * NF + nf_];  // S.ft - N.ft
+    double py_m = FB[0 * NFC + sf] - FB[0 * NFC + nf_];
+    double py_a = FB[2 * NFC + sf] - FB[1 * NFC + nf_];  // S.fnr - N.fnl
+    double py_c = FB[3 * NFC + sf] - FB[3 * NFC + nf_];  // S.ft - N.ft
     double d = R[F_D * RREG + s];
     bool wet = d > P.eps;
     double cx = 0.0, cy = 0.0;
@@ -609,12 +923,11 @@ __global__ void __launch_bounds__(NTHR, 2) k_step(Geo G, StepArgs A) {
     double Fh = px_m[m] + py_m;
     double Fvx = (px_a[m] + py_c) + cx;
     double Fvy = (py_a + px_c[m]) + cy;
-    double sgn_ = 0.0;
-    if (nsrc > 0) sgn_ = cell_sigma_only(A.src, sig_n, nsrc, i, jg);
-    bool act = Hn > P.eps || sgn_ != 0.0;
+    bool act = (actbits >> m) & 1u;
+    double Hn = act ? 0.0 : A.H[k];
     double H1, qx, qy, dfc;
-    final_cell(act ? Ht[m] : Hn, act ? Qx[m] : qxn, act ? Qy[m] : qyn, Fh, Fvx, Fvy, dt_h, P.eps,
-               H1, qx, qy, dfc);
+    final_cell(act ? Ht[m] : Hn, act ? Qx[m] : A.HUx[k], act ? Qy[m] : A.HUy[k], Fh, Fvx, Fvy,
+               dt_h, P.eps, H1, qx, qy, dfc);
     deficit += dfc;
     A.Ho[k] = H1;
     A.HUxo[k] = qx;
@@ -623,7 +936,6 @@ __global__ void __launch_bounds__(NTHR, 2) k_step(Geo G, StepArgs A) {
   if (tid == 0) A.tile_same[tile] = 0;
 
   // ---- per-tile diagnostic partials (deterministic) ------------------------
-  __shared__ double s_red[3][NTHR / 32];
   double v3[3] = {deficit, srcvol, outflow};
 #pragma unroll
   for (int q = 0; q < 3; ++q) {
@@ -636,40 +948,53 @@ __global__ void __launch_bounds__(NTHR, 2) k_step(Geo G, StepArgs A) {
   if (tid < 3) {
     double v = 0.0;
     for (int w = 0; w < NTHR / 32; ++w) v += s_red[tid][w];
-    A.part[3 * tile + tid] = v;
+    A.part[5 * (size_t)tile + tid] = v;
   }
 }
 
-// k_finish: diagnostics over tiles in tile order (deterministic), commit t.
-__global__ void k_finish(Geo G, const double* part, int ntiles, StepScalars* sc, double area,
-                         double h) {
-  __shared__ double s[3][256];
-  bool stop = stopped(sc);
-  double v[3] = {0.0, 0.0, 0.0};
-  int per = (ntiles + blockDim.x - 1) / blockDim.x;
-  int a = threadIdx.x * per, e = min(a + per, ntiles);
-  if (!stop)
-    for (int t = a; t < e; ++t) {
-      v[0] += part[3 * t + 0];
-      v[1] += part[3 * t + 1];
-      v[2] += part[3 * t + 2];
-    }
-  for (int q = 0; q < 3; ++q) s[q][threadIdx.x] = v[q];
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    if (stop) {
-      if (sc->fail_step < 0) sc->fail_step = sc->steps_done;
-      return;
-    }
-    double w[3] = {0.0, 0.0, 0.0};
-    for (int t = 0; t < (int)blockDim.x; ++t)
-      for (int q = 0; q < 3; ++q) w[q] += s[q][t];
-    sc->deficit = w[0] * area;
-    sc->srcvol = w[1] * area;
-    sc->outflow = (w[2] * sc->tau) * h;
-    sc->t += sc->tau;  // stepper.cpp:703
-    sc->steps_done += 1;
+// k_reduce: RED_CTAS fixed-order partial sums of the per-tile partials
+// (deficit, source volume, outflow, Lagrangian blocks, flux blocks; coalesced,
+// deterministic); k_finish adds them in CTA order and commits t.
+constexpr int NPART = 5;
+__global__ void k_reduce(const double* part, int ntiles, double* red, const StepScalars* sc) {
+  __shared__ double s[NPART][NTHR];
+  double v[NPART] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  if (!stopped(sc)) {
+    int chunk = (ntiles + gridDim.x - 1) / gridDim.x;
+    int a = blockIdx.x * chunk, e = min(a + chunk, ntiles);
+    for (int t = a + threadIdx.x; t < e; t += NTHR)
+#pragma unroll
+      for (int q = 0; q < NPART; ++q) v[q] += part[NPART * (size_t)t + q];
   }
+  for (int q = 0; q < NPART; ++q) s[q][threadIdx.x] = v[q];
+  __syncthreads();
+  for (int w = NTHR / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w)
+      for (int q = 0; q < NPART; ++q) s[q][threadIdx.x] += s[q][threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x < NPART) red[NPART * blockIdx.x + threadIdx.x] = s[threadIdx.x][0];
+}
+
+__global__ void k_finish(const double* red, int nred, StepScalars* sc, double area, double h,
+                         int counts_from_tiles) {
+  if (stopped(sc)) {
+    if (sc->fail_step < 0) sc->fail_step = sc->steps_done;
+    return;
+  }
+  double w[NPART] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int t = 0; t < nred; ++t)
+    for (int q = 0; q < NPART; ++q) w[q] += red[NPART * t + q];
+  sc->deficit = w[0] * area;
+  sc->srcvol = w[1] * area;
+  sc->outflow = (w[2] * sc->tau) * h;
+  if (counts_from_tiles) {
+    sc->lag_act = (int)w[3];
+    sc->flux_act = (int)w[4];
+  }
+  sc->t += sc->tau;  // stepper.cpp:703
+  sc->steps_done += 1;
+  sc->mask_valid = 1;
 }
 
 StepArgs step_args(swf_ctx* c) {
@@ -688,18 +1013,14 @@ StepArgs step_args(swf_ctx* c) {
   A.src = c->d_src;
   A.sig = c->d_sig;
   A.bflag = c->d_bflag;
-  A.tile_act = c->d_tile_act;
+  A.tile_act = tile_act_at(c, c->cur);
   A.tile_same = c->d_tile_same;
   A.part = c->d_part;
   A.sc = c->d_sc;
   return A;
 }
 
-constexpr size_t step_smem() {
-  return (size_t)(F_NUM * RREG + 4 * ((BX + 1) * BY > BX * (BY + 1) ? (BX + 1) * BY
-                                                                     : BX * (BY + 1))) *
-         sizeof(double);
-}
+constexpr size_t step_smem() { return (size_t)(F_NUM * RREG + 3 * NSL + 4 * NFC) * sizeof(double); }
 
 void ev(swf_ctx* c, int i) {
   if (!c->timing) return;
@@ -719,6 +1040,8 @@ void forces_rows(const swf_ctx* c, int& ra0, int& ra1) {
   if (ra1 > c->geo.r1 && ra1 == c->geo.rows) ra1 = c->geo.rows - 1;
 }
 
+bool mask_fused(const Geo& G) { return G.bs <= 16 && 16 % G.bs == 0; }
+
 }  // namespace
 
 int launch_begin(swf_ctx* c, double dt_cap) {
@@ -735,7 +1058,8 @@ int launch_mask(swf_ctx* c) {
                                                       c->d_interior, c->d_halo, c->d_bflag,
                                                       c->d_sc);
   int nt = G.tiles_x * G.tiles_y;
-  if (nt > 0) k_tiles<<<(nt + 127) / 128, 128, 0, c->stream>>>(G, c->d_bflag, c->d_tile_act);
+  if (nt > 0)
+    k_tiles<<<(nt + 127) / 128, 128, 0, c->stream>>>(G, c->d_bflag, tile_act_at(c, c->cur));
   return cuda_check(c, cudaGetLastError(), "k_mask");
 }
 
@@ -756,15 +1080,33 @@ int fused_enqueue_phase1(swf_ctx* c, double dt_cap) {
   int rc;
   ev(c, 0);
   if ((rc = launch_begin(c, dt_cap))) return rc;
-  if ((rc = launch_mask(c))) return rc;
+  bool fm = mask_fused(G);
+  if (!fm && (rc = launch_mask(c))) return rc;
   ev(c, 1);
-  int ra0, ra1;
-  forces_rows(c, ra0, ra1);
-  int txa = (G.nx + AX - 1) / AX, tya = (ra1 - ra0 + AY - 1) / AY;
-  if (txa * tya > 0)
-    k_forces<<<txa * tya, NTHR, 0, c->stream>>>(G, ra0, ra1, txa, c->H[c->cur], c->HUx[c->cur],
-                                                c->HUy[c->cur], c->b, c->nf, c->d_src, c->d_sig,
-                                                c->fpx, c->fpy, c->d_sc);
+  ForcesArgs A;
+  A.H = c->H[c->cur];
+  A.HUx = c->HUx[c->cur];
+  A.HUy = c->HUy[c->cur];
+  A.b = c->b;
+  A.nf = c->nf;
+  A.src = c->d_src;
+  A.sig = c->d_sig;
+  A.fpx = c->fpx;
+  A.fpy = c->fpy;
+  A.interior = c->d_interior;
+  A.halo = c->d_halo;
+  A.bflag = c->d_bflag;
+  A.tile_act = tile_act_at(c, c->cur);
+  A.tile_prev = tile_act_at(c, 1 - c->cur);
+  A.sc = c->d_sc;
+  A.cnt_part = c->d_part;
+  forces_rows(c, A.ra0, A.ra1);
+  A.tr_lo = -((G.r0 - A.ra0 + BY - 1) / BY);
+  int tr_hi = (A.ra1 - G.r0 + BY - 1) / BY;
+  if (tr_hi < G.tiles_y) tr_hi = G.tiles_y;
+  A.do_mask = fm ? 1 : 0;
+  int ntile = G.tiles_x * (tr_hi - A.tr_lo);
+  if (ntile > 0) k_forces<<<ntile, NTHR, 0, c->stream>>>(G, A);
   ev(c, 2);
   return cuda_check(c, cudaGetLastError(), "k_forces");
 }
@@ -777,7 +1119,10 @@ int fused_enqueue_phase2(swf_ctx* c, double dt_cap, double global_speed) {
   int nt = G.tiles_x * G.tiles_y;
   if (nt > 0) k_step<<<nt, NTHR, step_smem(), c->stream>>>(G, step_args(c));
   ev(c, 4);
-  k_finish<<<1, 256, 0, c->stream>>>(G, c->d_part, nt, c->d_sc, c->h * c->h, c->h);
+  double* red = c->d_part + NPART * (size_t)(nt > 0 ? nt : 1);
+  k_reduce<<<RED_CTAS, NTHR, 0, c->stream>>>(c->d_part, nt, red, c->d_sc);
+  k_finish<<<1, 1, 0, c->stream>>>(red, RED_CTAS, c->d_sc, c->h * c->h, c->h,
+                                   mask_fused(G) ? 1 : 0);
   ev(c, 5);
   if (c->timing && c->tslots > 0) ++c->tstep;
   c->cur = 1 - c->cur;  // optimistic; rolled back by the caller on failure
@@ -793,13 +1138,18 @@ int fused_enqueue_step(swf_ctx* c, double dt_cap) {
 }
 
 size_t fused_tile_bytes() { return step_smem(); }
+int fused_reduce_ctas() { return RED_CTAS; }
 
 // Kernel attributes must be set outside stream capture (a CUDA graph does not
 // record cudaFuncSetAttribute), so contexts call this at creation.
 int fused_prepare(swf_ctx* c) {
   cudaError_t e = cudaFuncSetAttribute(k_step, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)step_smem());
-  return cuda_check(c, e, "k_step shared-memory attribute");
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_step, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_forces, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  return cuda_check(c, e, "kernel attributes");
 }
 
 }  // namespace swf

@@ -21,6 +21,8 @@ struct DevSrc {
   double count_area;  // (double)count * (h*h), sources.cpp:40
 };
 
+constexpr int SPEED_SLOTS = 64;
+
 // Device-resident per-step scalars.
 struct StepScalars {
   double t;      // FlowState::t on the device
@@ -28,6 +30,7 @@ struct StepScalars {
   double t_mid;  // t + 0.5*tau
   double dt_cap;
   unsigned long long speed_bits;  // max CFL speed (non-negative double bits)
+  unsigned long long speed_slots[SPEED_SLOTS];  // per-CTA maxima, spread
   double wind_n[2], wind_mid[2];
   unsigned long long err_key;  // (kind << 58) | detail; ~0ull = none
   double err_val[3];           // dt floor: cfl, dt_min, speed
@@ -37,6 +40,7 @@ struct StepScalars {
   int fail_step;    // step index of the first failure (-1 none)
   double deficit, srcvol, outflow;  // this step's diagnostics (volumes)
   double speed_local;               // strips: local max speed (phase 1 out)
+  int mask_valid;  // the tile flags of the previous step describe the current state
 };
 
 enum ErrKind : unsigned long long { ERR_DT = 1, ERR_CFL = 2, ERR_FLUX = 3 };
@@ -96,7 +100,7 @@ struct swf_ctx {
   int* d_interior = nullptr;
   int* d_halo = nullptr;
   unsigned char* d_bflag = nullptr;  // bit0 lagrangian-active, bit1 flux-active
-  unsigned char* d_tile_act = nullptr;
+  unsigned char* d_tile_act = nullptr;  // 2 x tiles: [cur] this step, [1-cur] previous
   unsigned char* d_tile_same = nullptr;  // tile identical in both state buffers
   double* d_part = nullptr;              // per-tile diagnostic partials (3 per tile)
   // scalars
@@ -134,6 +138,7 @@ void stage_free(swf_ctx* c);
 // fused path (swf_fused.cu)
 int fused_enqueue_step(swf_ctx* c, double dt_cap);
 int fused_prepare(swf_ctx* c);
+int fused_reduce_ctas();
 int fused_enqueue_phase1(swf_ctx* c, double dt_cap);
 int fused_enqueue_phase2(swf_ctx* c, double dt_cap);
 int fused_enqueue_phase2(swf_ctx* c, double dt_cap, double global_speed);
@@ -150,6 +155,10 @@ int set_err(swf_ctx* c, int code, const std::string& msg);
 int cuda_check(swf_ctx* c, cudaError_t e, const char* what);
 int check_device_error(swf_ctx* c);  // after a sync: maps err_key to status
 size_t local_cells(const swf_ctx* c);
+void invalidate_mask(swf_ctx* c);  // the state changed outside the fused path
+inline unsigned char* tile_act_at(swf_ctx* c, int parity) {
+  return c->d_tile_act + (size_t)parity * ((size_t)c->geo.tiles_x * c->geo.tiles_y);
+}
 
 // per-cell source evaluation (sources.cpp:45-64, 66-75) on the device
 __device__ __forceinline__ double cell_source(const DevSrc* src, const double* sig, int nsrc,

@@ -618,6 +618,7 @@ int stage_run(swf_ctx* c, int stage, double arg, double* tau_out) {
       // the state changed in place: both fused buffers are stale for tiles
       if (c->d_tile_same)
         cudaMemsetAsync(c->d_tile_same, 0, (size_t)G.tiles_x * G.tiles_y, c->stream);
+      invalidate_mask(c);
       break;
     }
     default:
