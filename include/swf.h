@@ -201,6 +201,9 @@ int swf_last_volumes(swf_ctx* ctx, double* clamp_deficit, double* source_volume,
 /* hll_face_flux, riemann.hpp:18-19: in = n x {hL,unL,utL,hR,unR,utR},
  * out = n x {fm,fn,ft}. */
 int swf_dev_hll_face_flux(int n, const double* in, double g, double* out);
+/* the shared-reciprocal division of the kernels against plain IEEE division:
+ * in = n x {a, b}, out = n x {rdiv(a, recip_of(b)), a/b} (must be equal). */
+int swf_dev_rdiv(int n, const double* ab, double* out);
 /* the libm-compatible cube root used by friction (forcing.hpp:81). */
 int swf_dev_cbrt(int n, const double* x, double* y);
 /* bottom_friction, forcing.cpp:26-28: in = n x {ux,uy,H}, out = n x {fx,fy}. */

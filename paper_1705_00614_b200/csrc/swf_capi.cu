@@ -236,6 +236,12 @@ int create_impl(const swf_terrain* T, const swf_params* P, const swf_control* K,
   G.P.h = T->h;
   G.P.inv_h2 = 1.0 / (T->h * T->h);
   G.P.two_h = 2.0 * T->h;
+  // divisors of eta_grad_comp; r = 0 makes rdiv use plain division until a
+  // kernel refines the reciprocal on the device (with_recips)
+  G.P.rh.b = T->h;
+  G.P.rh.r = 0.0;
+  G.P.r2h.b = G.P.two_h;
+  G.P.r2h.r = 0.0;
   G.tiles_x = (G.nx + 31) / 32;
   G.tiles_y = (G.r1 - G.r0 + 15) / 16;
   apply_control(c, K);
@@ -572,6 +578,25 @@ int swf_step_host(swf_ctx* c, double* H, double* HUx, double* HUy, double* t, do
   swf_step_info tmp;
   rc = swf_step(c, dt_cap, info ? info : &tmp);
   if (rc) return rc;  // state untouched on abort (stepper.cpp:391-399, 568-577)
+  // The caller's arrays hold the step-start state.  When they are pinned
+  // (device-mapped under UVA), write back only the tiles the fused step
+  // updated, straight from the kernel; otherwise copy everything.
+  auto pinned = [](const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return a.type == cudaMemoryTypeHost && a.devicePointer == p;
+  };
+  if (c->mode == 0 && c->geo.r0 == 0 && c->geo.r1 == c->geo.rows && pinned(H) && pinned(HUx) &&
+      pinned(HUy)) {
+    rc = fused_scatter_host(c, H, HUx, HUy);
+    if (rc) return rc;
+    cudaError_t e = cudaMemcpyAsync(t, &c->d_sc->t, sizeof(double), cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    return cuda_check(c, e, "step_host write-back");
+  }
   return swf_download_state(c, H, HUx, HUy, t);
 }
 
@@ -765,6 +790,15 @@ __global__ void k_hll(int n, const double* in, double g, double* out) {
   out[3 * (size_t)i + 2] = f.ft;
 }
 
+// out[2i] = rdiv(a, recip_of(b)) (shared-reciprocal division), out[2i+1] = a/b
+__global__ void k_rdiv(int n, const double* in, double* out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double a = in[2 * (size_t)i], b = in[2 * (size_t)i + 1];
+  out[2 * (size_t)i] = rdiv(a, recip_of(b));
+  out[2 * (size_t)i + 1] = a / b;
+}
+
 __global__ void k_cbrt(int n, const double* x, double* y) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) y[i] = glibc_cbrt(x[i]);
@@ -803,6 +837,12 @@ extern "C" {
 int swf_dev_hll_face_flux(int n, const double* in, double g, double* out) {
   return run_kat(6 * (size_t)n, in, 3 * (size_t)n, out, [&](double* di, double* dout) {
     k_hll<<<(n + 255) / 256, 256>>>(n, di, g, dout);
+  });
+}
+
+int swf_dev_rdiv(int n, const double* ab, double* out) {
+  return run_kat(2 * (size_t)n, ab, 2 * (size_t)n, out, [&](double* di, double* dout) {
+    k_rdiv<<<(n + 255) / 256, 256>>>(n, di, dout);
   });
 }
 

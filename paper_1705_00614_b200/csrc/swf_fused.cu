@@ -261,58 +261,59 @@ __global__ void __launch_bounds__(NTHR, SWF_FORCES_MINB) k_forces(Geo G, ForcesA
   __shared__ unsigned long long s_max[NTHR / 32];
   StepScalars* sc = A.sc;
   if (stopped(sc)) return;
-  const PhysConst& P = G.P;
+  const PhysConst P = with_recips(G.P);
   const int tid = threadIdx.x;
   const int tx = blockIdx.x % G.tiles_x, tr = (int)(blockIdx.x / G.tiles_x) + A.tr_lo;
   const int i0 = tx * BX, rr0 = G.r0 + tr * BY;
   const size_t nx = G.nx;
   // mask rows (owned rows only)
   const bool mask_tile = A.do_mask && tr >= 0 && tr < G.tiles_y;
-  if (tid == 0) {
-    unsigned m = src_mask_for(G, A.src, i0 - 1, i0 + BX, G.jg0 + rr0 - 1, G.jg0 + rr0 + BY);
-    s_srcm = m;
-    // Dry neighbourhood: if this tile and its 8 neighbours had no flux-active
-    // block in the previous step, k_step left all their cells untouched, so
-    // this tile's block counts, flags and (empty) forces are unchanged: skip.
-    // Not across a strip boundary (ghost rows change by exchange) and not
-    // near a source (sigma(t) can switch a marker on).
-    int skip = 0;
-    if (mask_tile && G.skip && !m && sc->mask_valid && (tr > 0 || G.r0 == 0) &&
-        (tr < G.tiles_y - 1 || G.r1 == G.rows)) {
-      skip = 1;
-      for (int dy = -1; dy <= 1 && skip; ++dy)
-        for (int dx = -1; dx <= 1; ++dx) {
-          int x2 = tx + dx, y2 = tr + dy;
-          if (x2 < 0 || x2 >= G.tiles_x || y2 < 0 || y2 >= G.tiles_y) continue;
-          if (A.tile_prev[x2 + y2 * G.tiles_x]) {
-            skip = 0;
-            break;
-          }
-        }
-      if (skip) A.tile_act[tx + tr * G.tiles_x] = 0;
-    }
-    s_cnt[2] = skip;
+  if (tid == 0)
+    s_srcm = src_mask_for(G, A.src, i0 - 1, i0 + BX, G.jg0 + rr0 - 1, G.jg0 + rr0 + BY);
+  // Dry neighbourhood: if this tile and its 8 neighbours had no flux-active
+  // block in the previous step, k_step left all their cells untouched, so
+  // this tile's block counts, flags and (empty) forces are unchanged: skip.
+  // Not across a strip boundary (ghost rows change by exchange) and not near
+  // a source (sigma(t) can switch a marker on).  Threads 0..8 read one
+  // neighbour flag each.
+  const bool may_skip = mask_tile && G.skip && sc->mask_valid && (tr > 0 || G.r0 == 0) &&
+                        (tr < G.tiles_y - 1 || G.r1 == G.rows);
+  bool busy = !may_skip;
+  if (may_skip && tid < 9) {
+    int x2 = tx + tid % 3 - 1, y2 = tr + tid / 3 - 1;
+    if (x2 >= 0 && x2 < G.tiles_x && y2 >= 0 && y2 < G.tiles_y)
+      busy = A.tile_prev[x2 + y2 * G.tiles_x] != 0;
   }
-  __syncthreads();
-  if (s_cnt[2]) return;
+  busy = __syncthreads_or(busy);
   const unsigned srcm = s_srcm;
+  if (!busy && !srcm) {
+    if (tid == 0) A.tile_act[tx + tr * G.tiles_x] = 0;
+    return;
+  }
   // forces rows of this tile
   const int fa = max(rr0, A.ra0), fb = min(rr0 + BY, A.ra1);
 
-  // ---- region H + wet flags (wet = H > eps or an active source, K1) ---------
+  // ---- region state (all loads issued together) + wet flags (K1) ------------
   bool anywet = false;
   for (int c = tid; c < AREG; c += NTHR) {
     int i = i0 - 1 + c % AREGX, r = rr0 - 1 + c / AREGX;
-    double d = 0.0;
+    double d = 0.0, mx = 0.0, my = 0.0, bb = 0.0;
     unsigned char w = 0;
     if (i >= 0 && i < G.nx && r >= 0 && r < G.rows) {
-      d = A.H[(size_t)i + (size_t)r * nx];
+      size_t k = (size_t)i + (size_t)r * nx;
+      d = A.H[k];
+      mx = A.HUx[k];
+      my = A.HUy[k];
+      bb = A.b[k];
       bool wet = d > P.eps;
       w = wet || (srcm && msig(G, A.src, A.sig, srcm, i, G.jg0 + r) != 0.0);
       int x = c % AREGX - 1, y = c / AREGX - 1;
       if (wet && x >= 0 && x < BX && y >= 0 && y < BY && r >= fa && r < fb) anywet = true;
     }
     s_d[c] = d;
+    s_u[c] = mx;
+    s_v[c] = my;
+    s_e[c] = bb;
     s_w[c] = w;
   }
   if (tid < 3) s_cnt[tid] = 0;
@@ -384,17 +385,13 @@ __global__ void __launch_bounds__(NTHR, SWF_FORCES_MINB) k_forces(Geo G, ForcesA
   if (!anywet) return;
 
   // ---- region momentum -> eta, velocity ---------------------------------------
-  for (int c = tid; c < AREG; c += NTHR) {
-    int i = i0 - 1 + c % AREGX, r = rr0 - 1 + c / AREGX;
-    double e = 0.0, u = 0.0, v = 0.0;
-    if (i >= 0 && i < G.nx && r >= 0 && r < G.rows) {
-      size_t k = (size_t)i + (size_t)r * nx;
-      double d = s_d[c];
-      e = d + A.b[k];
-      if (d > P.eps) {
-        u = A.HUx[k] / d;
-        v = A.HUy[k] / d;
-      }
+  for (int c = tid; c < AREG; c += NTHR) {  // pointwise, in place (same c)
+    double d = s_d[c];
+    double e = d + s_e[c], u = 0.0, v = 0.0;
+    if (d > P.eps) {
+      Recip Rd = recip_of(d);
+      u = rdiv(s_u[c], Rd);
+      v = rdiv(s_v[c], Rd);
     }
     s_e[c] = e;
     s_u[c] = u;
@@ -529,9 +526,10 @@ __device__ __forceinline__ Slopes cell_slopes(double em, double um, double tm, d
   double d_in = p_in - sc_;
   double d_out = sc_ - p_out;
   Slopes s;
-  s.eta = minmod((ep - ec) / d_in, (ec - em) / d_out);
-  s.un = minmod((up - uc) / d_in, (uc - um) / d_out);
-  s.ut = minmod((tp - tc) / d_in, (tc - tm) / d_out);
+  Recip Ri = recip_of(d_in), Ro = recip_of(d_out);
+  s.eta = minmod(rdiv(ep - ec, Ri), rdiv(ec - em, Ro));
+  s.un = minmod(rdiv(up - uc, Ri), rdiv(uc - um, Ro));
+  s.ut = minmod(rdiv(tp - tc, Ri), rdiv(tc - tm, Ro));
   return s;
 }
 
@@ -577,7 +575,7 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
   double* FB = SL + 3 * NSL;              // 4 x NFC faces (fm, fnl, fnr, ft)
   __shared__ unsigned s_srcm;
   __shared__ double s_red[3][NTHR / 32];
-  const PhysConst& P = G.P;
+  const PhysConst P = with_recips(G.P);
   StepScalars* sc = A.sc;
   if (stopped(sc)) return;
   const int tid = threadIdx.x;
@@ -615,28 +613,63 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
   const double* sig_n = A.sig;
   const double* sig_m = A.sig + nsrc;
 
-  // ---- phase 1: half-step view on the region (K4 predictor, HalfView) ------
+  // ---- phase 1a: stage the region's inputs in shared memory ----------------
+  // All loads of a thread are independent (memory-level parallelism); the
+  // slope/face buffers (SL, FB: 3904 doubles) are free until phase 3 and hold
+  // f', n and the owned cells' step-start state meanwhile.
+  double* SC = SL;                      // [0,RREG) fpx  [RREG,2RREG) fpy  [2RREG,3RREG) n
+  double* OWN = SL + 3 * RREG;          // 3 x (BX*BY): H, HUx, HUy at t_n of owned cells
+  static_assert(3 * RREG + 3 * BX * BY <= 3 * NSL + 4 * NFC, "phase-1 scratch overflow");
   for (int c = tid; c < RREG; c += NTHR) {
     int i = i0 - 2 + c % RX, r = r0 - 2 + c / RX;
-    double d = 0.0, e = 0.0, u = 0.0, v = 0.0, sx = 0.0, sy = 0.0, bb = 0.0;
+    double h = 0.0, mx = 0.0, my = 0.0, bb = 0.0, fx = 0.0, fy = 0.0, n = G.n_manning;
     if (i >= 0 && i < G.nx && r >= 0 && r < G.rows) {
       size_t k = (size_t)i + (size_t)r * nx;
-      double Hn = A.H[k];
-      double mx = A.HUx[k], my = A.HUy[k];
+      h = A.H[k];
+      mx = A.HUx[k];
+      my = A.HUy[k];
       bb = A.b[k];
+      fx = A.fpx[k];  // meaningful for wet cells only (k_forces writes those)
+      fy = A.fpy[k];
+      if (G.has_nfield) n = A.nf[k];
+    }
+    R[F_D * RREG + c] = h;
+    R[F_U * RREG + c] = mx;
+    R[F_V * RREG + c] = my;
+    R[F_B * RREG + c] = bb;
+    SC[c] = fx;
+    SC[RREG + c] = fy;
+    SC[2 * RREG + c] = n;
+  }
+  __syncthreads();
+
+  // ---- phase 1b: half-step view on the region (K4 predictor, HalfView) -----
+  for (int c = tid; c < RREG; c += NTHR) {
+    int xr = c % RX, yr = c / RX;
+    int i = i0 - 2 + xr, r = r0 - 2 + yr;
+    double d = 0.0, e = 0.0, u = 0.0, v = 0.0, sx = 0.0, sy = 0.0;
+    double Hn = R[F_D * RREG + c], mx = R[F_U * RREG + c], my = R[F_V * RREG + c];
+    double bb = R[F_B * RREG + c];
+    if (xr >= 2 && xr < BX + 2 && yr >= 2 && yr < BY + 2) {  // owned: keep t_n
+      int o = (xr - 2) + (yr - 2) * BX;
+      OWN[o] = Hn;
+      OWN[BX * BY + o] = mx;
+      OWN[2 * BX * BY + o] = my;
+    }
+    if (i >= 0 && i < G.nx && r >= 0 && r < G.rows) {
       double sg = srcm ? msig(G, A.src, sig_n, srcm, i, G.jg0 + r) : 0.0;
       bool act = Hn > P.eps || sg != 0.0;
       d = Hn;
       if (act) {
         bool wet = Hn > P.eps;
-        double fx = wet ? A.fpx[k] : 0.0, fy = wet ? A.fpy[k] : 0.0;
-        double n = G.has_nfield ? A.nf[k] : G.n_manning;
-        predict_cell(Hn, mx, my, sg, fx, fy, n, half_tau, P.eps, P.g, d, mx, my);
+        double fx = wet ? SC[c] : 0.0, fy = wet ? SC[RREG + c] : 0.0;
+        predict_cell(Hn, mx, my, sg, fx, fy, SC[2 * RREG + c], half_tau, P.eps, P.g, d, mx, my);
       }
       e = d + bb;
       if (d > P.eps) {
-        u = mx / d;
-        v = my / d;
+        Recip Rd = recip_of(d);
+        u = rdiv(mx, Rd);
+        v = rdiv(my, Rd);
       }
       if (act) {
         // shift = 0.5*dr with dr = tau * u12 (stepper.cpp:72-73, 373-379);
@@ -651,14 +684,14 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
     R[F_V * RREG + c] = v;
     R[F_SX * RREG + c] = sx;
     R[F_SY * RREG + c] = sy;
-    R[F_B * RREG + c] = bb;
   }
   __syncthreads();
 
   // ---- phase 2: K5 mid forces + K6 corrector on owned active cells ---------
   constexpr int PER = BX * BY / NTHR;  // owned cells per thread (2)
+  // (Ht, Qx, Qy) end up as the final update's base state: the Lagrangian
+  // state for active cells, the step-start state otherwise (stepper.cpp:641-651)
   double Ht[PER], Qx[PER], Qy[PER];
-  unsigned actbits = 0;
   double srcvol = 0.0;
   const double wmx = sc->wind_mid[0], wmy = sc->wind_mid[1];
 #pragma unroll
@@ -666,14 +699,13 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
     int c = tid + m * NTHR;
     int x = c % BX, y = c / BX;
     int i = i0 + x, r = r0 + y;
-    Ht[m] = 0.0;
-    Qx[m] = 0.0;
-    Qy[m] = 0.0;
+    double Hn = OWN[c], qxn = OWN[BX * BY + c], qyn = OWN[2 * BX * BY + c];
+    Ht[m] = Hn;
+    Qx[m] = qxn;
+    Qy[m] = qyn;
     if (i >= G.nx || r >= G.r1) continue;
     int s = (x + 2) + (y + 2) * RX;
     int jg = G.jg0 + r;
-    size_t k = (size_t)i + (size_t)r * nx;
-    double Hn = A.H[k];
     double sgn_ = 0.0, svx = 0.0, svy = 0.0, sgm = 0.0;
     if (srcm) {
       sgn_ = msrc(G, A.src, sig_n, srcm, i, jg, svx, svy);
@@ -681,8 +713,7 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
     }
     bool act = Hn > P.eps || sgn_ != 0.0;
     if (!act) continue;
-    actbits |= 1u << m;
-    double n = G.has_nfield ? A.nf[k] : G.n_manning;
+    double n = SC[2 * RREG + s];
     double d = R[F_D * RREG + s];  // H12
     double fmx = 0.0, fmy = 0.0;
     if (d > P.eps) {
@@ -704,8 +735,7 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
       fmy = o.fy - o.fry;
     }
     double ht, qx, qy, sv;
-    correct_cell(Hn, A.HUx[k], A.HUy[k], nsrc > 0, sgm, d, fmx, fmy, n, tau, P.eps, P.g, ht, qx,
-                 qy, sv);
+    correct_cell(Hn, qxn, qyn, nsrc > 0, sgm, d, fmx, fmy, n, tau, P.eps, P.g, ht, qx, qy, sv);
     srcvol += sv;
     // CFL abort (stepper.cpp:378-380, 391-399): dr = tau * u12
     double dx = tau * R[F_U * RREG + s], dy = tau * R[F_V * RREG + s];
@@ -891,9 +921,9 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
     int lb = i / G.bs + (jg / G.bs - G.bj0) * G.nbx;
     bool flux_on = !G.skip || (A.bflag[lb] & 2);
     if (!flux_on) {  // block skipped by the reference: state unchanged
-      A.Ho[k] = A.H[k];
-      A.HUxo[k] = A.HUx[k];
-      A.HUyo[k] = A.HUy[k];
+      A.Ho[k] = Ht[m];  // no active cell in such a block: (Ht, Qx, Qy) = step-start state
+      A.HUxo[k] = Qx[m];
+      A.HUyo[k] = Qy[m];
       continue;
     }
     int sf = x + y * BX, nf_ = sf + BX;  // S and N face of the cell
@@ -923,11 +953,8 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
     double Fh = px_m[m] + py_m;
     double Fvx = (px_a[m] + py_c) + cx;
     double Fvy = (py_a + px_c[m]) + cy;
-    bool act = (actbits >> m) & 1u;
-    double Hn = act ? 0.0 : A.H[k];
     double H1, qx, qy, dfc;
-    final_cell(act ? Ht[m] : Hn, act ? Qx[m] : A.HUx[k], act ? Qy[m] : A.HUy[k], Fh, Fvx, Fvy,
-               dt_h, P.eps, H1, qx, qy, dfc);
+    final_cell(Ht[m], Qx[m], Qy[m], Fh, Fvx, Fvy, dt_h, P.eps, H1, qx, qy, dfc);
     deficit += dfc;
     A.Ho[k] = H1;
     A.HUxo[k] = qx;
@@ -1135,6 +1162,37 @@ int fused_enqueue_step(swf_ctx* c, double dt_cap) {
   int rc = fused_enqueue_phase1(c, dt_cap);
   if (rc) return rc;
   return fused_enqueue_phase2(c, dt_cap, -1.0);
+}
+
+// Zero-copy result write-back for the host-buffer step: the cells of the
+// tiles k_step updated are stored straight into pinned host memory over
+// PCIe; every other tile kept its step-start state, which the caller's
+// arrays already hold.  `flags` are the tile flags of the step just run.
+__global__ void k_scatter_host(Geo G, const unsigned char* __restrict__ flags,
+                               const double* __restrict__ H, const double* __restrict__ HUx,
+                               const double* __restrict__ HUy, double* hH, double* hHUx,
+                               double* hHUy) {
+  const int nt = G.tiles_x * G.tiles_y;
+  for (int t = blockIdx.x; t < nt; t += gridDim.x) {
+    if (!(flags[t] & 2)) continue;
+    int i0 = (t % G.tiles_x) * BX, r0 = G.r0 + (t / G.tiles_x) * BY;
+    for (int c = threadIdx.x; c < BX * BY; c += blockDim.x) {
+      int i = i0 + c % BX, r = r0 + c / BX;
+      if (i >= G.nx || r >= G.r1) continue;
+      size_t k = (size_t)i + (size_t)r * G.nx;
+      hH[k] = H[k];
+      hHUx[k] = HUx[k];
+      hHUy[k] = HUy[k];
+    }
+  }
+}
+
+int fused_scatter_host(swf_ctx* c, double* hH, double* hHUx, double* hHUy) {
+  const Geo& G = c->geo;
+  int cur = c->cur;  // the committed state; its step used the flags of parity 1 - cur
+  k_scatter_host<<<148 * 8, NTHR, 0, c->stream>>>(G, tile_act_at(c, 1 - cur), c->H[cur],
+                                                  c->HUx[cur], c->HUy[cur], hH, hHUx, hHUy);
+  return cuda_check(c, cudaGetLastError(), "k_scatter_host");
 }
 
 size_t fused_tile_bytes() { return step_smem(); }

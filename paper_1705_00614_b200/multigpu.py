@@ -217,40 +217,102 @@ def local_step(strips: Sequence[Strip], dt_cap: float = 0.0):
 # bench (torchrun, one rank per GPU)
 # ---------------------------------------------------------------------------
 
+class RankStrip:
+    """One rank's strip of a scenario plus its exchange/allreduce step, over
+    torch.distributed: NCCL on device buffers (production), or gloo with host
+    staging (SWF_DIST_BACKEND=gloo; lets 2+ ranks share one GPU in tests)."""
+
+    def __init__(self, config: str, n_full: int = 0, no_skip: bool = False):
+        import torch
+        import torch.distributed as dist
+        from . import scenarios as S
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        ndev = max(1, torch.cuda.device_count())
+        self.local = local % ndev
+        torch.cuda.set_device(self.local)
+        self.dev = torch.device("cuda", self.local)
+        self.backend = os.environ.get("SWF_DIST_BACKEND", "nccl")
+        if not dist.is_initialized():
+            if self.backend == "nccl":
+                dist.init_process_group("nccl", device_id=self.dev)
+            else:
+                dist.init_process_group(self.backend)
+        self.xdev = self.dev if self.backend == "nccl" else torch.device("cpu")
+        self.n = n_full or {"C3": 16384, "C5": 32768, "C2": 2048}[config]
+        self.bounds = strip_bounds(self.n, self.world, 16)
+        self.j0, self.j1 = self.bounds[self.rank]
+        self.w0, self.w1 = window_rows(self.j0, self.j1, self.n)
+        if config in ("C3", "C5") and n_full:
+            sc = S.floodplain(self.n, 50.0, window=(0, self.w0, self.n, self.w1 - self.w0),
+                              device=f"cuda:{self.local}")
+        else:
+            sc = S.build(config, device=f"cuda:{self.local}",
+                         window=(0, self.w0, self.n, self.w1 - self.w0))
+        if no_skip:
+            sc.options.skip_dry_blocks = False
+        self.sc = sc
+        self.strip = Strip(sc, self.n, self.j0, self.j1, sc.global_sources, sc.wind,
+                           device=self.local)
+        self.strip.upload(sc.state.H, sc.state.HUx, sc.state.HUy, 0.0)
+
+    def _pack(self, side, t):
+        import torch
+        if t.is_cuda:
+            self.strip.pack(side, t.data_ptr())
+        else:
+            tmp = torch.empty(t.numel(), dtype=torch.float64, device=self.dev)
+            self.strip.pack(side, tmp.data_ptr())
+            t.copy_(tmp.cpu())
+
+    def _unpack(self, side, t):
+        if t.is_cuda:
+            self.strip.unpack(side, t.data_ptr())
+        else:
+            tmp = t.to(self.dev)
+            self.strip.unpack(side, tmp.data_ptr())
+
+    def step(self, dt_cap: float = 0.0):
+        dist_exchange(self._pack, self._unpack, self.strip.count, self.rank, self.world, self.xdev)
+        sp = self.strip.phase1(dt_cap)
+        g = dist_allreduce_max(sp, self.xdev)
+        return self.strip.phase2(g, dt_cap)
+
+    def gather_state(self):
+        """Full-grid state on rank 0 (None elsewhere)."""
+        import torch
+        import torch.distributed as dist
+        win = self.sc.state
+        H, X, Y = np.empty_like(win.H), np.empty_like(win.H), np.empty_like(win.H)
+        t = self.strip.download(H, X, Y)
+        r0 = (self.j0 - self.w0) * self.n
+        own = np.concatenate([a[r0:r0 + (self.j1 - self.j0) * self.n] for a in (H, X, Y)])
+        objs = [None] * self.world
+        dist.all_gather_object(objs, (self.j0, self.j1, own, t))
+        if self.rank != 0:
+            return None
+        n = self.n
+        out = [np.empty(n * n) for _ in range(3)]
+        for j0, j1, o, _ in objs:
+            m = (j1 - j0) * n
+            for q in range(3):
+                out[q][j0 * n:j1 * n] = o[q * m:(q + 1) * m]
+        return out, t
+
+
 def bench_strips(args) -> Optional[dict]:
     import torch
     import torch.distributed as dist
-    from . import scenarios as S
 
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=dev)
-    full_n = {"C3": 16384, "C5": 32768, "C2": 2048}[args.config]
+    rs = RankStrip(args.config, no_skip=args.no_skip)
+    rank, world, dev, strip, sc = rs.rank, rs.world, rs.dev, rs.strip, rs.sc
+    local = rs.local
+    full_n, bounds, j0, j1 = rs.n, rs.bounds, rs.j0, rs.j1
     bs = 16
-    bounds = strip_bounds(full_n, world, bs)
-    j0, j1 = bounds[rank]
-    w0, w1 = window_rows(j0, j1, full_n)
-    sc = S.build(args.config, device=f"cuda:{local}", window=(0, w0, full_n, w1 - w0))
-    if args.no_skip:
-        sc.options.skip_dry_blocks = False
-    strip = Strip(sc, full_n, j0, j1, sc.global_sources, sc.wind, device=local)
-    strip.upload(sc.state.H, sc.state.HUx, sc.state.HUy, 0.0)
-
-    def pack(side, t):
-        strip.pack(side, t.data_ptr())
-
-    def unpack(side, t):
-        strip.unpack(side, t.data_ptr())
 
     def step():
-        dist_exchange(pack, unpack, strip.count, rank, world, dev)
-        sp = strip.phase1(0.0)
-        g = dist_allreduce_max(sp, dev)
-        return strip.phase2(g, 0.0)
+        return rs.step(0.0)
 
     for _ in range(args.warmup):
         step()
@@ -270,7 +332,7 @@ def bench_strips(args) -> Optional[dict]:
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=rs.xdev)
     dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max = float(ms_t.item())
     clk = clocks.stop() if clocks else None
@@ -283,7 +345,7 @@ def bench_strips(args) -> Optional[dict]:
     per_act = 56 + (8 if sc.params.n_field is not None else 0)
     alg = per_act * n_act + 8 * (n_own - n_act)
     # aggregate kernel-level bandwidth: sum of per-rank algorithmic bytes / max k_step time
-    agg = torch.tensor([alg, t_kstep], dtype=torch.float64, device=dev)
+    agg = torch.tensor([alg, t_kstep], dtype=torch.float64, device=rs.xdev)
     alg_all = agg[0:1].clone()
     dist.all_reduce(alg_all, op=dist.ReduceOp.SUM)
     tmax = agg[1:2].clone()

@@ -1,0 +1,44 @@
+"""Run under torchrun: N ranks each own a row strip of a floodplain, step it
+through the same RankStrip code the multi-GPU bench uses (exchange + exact
+allreduce-max), gather on rank 0 and compare bit for bit with a single
+context stepping the whole grid.  Exit code 0 = identical."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    import numpy as np
+    import torch.distributed as dist
+    from paper_1705_00614_b200 import CsphTvdStepper, multigpu as M, scenarios as S
+    n = int(os.environ.get("SWF_CHECK_N", "512"))
+    steps = int(os.environ.get("SWF_CHECK_STEPS", "20"))
+    rs = M.RankStrip("C3", n_full=n)
+    for _ in range(steps):
+        rs.step()
+    got = rs.gather_state()
+    ok = 1
+    if rs.rank == 0:
+        full = S.floodplain(n, 50.0, device="cuda")
+        one = CsphTvdStepper(full.terrain, full.params, full.control, full.options)
+        one.set_wind(full.wind)
+        one.set_sources(full.sources)
+        st = full.state.copy()
+        one.upload(st)
+        one.run(steps)
+        one.download(st)
+        (H, X, Y), t = got
+        same = all(np.array_equal(a.view(np.int64), b.view(np.int64))
+                   for a, b in ((H, st.H), (X, st.HUx), (Y, st.HUy))) and t == st.t
+        print(f"multirank world={rs.world} n={n} steps={steps} bitwise_equal={same} t={t}", flush=True)
+        ok = 1 if same else 0
+    flag = [ok]
+    dist.broadcast_object_list(flag, src=0)
+    dist.destroy_process_group()
+    sys.exit(0 if flag[0] else 1)
+
+
+if __name__ == "__main__":
+    main()

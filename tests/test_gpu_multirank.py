@@ -1,0 +1,32 @@
+"""The multi-rank strip path end to end on one GPU: torchrun with 2 and 3
+ranks (gloo with host-staged halos, so several ranks can share the single
+GPU of the test box), bit-identical to the single-context run."""
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_torchrun_strips_bitwise(world):
+    env = dict(os.environ, SWF_DIST_BACKEND="gloo", SWF_CHECK_N="512", SWF_CHECK_STEPS="15")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+           os.path.join(ROOT, "tests", "multirank_check.py")]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "bitwise_equal=True" in r.stdout

@@ -59,6 +59,32 @@ def test_device_hll_matches_oracle(oracle_built):
     assert list(hll_face_flux_device(np.array([[1.0, 0, 0, 0, 0, 0]]), 9.81)[0]) == G["kat"]["hll_dam_break"]
 
 
+def test_device_rdiv_matches_division():
+    """The shared-reciprocal division used by the kernels is bit-identical to
+    nvcc's IEEE division on random, extreme and special operands."""
+    from paper_1705_00614_b200._lib import lib
+    from paper_1705_00614_b200 import _abi as A
+    rng = np.random.default_rng(11)
+    n = 400000
+    a = np.concatenate([rng.normal(0, 1, n) * 10.0 ** rng.integers(-30, 30, n),
+                        2.0 ** rng.uniform(-1074, 1023, n) * rng.choice([-1, 1], n),
+                        rng.uniform(-5, 5, n)])
+    b = np.concatenate([rng.normal(0, 1, n) * 10.0 ** rng.integers(-30, 30, n),
+                        2.0 ** rng.uniform(-1074, 1023, n) * rng.choice([-1, 1], n),
+                        rng.uniform(0.4, 1.6, n) * 50.0])
+    special = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 5e-324, -5e-324, 2.2250738585072014e-308,
+                        1.7976931348623157e308, 1.0, -1.0, 3.0])
+    sa, sb = np.meshgrid(special, special)
+    a = np.concatenate([a, sa.ravel()])
+    b = np.concatenate([b, sb.ravel()])
+    ab = np.ascontiguousarray(np.column_stack([a, b]))
+    out = np.empty_like(ab)
+    assert lib().swf_dev_rdiv(ab.shape[0], A.dptr(ab), A.dptr(out)) == 0
+    assert_bitwise(out[:, 0], out[:, 1], "rdiv vs a/b")
+    with np.errstate(all="ignore"):
+        assert_bitwise(out[:, 1], a / b, "device a/b vs IEEE")
+
+
 def test_device_friction_known_answer():
     from paper_1705_00614_b200.stepper import bottom_friction_device
     f = bottom_friction_device(np.array([[1.0, 0.0]]), np.array([1.0]), 9.81, 0.02)
@@ -109,6 +135,23 @@ def test_flood64_arrays_and_host_step(gpu_cls):
     assert_bitwise(st.HUx, z["HUx"], "HUx")
     assert_bitwise(st.HUy, z["HUy"], "HUy")
     assert st.t == float(z["t"][0])
+
+
+def test_host_step_pinned_write_back(gpu_cls, oracle_built):
+    """step() on pinned host arrays writes back only the updated tiles from
+    the kernel; the result must still be the full new state."""
+    import torch
+    sc = S.floodplain(16384, 50.0, window=(7600, 7000, 333, 250))
+    pin = lambda a: torch.from_numpy(a.copy()).pin_memory().numpy()
+    st = sc.state.copy()
+    st.H, st.HUx, st.HUy = pin(st.H), pin(st.HUx), pin(st.HUy)
+    so = sc.state.copy()
+    g = make(gpu_cls, sc)
+    o = make(oracle_built.OracleStepper, sc, kind="orc")
+    for _ in range(12):
+        ig, io = g.step(st), o.step(so)
+        assert ig.tau == io.tau
+    assert_state_bitwise(st, so, "pinned host step")
 
 
 # ------------------------------------------------------------ stage API parity
