@@ -165,6 +165,11 @@ int swf_step(swf_ctx* ctx, double dt_cap, swf_step_info* info);
  * state as it was before that step; *done receives the steps completed. */
 int swf_run(swf_ctx* ctx, int n, double dt_cap, int* done,
             swf_step_info* last);
+/* Tiles (32 x 16 cells) the last fused step updated; swf_step_host writes
+ * back only these when the host arrays are pinned (the rest kept their
+ * step-start values, which the caller's arrays already hold). */
+int swf_active_tiles(swf_ctx* ctx, int* n_active, int* n_total,
+                     int* cells_per_tile);
 /* Synchronise the context's stream and report a pending device error. */
 int swf_sync(swf_ctx* ctx);
 /* Device timing with CUDA events on the context's stream.  slots == 0: off;

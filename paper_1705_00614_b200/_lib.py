@@ -47,6 +47,7 @@ def declare(lib):
     _sig(lib, "swf_step", I, P, D, PN)
     _sig(lib, "swf_run", I, P, I, D, PI, PN)
     _sig(lib, "swf_sync", I, P)
+    _sig(lib, "swf_active_tiles", I, P, PI, PI, PI)
     _sig(lib, "swf_set_timing", I, P, I)
     _sig(lib, "swf_timing_read", I, P, I, PD)
     _sig(lib, "swf_stream", P, P)

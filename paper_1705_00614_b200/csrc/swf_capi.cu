@@ -664,6 +664,22 @@ int swf_run(swf_ctx* c, int n, double dt_cap, int* done, swf_step_info* last) {
   return rc;
 }
 
+int swf_active_tiles(swf_ctx* c, int* n_active, int* n_total, int* cells_per_tile) {
+  cudaSetDevice(c->device);
+  size_t nt = (size_t)c->geo.tiles_x * c->geo.tiles_y;
+  std::vector<unsigned char> f(nt ? nt : 1);
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e == cudaSuccess && nt)
+    e = cudaMemcpy(f.data(), tile_act_at(c, 1 - c->cur), nt, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_check(c, e, "active tiles");
+  int n = 0;
+  for (size_t t = 0; t < nt; ++t) n += (f[t] & 2) ? 1 : 0;
+  if (n_active) *n_active = n;
+  if (n_total) *n_total = (int)nt;
+  if (cells_per_tile) *cells_per_tile = 32 * 16;
+  return SWF_OK;
+}
+
 int swf_sync(swf_ctx* c) {
   cudaSetDevice(c->device);
   cudaError_t e = cudaStreamSynchronize(c->stream);

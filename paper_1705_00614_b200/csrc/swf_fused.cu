@@ -47,6 +47,24 @@ constexpr int NPART_ALLOC = 5;  // doubles per tile in d_part (see k_reduce)
 
 __device__ __forceinline__ bool stopped(const StepScalars* sc) { return sc->err_key != ERR_NONE; }
 
+// Developer instrumentation (-DSWF_PHASE_TIMING): per-phase cycles of
+// k_step summed over CTAs (thread 0 of each CTA; phases end at barriers).
+#ifdef SWF_PHASE_TIMING
+__device__ unsigned long long g_phase_cycles[16];
+#define PHASE_MARK(i)                                                         \
+  do {                                                                        \
+    if (threadIdx.x == 0) {                                                   \
+      long long t2_ = clock64();                                              \
+      atomicAdd(&g_phase_cycles[i], (unsigned long long)(t2_ - t_ph));        \
+      t_ph = t2_;                                                             \
+    }                                                                         \
+  } while (0)
+#else
+#define PHASE_MARK(i) \
+  do {                \
+  } while (0)
+#endif
+
 // ---------------------------------------------------------------------------
 // k_begin: per-step scalars at t_n (begin_step stepper.cpp:176-183,
 // source_terms sources.cpp:45-64, WindForcing::at grid.cpp:64-75)
@@ -603,6 +621,9 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
     return;
   }
 
+#ifdef SWF_PHASE_TIMING
+  long long t_ph = clock64();
+#endif
   if (tid == 0)
     s_srcm = src_mask_for(G, A.src, i0 - 2, i0 + BX + 1, G.jg0 + r0 - 2, G.jg0 + r0 + BY + 1);
   __syncthreads();
@@ -643,6 +664,7 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
   }
   __syncthreads();
 
+  PHASE_MARK(0);
   // ---- phase 1b: half-step view on the region (K4 predictor, HalfView) -----
   for (int c = tid; c < RREG; c += NTHR) {
     int xr = c % RX, yr = c / RX;
@@ -687,6 +709,7 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
   }
   __syncthreads();
 
+  PHASE_MARK(1);
   // ---- phase 2: K5 mid forces + K6 corrector on owned active cells ---------
   constexpr int PER = BX * BY / NTHR;  // owned cells per thread (2)
   // (Ht, Qx, Qy) end up as the final update's base state: the Lagrangian
@@ -750,6 +773,7 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
     Qy[m] = qy;
   }
 
+  PHASE_MARK(2);
   // ---- phase 3x: x slopes of columns -1..BX (rows of the tile) -------------
   for (int c = tid; c < (BX + 2) * BY; c += NTHR) {
     int xx = c % (BX + 2), y = c / (BX + 2);
@@ -772,6 +796,7 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
   }
   __syncthreads();
 
+  PHASE_MARK(3);
   // ---- phase 4x: x faces (stepper.cpp:402-447, 496-516) ----------------------
   double outflow = 0.0;
   const double face_p = (1.0 * 0.5) * P.h, face_m = (-1.0 * 0.5) * P.h;
@@ -834,6 +859,7 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
     px_c[m] = FB[3 * NFC + w] - FB[3 * NFC + e];
   }
 
+  PHASE_MARK(4);
   // ---- phase 3y: y slopes of rows -1..BY (columns of the tile) -------------
   for (int c = tid; c < BX * (BY + 2); c += NTHR) {
     int x = c % BX, yy = c / BX;
@@ -856,6 +882,7 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
   }
   __syncthreads();
 
+  PHASE_MARK(5);
   // ---- phase 4y: y faces (stepper.cpp:449-494, 518-538) ----------------------
   for (int c = tid; c < BX * (BY + 1); c += NTHR) {
     int x = c % BX, fy = c / BX;
@@ -906,6 +933,7 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
   }
   __syncthreads();
 
+  PHASE_MARK(6);
   // ---- phase 5: accumulate (stepper.cpp:540-566) + final (628-659) ---------
   double deficit = 0.0;
   const double dt_h = tau / P.h;
@@ -962,6 +990,7 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
   }
   if (tid == 0) A.tile_same[tile] = 0;
 
+  PHASE_MARK(7);
   // ---- per-tile diagnostic partials (deterministic) ------------------------
   double v3[3] = {deficit, srcvol, outflow};
 #pragma unroll
@@ -1196,6 +1225,18 @@ int fused_scatter_host(swf_ctx* c, double* hH, double* hHUx, double* hHUy) {
 }
 
 size_t fused_tile_bytes() { return step_smem(); }
+
+#ifdef SWF_PHASE_TIMING
+extern "C" int swf_debug_phase_cycles(unsigned long long* out16, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out16, g_phase_cycles, 16 * sizeof(unsigned long long));
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(g_phase_cycles, z, sizeof z);
+  }
+  return (int)cudaGetLastError();
+}
+#endif
 int fused_reduce_ctas() { return RED_CTAS; }
 
 // Kernel attributes must be set outside stream capture (a CUDA graph does not

@@ -207,6 +207,12 @@ class CsphTvdStepper:
         self._rc(rc)
         return done.value, info_from_c(info)
 
+    def active_tiles(self):
+        """(updated tiles, all tiles, cells per tile) of the last fused step."""
+        a, b, c = C.c_int(), C.c_int(), C.c_int()
+        self._rc(self._lib.swf_active_tiles(self._ctx, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
     def sync(self) -> None:
         self._rc(self._lib.swf_sync(self._ctx))
 
