@@ -64,6 +64,21 @@ def build(force=False, verbose=False):
     return OUT
 
 
+def build_variant(name, defines):
+    """Developer A/B builds: paper_1705_00614_b200/variants/libswf_<name>.so with
+    extra -D flags (select one at run time with SWF_LIB=...)."""
+    vdir = os.path.join(HERE, "variants")
+    os.makedirs(vdir, exist_ok=True)
+    out = os.path.join(vdir, f"libswf_{name}.so")
+    cmd = [nvcc()] + NVCC_FLAGS + [f"-D{d}" for d in defines] + ["-shared", "-o", out] + \
+        [os.path.join(CSRC, s) for s in SOURCES]
+    subprocess.run(cmd, check=True, cwd=CSRC)
+    return out
+
+
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(OUT)
+    if len(sys.argv) > 2 and sys.argv[1] == "variant":  # build.py variant NAME [DEF=V ...]
+        print(build_variant(sys.argv[2], sys.argv[3:]))
+    else:
+        build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+        print(OUT)

@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(NTHR, SWF_FORCES_MINB) k_forces(Geo G, ForcesA
   __shared__ unsigned long long s_max[NTHR / 32];
   StepScalars* sc = A.sc;
   if (stopped(sc)) return;
-  const PhysConst P = with_recips(G.P);
+  const PhysConst& P = G.P;  // reciprocals refined at context creation (fused_prepare)
   const int tid = threadIdx.x;
   const int tx = blockIdx.x % G.tiles_x, tr = (int)(blockIdx.x / G.tiles_x) + A.tr_lo;
   const int i0 = tx * BX, rr0 = G.r0 + tr * BY;
@@ -474,6 +474,9 @@ __global__ void __launch_bounds__(NTHR, SWF_FORCES_MINB) k_forces(Geo G, ForcesA
 enum { F_D = 0, F_E, F_U, F_V, F_SX, F_SY, F_B, F_NUM };
 constexpr int NSL = (BX + 2) * BY > BX * (BY + 2) ? (BX + 2) * BY : BX * (BY + 2);  // slopes
 constexpr int NFC = (BX + 1) * BY > BX * (BY + 1) ? (BX + 1) * BY : BX * (BY + 1);  // faces
+constexpr int SCRATCH_A = 3 * NSL + 4 * NFC;               // slopes + faces (phases 3-5)
+constexpr int SCRATCH_B = 3 * NSL + 3 * BX * BY + RREG;    // phase 1-2 staging (see k_step)
+constexpr int SCRATCH = SCRATCH_A > SCRATCH_B ? SCRATCH_A : SCRATCH_B;
 
 struct StepArgs {
   const double* __restrict__ H;
@@ -593,7 +596,7 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
   double* FB = SL + 3 * NSL;              // 4 x NFC faces (fm, fnl, fnr, ft)
   __shared__ unsigned s_srcm;
   __shared__ double s_red[3][NTHR / 32];
-  const PhysConst P = with_recips(G.P);
+  const PhysConst& P = G.P;  // reciprocals refined at context creation (fused_prepare)
   StepScalars* sc = A.sc;
   if (stopped(sc)) return;
   const int tid = threadIdx.x;
@@ -638,9 +641,13 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
   // All loads of a thread are independent (memory-level parallelism); the
   // slope/face buffers (SL, FB: 3904 doubles) are free until phase 3 and hold
   // f', n and the owned cells' step-start state meanwhile.
-  double* SC = SL;                      // [0,RREG) fpx  [RREG,2RREG) fpy  [2RREG,3RREG) n
-  double* OWN = SL + 3 * RREG;          // 3 x (BX*BY): H, HUx, HUy at t_n of owned cells
-  static_assert(3 * RREG + 3 * BX * BY <= 3 * NSL + 4 * NFC, "phase-1 scratch overflow");
+  // Phase 2 reads OWN and NF after phase-2 threads may already be writing the
+  // x slopes (no barrier between them), so both live above the slope block.
+  double* SC = SL;                      // [0,RREG) fpx  [RREG,2RREG) fpy   (phase 1 only)
+  double* OWN = SL + 3 * NSL;           // 3 x (BX*BY): H, HUx, HUy at t_n of owned cells
+  double* NF = OWN + 3 * BX * BY;       // RREG: Manning n of the region
+  static_assert(2 * RREG <= 3 * NSL, "phase-1 scratch overlaps OWN");
+  static_assert(3 * NSL + 3 * BX * BY + RREG <= SCRATCH, "phase-1 scratch overflow");
   for (int c = tid; c < RREG; c += NTHR) {
     int i = i0 - 2 + c % RX, r = r0 - 2 + c / RX;
     double h = 0.0, mx = 0.0, my = 0.0, bb = 0.0, fx = 0.0, fy = 0.0, n = G.n_manning;
@@ -660,7 +667,7 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
     R[F_B * RREG + c] = bb;
     SC[c] = fx;
     SC[RREG + c] = fy;
-    SC[2 * RREG + c] = n;
+    NF[c] = n;
   }
   __syncthreads();
 
@@ -685,7 +692,7 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
       if (act) {
         bool wet = Hn > P.eps;
         double fx = wet ? SC[c] : 0.0, fy = wet ? SC[RREG + c] : 0.0;
-        predict_cell(Hn, mx, my, sg, fx, fy, SC[2 * RREG + c], half_tau, P.eps, P.g, d, mx, my);
+        predict_cell(Hn, mx, my, sg, fx, fy, NF[c], half_tau, P.eps, P.g, d, mx, my);
       }
       e = d + bb;
       if (d > P.eps) {
@@ -736,7 +743,7 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
     }
     bool act = Hn > P.eps || sgn_ != 0.0;
     if (!act) continue;
-    double n = SC[2 * RREG + s];
+    double n = NF[s];
     double d = R[F_D * RREG + s];  // H12
     double fmx = 0.0, fmy = 0.0;
     if (d > P.eps) {
@@ -1076,7 +1083,12 @@ StepArgs step_args(swf_ctx* c) {
   return A;
 }
 
-constexpr size_t step_smem() { return (size_t)(F_NUM * RREG + 3 * NSL + 4 * NFC) * sizeof(double); }
+#ifndef SWF_STEP_SMEM_PAD
+#define SWF_STEP_SMEM_PAD 0  // developer knob: extra bytes to force lower occupancy
+#endif
+constexpr size_t step_smem() {
+  return (size_t)(F_NUM * RREG + SCRATCH) * sizeof(double) + SWF_STEP_SMEM_PAD;
+}
 
 void ev(swf_ctx* c, int i) {
   if (!c->timing) return;
@@ -1241,9 +1253,31 @@ int fused_reduce_ctas() { return RED_CTAS; }
 
 // Kernel attributes must be set outside stream capture (a CUDA graph does not
 // record cudaFuncSetAttribute), so contexts call this at creation.
+// The reciprocal refinements of h and 2h (eta_grad_comp's divisors) depend
+// on the terrain only: refined once here on the device and carried in Geo,
+// instead of by every thread of every tile kernel.
+__global__ void k_recips(double h, double two_h, double* out) {
+  out[0] = recip_of(h).r;
+  out[1] = recip_of(two_h).r;
+}
+
 int fused_prepare(swf_ctx* c) {
-  cudaError_t e = cudaFuncSetAttribute(k_step, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)step_smem());
+  double* d = nullptr;
+  double r[2] = {0.0, 0.0};
+  cudaError_t e = cudaMalloc(&d, 2 * sizeof(double));
+  if (e == cudaSuccess) {
+    k_recips<<<1, 1, 0, c->stream>>>(c->geo.P.h, c->geo.P.two_h, d);
+    e = cudaMemcpyAsync(r, d, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    cudaFree(d);
+  }
+  if (e == cudaSuccess) {
+    c->geo.P.rh.r = r[0];
+    c->geo.P.r2h.r = r[1];
+  }
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_step, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)step_smem());
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_step, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e == cudaSuccess)

@@ -18,7 +18,7 @@ import sys
 import tempfile
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-LIB = os.path.join(ROOT, "paper_1705_00614_b200", "libswflood_cuda.so")
+LIB = os.environ.get("SWF_LIB") or os.path.join(ROOT, "paper_1705_00614_b200", "libswflood_cuda.so")
 
 
 def sass_lines(kernel, cubin_name="swf_fused.sm_100a.cubin", src="swf_fused.cu"):
