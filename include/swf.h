@@ -248,6 +248,48 @@ int swf_strip_unpack(swf_ctx* ctx, int side, const double* src);
 int swf_strip_rows(const swf_ctx* ctx, int* j0, int* j1, int* ghost_lo,
                    int* ghost_hi);
 
+/* ---- two-level nested grids (SPEC.md [MODULE] nesting) ----
+ * The reference ships no code for this module; these entry
+ * points implement its SPEC operations prolong_boundary,
+ * restrict_feedback (:379-385) and coupled_step (:386-392) on the device.
+ * The operator details are in paper_1705_00614_b200/csrc/swf_nest.cu.
+ * A nest couples a global (coarse) context with a fine context created for
+ * the window at h/r plus a ghost band: fine nx = r*ni + 2*ghost, ny likewise,
+ * fine h = coarse h / r, same device, not strip contexts. */
+typedef struct swf_nest swf_nest;
+typedef struct swf_nest_desc {
+  int i0, j0, ni, nj; /* window: coarse cells [i0, i0+ni) x [j0, j0+nj) */
+  int r;              /* refinement factor (>= 1) */
+  int ghost;          /* ghost band width in fine cells (SPEC default 2) */
+  int two_way;        /* 1: restrict_feedback after each coupled step */
+} swf_nest_desc;
+typedef struct swf_coupled_info {
+  double tau;           /* the global step's tau */
+  int substeps_total;   /* fine steps over all nests */
+  int substeps_max;     /* most fine steps of one nest */
+  double fine_tau_min;  /* smallest fine tau */
+  swf_step_info coarse; /* the global step */
+} swf_coupled_info;
+int swf_nest_create(swf_ctx* coarse, swf_ctx* fine, const swf_nest_desc* desc,
+                    swf_nest** out);
+void swf_nest_destroy(swf_nest* nest);
+const char* swf_nest_last_error(const swf_nest* nest);
+/* ghost cells of the fine grid: nxf*nyf - (r*ni)*(r*nj) */
+int swf_nest_ghost_count(const swf_nest* nest, size_t* count);
+/* prolong_boundary of the coarse CURRENT state into ghost slot 0 or 1 */
+int swf_nest_prolong(swf_nest* nest, int slot);
+/* the fine ghost band := lerp(slot 0, slot 1, alpha) */
+int swf_nest_apply_ghosts(swf_nest* nest, double alpha);
+/* restrict_feedback: window cells := means of their r x r fine cells */
+int swf_nest_restrict(swf_nest* nest);
+/* slot values [H | HUx | HUy], 3*count doubles, ghost-cell order */
+int swf_nest_download_ghosts(swf_nest* nest, int slot, double* out);
+/* coupled_step: one global step (dt_cap as in step()), then every nest
+ * subcycles to the new global time with time-interpolated ghosts and, when
+ * two_way, restricts.  The fine contexts must be at the global time. */
+int swf_coupled_step(swf_ctx* coarse, swf_nest** nests, int n_nests, double dt_cap,
+                     swf_coupled_info* info);
+
 #ifdef __cplusplus
 }
 #endif

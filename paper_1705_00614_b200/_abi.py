@@ -68,3 +68,13 @@ def dptr(a):
         return PD()
     assert a.dtype.name == "float64" and a.flags["C_CONTIGUOUS"], "need C-contiguous float64"
     return a.ctypes.data_as(PD)
+
+
+class swf_nest_desc(C.Structure):
+    _fields_ = [("i0", C.c_int), ("j0", C.c_int), ("ni", C.c_int), ("nj", C.c_int),
+                ("r", C.c_int), ("ghost", C.c_int), ("two_way", C.c_int)]
+
+
+class swf_coupled_info(C.Structure):
+    _fields_ = [("tau", C.c_double), ("substeps_total", C.c_int), ("substeps_max", C.c_int),
+                ("fine_tau_min", C.c_double), ("coarse", swf_step_info)]

@@ -66,6 +66,16 @@ def declare(lib):
     _sig(lib, "swf_strip_rows", I, P, PI, PI, PI, PI)
     _sig(lib, "swf_strip_pack", I, P, I, C.c_void_p)
     _sig(lib, "swf_strip_unpack", I, P, I, C.c_void_p)
+    PND = C.POINTER(A.swf_nest_desc)
+    _sig(lib, "swf_nest_create", I, P, P, PND, C.POINTER(P))
+    _sig(lib, "swf_nest_destroy", V, P)
+    _sig(lib, "swf_nest_last_error", C.c_char_p, P)
+    _sig(lib, "swf_nest_ghost_count", I, P, C.POINTER(C.c_size_t))
+    _sig(lib, "swf_nest_prolong", I, P, I)
+    _sig(lib, "swf_nest_apply_ghosts", I, P, D)
+    _sig(lib, "swf_nest_restrict", I, P)
+    _sig(lib, "swf_nest_download_ghosts", I, P, I, PD)
+    _sig(lib, "swf_coupled_step", I, P, C.POINTER(P), I, D, C.POINTER(A.swf_coupled_info))
     return lib
 
 

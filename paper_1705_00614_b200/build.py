@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libswflood_cuda.so")
-SOURCES = ["swf_capi.cu", "swf_stage.cu", "swf_fused.cu"]
+SOURCES = ["swf_capi.cu", "swf_stage.cu", "swf_fused.cu", "swf_nest.cu"]
 HEADERS = ["swf_math.cuh", "swf_internal.cuh"]
 
 # -fmad=false: no FMA contraction, so every + and * rounds exactly like the

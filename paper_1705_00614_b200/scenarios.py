@@ -181,6 +181,78 @@ def floodplain(n: int = 16384, h: float = 50.0, window=None, device: str = "cpu"
                     global_sources=full_specs)
 
 
+@dataclass
+class NestedScenario:
+    """C4: a global scenario plus one fine window."""
+    coarse: Scenario
+    fine: Scenario
+    window: Tuple[int, int, int, int]  # coarse cells i0, j0, ni, nj
+    r: int
+    ghost: int
+
+
+def nested_floodplain(n: int = 4096, h: float = 50.0, window=(1536, 1536, 1024, 1024),
+                      r: int = 4, ghost: int = 2, device: str = "cpu",
+                      seed: int = SEED) -> NestedScenario:
+    """C4 (BASELINE.json configs[3]): the floodplain
+    generator on a coarse n x n grid at h, and the SAME generator (same
+    physical features, feature scale h) sampled on the fine window at h/r plus
+    the ghost band.  Sources are clipped to the window and rescaled to fine
+    cells (sigma = q / (count h_f^2) is unchanged); wind, Coriolis, viscosity
+    and the Manning field are shared."""
+    torch = _torch()
+    coarse = floodplain(n, h, device=device, seed=seed)
+    coarse.name = f"C4-nested-coarse-{n}"
+    i0, j0, ni, nj = window
+    L = n * h
+    hf = h / r
+    nxf, nyf = r * ni + 2 * ghost, r * nj + 2 * ghost
+    x0f = i0 * h - ghost * hf
+    y0f = j0 * h - ghost * hf
+    x = x0f + (torch.arange(nxf, dtype=torch.float64, device=device) + 0.5) * hf
+    y = y0f + (torch.arange(nyf, dtype=torch.float64, device=device) + 0.5) * hf
+    X, Y = torch.meshgrid(x, y, indexing="xy")
+    b, noise, chan, nfield = _floodplain_fields(X, Y, L, h, seed)
+    off = _flood_offset(L, h, seed)
+    H = torch.clamp(5e-5 * (L - X) + off - b, min=0.0)
+    H = torch.where(H > 1e-6, H, torch.zeros_like(H))
+    to_np = lambda t: t.reshape(-1).cpu().numpy().copy()
+    cells = nxf * nyf
+    terrain = Terrain(nxf, nyf, hf, x0f, y0f, to_np(b))
+    params = PhysicalParams(n_manning=0.04, n_field=to_np(nfield), nu=coarse.params.nu,
+                            omega_z=coarse.params.omega_z)
+    opts = StepperOptions(boundaries=BoundaryConfig(EdgeKind.Open, EdgeKind.Open, EdgeKind.Open,
+                                                    EdgeKind.Open))
+    st = FlowState(nxf, nyf, 0.0, to_np(H), np.zeros(cells), np.zeros(cells))
+    # ingestion consistency (SPEC.md:368): the global bed over the window is
+    # the block mean of the fine bed (summed in restrict_feedback's order), so
+    # restricting a lake at rest gives the coarse lake at rest
+    bf = terrain.b.reshape(nyf, nxf)[ghost:ghost + r * nj, ghost:ghost + r * ni]
+    blk = bf.reshape(nj, r, ni, r)
+    acc = np.zeros((nj, ni))
+    for bb in range(r):
+        for aa in range(r):
+            acc = acc + blk[:, bb, :, aa]
+    Bc = coarse.terrain.b.reshape(n, n)
+    Bc[j0:j0 + nj, i0:i0 + ni] = acc / float(r * r)
+    xc = (np.arange(i0, i0 + ni) + 0.5) * h
+    eta_c = 5e-5 * (L - xc)[None, :] + off
+    Hc = np.maximum(eta_c - Bc[j0:j0 + nj, i0:i0 + ni], 0.0)
+    coarse.state.H.reshape(n, n)[j0:j0 + nj, i0:i0 + ni] = np.where(Hc > 1e-6, Hc, 0.0)
+    specs = []
+    for sp in coarse.global_sources:
+        a0, b0 = max(sp.cells.i0, i0), max(sp.cells.j0, j0)
+        a1, b1 = min(sp.cells.i1, i0 + ni - 1), min(sp.cells.j1, j0 + nj - 1)
+        if a0 <= a1 and b0 <= b1:
+            rect = CellRect(ghost + (a0 - i0) * r, ghost + (b0 - j0) * r,
+                            ghost + (a1 - i0 + 1) * r - 1, ghost + (b1 - j0 + 1) * r - 1)
+            specs.append(SourceSpec(sp.kind, sp.name, rect, list(sp.hydrograph), sp.rate,
+                                    sp.source_velocity))
+    fine = Scenario(f"C4-nested-fine-r{r}", terrain, params, TimestepControl(), opts, st, specs,
+                    coarse.wind, full_shape=(nxf, nyf), window=(0, 0, nxf, nyf))
+    return NestedScenario(coarse, fine, tuple(window), r, ghost)
+
+
 def lake_at_rest(n: int = 128, h: float = 10.0, level: float = 0.0, seed: int = SEED) -> Scenario:
     """SPEC.md:540 acceptance 1: still lake over a seeded bumpy bed."""
     torch = _torch()
@@ -208,6 +280,8 @@ def build(config: str, device: str = "cpu", window=None) -> Scenario:
         return circular_dam_break(window=window, device=device)
     if config == "C3":
         return floodplain(16384, 50.0, window=window, device=device)
+    if config == "C4":
+        return nested_floodplain(device=device)
     if config == "C5":
         return floodplain(32768, 25.0, window=window, device=device)
     raise ValueError(config)

@@ -1,0 +1,121 @@
+"""Nested grids on the GPU (csrc/swf_nest.cu through the C ABI) against the
+CPU nesting oracle (oracle/nest.py over the C oracle stepper): prolongation,
+subcycling and restriction must match bit for bit, and the SPEC.md examples
+ must hold on the device path."""
+import numpy as np
+import pytest
+
+from helpers import assert_bitwise, assert_state_bitwise, make
+from oracle import nest as N
+from paper_1705_00614_b200 import scenarios as S
+from paper_1705_00614_b200.types import ConfigError, FlowState
+
+pytestmark = pytest.mark.gpu
+EPS = 1e-6
+
+
+def _gpu(ns, two_way=True):
+    from paper_1705_00614_b200 import CsphTvdStepper
+    from paper_1705_00614_b200.nesting import NestedGrid
+    coarse = make(CsphTvdStepper, ns.coarse)
+    coarse.upload(ns.coarse.state)
+    nest = NestedGrid(coarse, ns.window, ns.r, ns.fine.terrain, ns.fine.params,
+                      ns.fine.control, ns.fine.options, ghost=ns.ghost, two_way=two_way)
+    if ns.fine.wind.any():
+        nest.fine.set_wind(ns.fine.wind)
+    if ns.fine.sources:
+        nest.fine.set_sources(ns.fine.sources)
+    nest.upload(ns.fine.state)
+    return coarse, nest
+
+
+def _oracle(oracle_built, ns, two_way=True):
+    cs = make(oracle_built.OracleStepper, ns.coarse)
+    fs = make(oracle_built.OracleStepper, ns.fine)
+    w = N.Window(*ns.window, r=ns.r, ghost=ns.ghost, two_way=two_way)
+    cstate, fstate = ns.coarse.state.copy(), ns.fine.state.copy()
+    return cs, cstate, N.OracleNest(w, fs, fstate, ns.fine.terrain.b, EPS)
+
+
+def _down(stepper, like):
+    st = FlowState(like.nx, like.ny, 0.0, np.empty_like(like.H), np.empty_like(like.H),
+                   np.empty_like(like.H))
+    stepper.download(st)
+    return st
+
+
+def test_prolong_matches_oracle(oracle_built):
+    ns = S.nested_floodplain(64, 50.0, (20, 22, 16, 12), 4, 2)
+    coarse, nest = _gpu(ns)
+    g = nest.prolong_boundary(0)
+    w = N.Window(*ns.window, r=ns.r, ghost=ns.ghost)
+    st = ns.coarse.state
+    exp = N.prolong(w, st.H, st.HUx, st.HUy, ns.coarse.terrain.b, 64, ns.fine.terrain.b, EPS)
+    assert_bitwise(g, exp, "prolong")
+    assert (g[0] > 0).any() and (g[0] == 0).any()  # a wet/dry front crosses the band
+
+
+@pytest.mark.parametrize("r,win", [(4, (20, 20, 16, 16)), (3, (18, 21, 15, 11)),
+                                   (2, (24, 8, 20, 24))])
+def test_coupled_steps_match_oracle(oracle_built, r, win):
+    ns = S.nested_floodplain(64, 50.0, win, r, 2)
+    coarse, nest = _gpu(ns)
+    from paper_1705_00614_b200.nesting import coupled_step
+    cs, cstate, onest = _oracle(oracle_built, ns)
+    for k in range(6):
+        gi = coupled_step(coarse, [nest])
+        oi, subs = N.coupled_step(cs, cstate, ns.coarse.terrain.b, [onest])
+        assert gi.tau == oi.tau
+        assert gi.substeps_total == subs[0], (k, gi.substeps_total, subs)
+    assert subs[0] >= 1
+    assert_state_bitwise(_down(coarse, cstate), cstate, f"coarse r={r}")
+    assert_state_bitwise(_down(nest.fine, onest.state), onest.state, f"fine r={r}")
+
+
+def test_one_way_bitwise_equals_unnested_gpu_run():
+    from paper_1705_00614_b200 import CsphTvdStepper
+    from paper_1705_00614_b200.nesting import coupled_step
+    ns = S.nested_floodplain(64, 50.0, (20, 20, 16, 16), 4, 2)
+    coarse, nest = _gpu(ns, two_way=False)
+    plain = make(CsphTvdStepper, ns.coarse)
+    plain.upload(ns.coarse.state)
+    for _ in range(6):
+        coupled_step(coarse, [nest])
+        plain.step_resident()
+    assert_state_bitwise(_down(coarse, ns.coarse.state), _down(plain, ns.coarse.state), "one-way")
+
+
+def test_two_windows_match_oracle(oracle_built):
+    from paper_1705_00614_b200.nesting import coupled_step
+    a = S.nested_floodplain(80, 50.0, (10, 30, 12, 12), 2, 2)
+    b = S.nested_floodplain(80, 50.0, (50, 34, 14, 10), 4, 2)
+    coarse, na = _gpu(a)
+    from paper_1705_00614_b200.nesting import NestedGrid
+    nb = NestedGrid(coarse, b.window, b.r, b.fine.terrain, b.fine.params, b.fine.control,
+                    b.fine.options, ghost=b.ghost)
+    nb.fine.set_wind(b.fine.wind)
+    nb.upload(b.fine.state)
+    cs, cstate, oa = _oracle(oracle_built, a)
+    fsb = make(oracle_built.OracleStepper, b.fine)
+    ob = N.OracleNest(N.Window(*b.window, r=b.r, ghost=b.ghost), fsb, b.fine.state.copy(),
+                      b.fine.terrain.b, EPS)
+    for _ in range(4):
+        coupled_step(coarse, [na, nb])
+        N.coupled_step(cs, cstate, a.coarse.terrain.b, [oa, ob])
+    assert_state_bitwise(_down(coarse, cstate), cstate, "coarse")
+    assert_state_bitwise(_down(na.fine, oa.state), oa.state, "window a")
+    assert_state_bitwise(_down(nb.fine, ob.state), ob.state, "window b")
+
+
+def test_unsynchronized_and_bad_windows_are_config_errors():
+    from paper_1705_00614_b200.nesting import NestedGrid, coupled_step
+    ns = S.nested_floodplain(64, 50.0, (20, 20, 16, 16), 4, 2)
+    coarse, nest = _gpu(ns)
+    st = ns.fine.state.copy()
+    st.t = 1.0
+    nest.upload(st)
+    with pytest.raises(ConfigError):
+        coupled_step(coarse, [nest])
+    with pytest.raises(ConfigError):  # touches the domain edge
+        bad = S.nested_floodplain(64, 50.0, (0, 20, 16, 16), 4, 2)
+        NestedGrid(coarse, bad.window, 4, bad.fine.terrain, bad.fine.params)
