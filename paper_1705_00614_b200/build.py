@@ -35,21 +35,34 @@ def stale():
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-HOST_SRC = os.path.join(HERE, "host", "swflood_b200.cpp")
+HOST_SRCS = [os.path.join(HERE, "host", f) for f in
+             ("swflood_b200.cpp", "swflood_nest.cpp", "swflood_io.cpp")]
 HOST_OUT = os.path.join(HERE, "libswflood_b200.so")
+CLI_SRC = os.path.join(HERE, "host", "swflood_cli.cpp")
+CLI_OUT = os.path.join(HERE, "swflood")
 INCLUDE = os.path.join(HERE, "..", "include")
 
 
+def _cxx():
+    return "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
+
+
 def build_host(force=False):
-    """The C++ drop-in API (include/swflood_b200.hpp) over the C ABI."""
-    deps = [HOST_SRC, os.path.join(INCLUDE, "swflood_b200.hpp"), os.path.join(INCLUDE, "swf.h"), OUT]
-    if not force and os.path.exists(HOST_OUT) and all(
-            os.path.getmtime(d) <= os.path.getmtime(HOST_OUT) for d in deps):
-        return HOST_OUT
-    cxx = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
-    cmd = [cxx, "-std=c++20", "-O2", "-fPIC", "-shared", "-I", INCLUDE, HOST_SRC, "-o", HOST_OUT,
-           "-L", HERE, "-lswflood_cuda", "-Wl,-rpath,$ORIGIN"]
-    subprocess.run(cmd, check=True)
+    """The C++ drop-in API (include/swflood_b200.hpp, include/swflood/*.hpp)
+    over the C ABI, and the `swflood` command-line driver."""
+    hdrs = [os.path.join(INCLUDE, "swflood_b200.hpp"), os.path.join(INCLUDE, "swf.h"),
+            os.path.join(INCLUDE, "swflood", "nesting.hpp"), os.path.join(INCLUDE, "swflood", "io.hpp")]
+    deps = HOST_SRCS + hdrs + [OUT]
+    if force or not os.path.exists(HOST_OUT) or any(
+            os.path.getmtime(d) > os.path.getmtime(HOST_OUT) for d in deps):
+        cmd = [_cxx(), "-std=c++20", "-O2", "-fPIC", "-shared", "-I", INCLUDE] + HOST_SRCS + \
+            ["-o", HOST_OUT, "-L", HERE, "-lswflood_cuda", "-Wl,-rpath,$ORIGIN"]
+        subprocess.run(cmd, check=True)
+    if force or not os.path.exists(CLI_OUT) or any(
+            os.path.getmtime(d) > os.path.getmtime(CLI_OUT) for d in [CLI_SRC, HOST_OUT] + hdrs):
+        cmd = [_cxx(), "-std=c++20", "-O2", "-I", INCLUDE, CLI_SRC, "-o", CLI_OUT, "-L", HERE,
+               "-lswflood_b200", "-lswflood_cuda", "-Wl,-rpath,$ORIGIN"]
+        subprocess.run(cmd, check=True)
     return HOST_OUT
 
 

@@ -1,0 +1,79 @@
+"""The `swflood` CLI on the GPU: validation cases (SPEC.md:513-521,
+ACCEPTANCE CRITERIA 1-5), run with snapshots and summary CSV
+(SPEC.md:452-466), bench (skip on/off speed-up and stage shares)."""
+import csv
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+CLI = os.path.join(ROOT, "paper_1705_00614_b200", "swflood")
+
+
+def run(*args, cwd=None):
+    p = subprocess.run([CLI, *args], capture_output=True, text=True, timeout=900, cwd=cwd)
+    return p.returncode, p.stdout, p.stderr
+
+
+def read_asc(path):
+    with open(path) as f:
+        hdr = {}
+        for _ in range(6):
+            k, v = f.readline().split()
+            hdr[k.lower()] = float(v)
+        data = np.loadtxt(f)
+    return hdr, data[::-1].reshape(-1)  # rows north->south -> j northward
+
+
+@pytest.mark.parametrize("case", ["lake-at-rest", "dam-break", "skip-equivalence", "mass-ledger",
+                                  "mirror-symmetry", "zoom-mass", "speedup", "stage-shares"])
+def test_validation_case_passes(case):
+    rc, out, err = run("validate", case)
+    assert rc == 0, out + err
+    assert "PASS" in out
+
+
+def test_run_writes_snapshots_and_summary(tmp_path):
+    cfg = tmp_path / "lake.cfg"
+    cfg.write_text("synthetic = lake 96 10\nduration = 30\ncadence = 10\n"
+                   "[initial]\nmode = level\nlevel = 0.5\n")
+    out = tmp_path / "out"
+    rc, so, se = run("run", str(cfg), "--out", str(out))
+    assert rc == 0, so + se
+    rows = list(csv.DictReader(open(out / "summary.csv")))
+    assert len(rows) == 4  # floor(duration / cadence) + 1
+    assert float(rows[-1]["t"]) == pytest.approx(30.0, abs=1e-9)
+    assert max(float(r["max_speed"]) for r in rows) <= 1e-10  # lake at rest
+    hdr, H = read_asc(out / "snap00003_H.asc")
+    assert hdr["ncols"] == 96 and hdr["cellsize"] == 10
+    vol = H.sum() * 100.0
+    assert vol == pytest.approx(float(rows[-1]["total_volume"]), rel=1e-6)  # %.6e round trip
+    _, eta = read_asc(out / "snap00003_eta.asc")
+    _, b = read_asc(out / "snap00000_eta.asc")
+    assert np.abs(eta - b).max() <= 1e-5
+
+
+def test_dry_run_eta_equals_bed(tmp_path):
+    cfg = tmp_path / "dry.cfg"
+    cfg.write_text("synthetic = floodplain 64 50\nduration = 5\n")
+    out = tmp_path / "o"
+    rc, so, se = run("run", str(cfg), "--out", str(out), "--no-skip")
+    assert rc == 0, so + se
+    _, eta = read_asc(out / "snap00001_eta.asc")
+    _, H = read_asc(out / "snap00001_H.asc")
+    assert not H.any()
+    # eta = H + b = b on a dry domain, compared at %.6e
+    _, eta0 = read_asc(out / "snap00000_eta.asc")
+    np.testing.assert_array_equal(eta, eta0)
+
+
+def test_bench_reports_speedup_and_shares(tmp_path):
+    cfg = tmp_path / "b.cfg"
+    cfg.write_text("synthetic = floodplain 512 50\nduration = 1\n[initial]\nmode = level\nlevel = -3\n")
+    rc, out, err = run("bench", str(cfg), "--steps", "20")
+    assert rc == 0, out + err
+    assert "speedup from dry-block skipping" in out and "lagrange+flux+final" in out
