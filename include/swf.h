@@ -244,6 +244,26 @@ int swf_strip_halo_ptrs(swf_ctx* ctx, int side, double** send3, double** recv3,
  * this strip's ghost rows on `side`.  Synchronous on the context stream. */
 int swf_strip_pack(swf_ctx* ctx, int side, double* dst);
 int swf_strip_unpack(swf_ctx* ctx, int side, const double* src);
+/* Asynchronous strip steps (no host synchronisation inside a batch, so the
+ * halo exchange and the dt allreduce can run as device-side collectives on
+ * the context stream, overlapped with interior compute):
+ *   swf_strip_begin_batch(ctx)
+ *   per step:  pack_async(side) -> exchange starts on the comm stream
+ *              swf_strip_forces(ctx, dt_cap, 0)   begin + interior tile rows
+ *              (exchange done) unpack_async(side)
+ *              swf_strip_forces(ctx, dt_cap, 1)   ghost-dependent tile rows
+ *              swf_strip_local_speed(ctx, dev)    strip CFL speed -> device
+ *              (allreduce-MAX of dev across strips, on the device)
+ *              swf_strip_finish(ctx, dev, dt_cap) tau from *dev, K4..K8
+ *   swf_strip_end_batch(ctx, &done, &last)        sync + commit (like swf_run)
+ * Every call is enqueued on the context stream (swf_stream). */
+int swf_strip_begin_batch(swf_ctx* ctx);
+int swf_strip_forces(swf_ctx* ctx, double dt_cap, int part);
+int swf_strip_local_speed(swf_ctx* ctx, double* dev_out);
+int swf_strip_finish(swf_ctx* ctx, const double* dev_global_speed, double dt_cap);
+int swf_strip_end_batch(swf_ctx* ctx, int* done, swf_step_info* last);
+int swf_strip_pack_async(swf_ctx* ctx, int side, double* dst);
+int swf_strip_unpack_async(swf_ctx* ctx, int side, const double* src);
 /* Owned global rows [j0, j1) and the ghost-row counts below/above. */
 int swf_strip_rows(const swf_ctx* ctx, int* j0, int* j1, int* ghost_lo,
                    int* ghost_hi);

@@ -66,6 +66,13 @@ def declare(lib):
     _sig(lib, "swf_strip_rows", I, P, PI, PI, PI, PI)
     _sig(lib, "swf_strip_pack", I, P, I, C.c_void_p)
     _sig(lib, "swf_strip_unpack", I, P, I, C.c_void_p)
+    _sig(lib, "swf_strip_begin_batch", I, P)
+    _sig(lib, "swf_strip_forces", I, P, D, I)
+    _sig(lib, "swf_strip_local_speed", I, P, C.c_void_p)
+    _sig(lib, "swf_strip_finish", I, P, C.c_void_p, D)
+    _sig(lib, "swf_strip_end_batch", I, P, PI, PN)
+    _sig(lib, "swf_strip_pack_async", I, P, I, C.c_void_p)
+    _sig(lib, "swf_strip_unpack_async", I, P, I, C.c_void_p)
     PND = C.POINTER(A.swf_nest_desc)
     _sig(lib, "swf_nest_create", I, P, P, PND, C.POINTER(P))
     _sig(lib, "swf_nest_destroy", V, P)

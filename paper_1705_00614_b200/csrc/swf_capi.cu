@@ -960,6 +960,79 @@ int swf_strip_unpack(swf_ctx* c, int side, const double* src) {
   return cuda_check(c, e, "strip unpack");
 }
 
+// ---- asynchronous strip steps: no host round trip inside a batch ----------
+int swf_strip_begin_batch(swf_ctx* c) {
+  cudaSetDevice(c->device);
+  if (c->mode != 0) return set_err(c, SWF_ECONFIG, "asynchronous strip steps need the fused path");
+  int rc = reset_counters(c);
+  if (rc) return rc;
+  c->batch_cur0 = c->cur;
+  c->batch_steps = 0;
+  return SWF_OK;
+}
+
+int swf_strip_forces(swf_ctx* c, double dt_cap, int part) {
+  cudaSetDevice(c->device);
+  if (c->batch_cur0 < 0) return set_err(c, SWF_ECONFIG, "strip_forces outside a batch");
+  if (part != 0 && part != 1) return set_err(c, SWF_ECONFIG, "strip_forces: part must be 0 or 1");
+  return fused_enqueue_phase1(c, dt_cap, part);
+}
+
+int swf_strip_local_speed(swf_ctx* c, double* dev_out) {
+  cudaSetDevice(c->device);
+  return fused_local_speed(c, dev_out);
+}
+
+int swf_strip_finish(swf_ctx* c, const double* dev_global_speed, double dt_cap) {
+  cudaSetDevice(c->device);
+  if (c->batch_cur0 < 0) return set_err(c, SWF_ECONFIG, "strip_finish outside a batch");
+  int rc = fused_enqueue_phase2(c, dt_cap, -1.0, dev_global_speed);
+  if (rc) return rc;
+  ++c->batch_steps;
+  return SWF_OK;
+}
+
+int swf_strip_end_batch(swf_ctx* c, int* done, swf_step_info* last) {
+  cudaSetDevice(c->device);
+  if (c->batch_cur0 < 0) return set_err(c, SWF_ECONFIG, "strip_end_batch without a batch");
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  int cur0 = c->batch_cur0;
+  c->batch_cur0 = -1;
+  if (e != cudaSuccess) return cuda_check(c, e, "strip batch");
+  int rc = commit_batch(c, cur0, c->batch_steps, done);
+  if (last && c->h_sc->steps_done > 0) fill_fused_info(c, last);
+  return rc;
+}
+
+int swf_strip_pack_async(swf_ctx* c, int side, double* dst) {
+  cudaSetDevice(c->device);
+  double *s3[3], *r3[3];
+  size_t count = 0;
+  swf_strip_halo_ptrs(c, side, s3, r3, &count);
+  cudaError_t e = cudaSuccess;
+  for (int q = 0; q < 3 && e == cudaSuccess && count; ++q)
+    e = cudaMemcpyAsync(dst + q * count, s3[q], count * sizeof(double), cudaMemcpyDeviceToDevice,
+                        c->stream);
+  return cuda_check(c, e, "strip pack");
+}
+
+int swf_strip_unpack_async(swf_ctx* c, int side, const double* src) {
+  cudaSetDevice(c->device);
+  double *s3[3], *r3[3];
+  size_t count = 0;
+  swf_strip_halo_ptrs(c, side, s3, r3, &count);
+  cudaError_t e = cudaSuccess;
+  for (int q = 0; q < 3 && e == cudaSuccess && count; ++q)
+    e = cudaMemcpyAsync(r3[q], src + q * count, count * sizeof(double), cudaMemcpyDeviceToDevice,
+                        c->stream);
+  if (e == cudaSuccess) {
+    // the ghost rows changed outside the fused path: their tiles' dry-skip
+    // flags are no longer valid (k_forces never skips strip-boundary tiles,
+    // so nothing else to do)
+  }
+  return cuda_check(c, e, "strip unpack");
+}
+
 int swf_strip_rows(const swf_ctx* c, int* j0, int* j1, int* glo, int* ghi) {
   const Geo& G = c->geo;
   if (j0) *j0 = G.jg0 + G.r0;

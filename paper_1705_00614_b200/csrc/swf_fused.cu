@@ -109,14 +109,16 @@ __device__ void mid_scalars(const Geo& G, const DevSrc* src, const double* ht, c
 
 // k_tau: compute_dt's scalar tail (stepper.cpp:253-266) + mid scalars.
 // global_speed >= 0 overrides the device max (multi-strip allreduce result).
+// gspeed (device pointer, may be null) overrides both: the allreduced speed
+// of an asynchronous multi-strip step, read without a host round trip.
 __global__ void k_tau(Geo G, const DevSrc* src, const double* ht, const double* hq,
                       const double* wt, const double* wv, double* sig, StepScalars* sc,
-                      double dt_cap, double global_speed) {
+                      double dt_cap, double global_speed, const double* gspeed) {
   if (stopped(sc)) return;
   unsigned long long mb = sc->speed_bits;
   for (int q = 0; q < SPEED_SLOTS; ++q) mb = sc->speed_slots[q] > mb ? sc->speed_slots[q] : mb;
   sc->speed_bits = mb;
-  double speed = global_speed >= 0.0 ? global_speed : bitsd(mb);
+  double speed = gspeed ? *gspeed : (global_speed >= 0.0 ? global_speed : bitsd(mb));
   double tau = G.dt_max;
   if (speed > 0.0) {
     double cfl = (G.courant * G.P.h) / speed;
@@ -284,6 +286,9 @@ __global__ void __launch_bounds__(NTHR, SWF_FORCES_MINB) k_forces(Geo G, ForcesA
   const int tx = blockIdx.x % G.tiles_x, tr = (int)(blockIdx.x / G.tiles_x) + A.tr_lo;
   const int i0 = tx * BX, rr0 = G.r0 + tr * BY;
   const size_t nx = G.nx;
+#ifdef SWF_EXP_EXIT_ALL
+  if (true) return;
+#endif
   // mask rows (owned rows only)
   const bool mask_tile = A.do_mask && tr >= 0 && tr < G.tiles_y;
   if (tid == 0)
@@ -607,6 +612,9 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
   const size_t nx = G.nx;
 
   // ---- inactive tile: keep the step-start state (skip semantics) ----------
+#ifdef SWF_EXP_EXIT_ALL
+  if (true) return;  // developer experiment: pure launch cost of the tile grid
+#endif
   if (!(A.tile_act[tile] & 2)) {
     if (!A.tile_same[tile]) {
       for (int c = tid; c < BX * BY; c += NTHR) {
@@ -1133,7 +1141,7 @@ int launch_mask(swf_ctx* c) {
 
 int launch_tau(swf_ctx* c, double dt_cap) {
   k_tau<<<1, 1, 0, c->stream>>>(c->geo, c->d_src, c->d_ht, c->d_hq, c->d_wt, c->d_wv, c->d_sig,
-                                c->d_sc, dt_cap, -1.0);
+                                c->d_sc, dt_cap, -1.0, nullptr);
   return cuda_check(c, cudaGetLastError(), "k_tau");
 }
 
@@ -1143,14 +1151,20 @@ int launch_mid(swf_ctx* c, double tau) {
   return cuda_check(c, cudaGetLastError(), "k_mid");
 }
 
-int fused_enqueue_phase1(swf_ctx* c, double dt_cap) {
+// part: -1 = the whole phase (begin + every forces tile row); 0 = begin +
+// the tile rows that read no ghost row (a strip's interior, computable while
+// its halo exchange is in flight); 1 = the remaining (ghost-dependent) rows.
+int fused_enqueue_phase1(swf_ctx* c, double dt_cap, int part) {
   const Geo& G = c->geo;
   int rc;
-  ev(c, 0);
-  if ((rc = launch_begin(c, dt_cap))) return rc;
   bool fm = mask_fused(G);
-  if (!fm && (rc = launch_mask(c))) return rc;
-  ev(c, 1);
+  if (part == 0 && !fm) return set_err(c, SWF_ECONFIG, "split phase 1 needs a block size dividing 16");
+  if (part <= 0) {
+    ev(c, 0);
+    if ((rc = launch_begin(c, dt_cap))) return rc;
+    if (!fm && (rc = launch_mask(c))) return rc;
+    ev(c, 1);
+  }
   ForcesArgs A;
   A.H = c->H[c->cur];
   A.HUx = c->HUx[c->cur];
@@ -1173,16 +1187,50 @@ int fused_enqueue_phase1(swf_ctx* c, double dt_cap) {
   int tr_hi = (A.ra1 - G.r0 + BY - 1) / BY;
   if (tr_hi < G.tiles_y) tr_hi = G.tiles_y;
   A.do_mask = fm ? 1 : 0;
-  int ntile = G.tiles_x * (tr_hi - A.tr_lo);
-  if (ntile > 0) k_forces<<<ntile, NTHR, 0, c->stream>>>(G, A);
-  ev(c, 2);
+  if (part < 0) {
+    int ntile = G.tiles_x * (tr_hi - A.tr_lo);
+    if (ntile > 0) k_forces<<<ntile, NTHR, 0, c->stream>>>(G, A);
+  } else {
+    // interior tile rows [a, b): their 1-row halo stays inside the owned rows
+    int a = G.r0 > 0 ? 1 : 0;
+    int b = G.r1 < G.rows ? G.tiles_y - 1 : G.tiles_y;
+    if (b < a) b = a;
+    const int lo = A.tr_lo;
+    auto launch = [&](int r_first, int r_end) {
+      if (r_end <= r_first) return;
+      ForcesArgs B = A;
+      B.tr_lo = r_first;
+      k_forces<<<G.tiles_x * (r_end - r_first), NTHR, 0, c->stream>>>(G, B);
+    };
+    if (part == 0) {
+      launch(a, b);
+    } else {
+      launch(lo, a);
+      launch(b, tr_hi);
+    }
+  }
+  if (part != 0) ev(c, 2);
   return cuda_check(c, cudaGetLastError(), "k_forces");
 }
 
-int fused_enqueue_phase2(swf_ctx* c, double dt_cap, double global_speed) {
+int fused_enqueue_phase1(swf_ctx* c, double dt_cap) { return fused_enqueue_phase1(c, dt_cap, -1); }
+
+// this context's CFL speed (max over the per-CTA slots) into a device double
+__global__ void k_local_speed(const StepScalars* sc, double* out) {
+  unsigned long long mb = sc->speed_bits;
+  for (int q = 0; q < SPEED_SLOTS; ++q) mb = sc->speed_slots[q] > mb ? sc->speed_slots[q] : mb;
+  *out = bitsd(mb);
+}
+
+int fused_local_speed(swf_ctx* c, double* dev_out) {
+  k_local_speed<<<1, 1, 0, c->stream>>>(c->d_sc, dev_out);
+  return cuda_check(c, cudaGetLastError(), "k_local_speed");
+}
+
+int fused_enqueue_phase2(swf_ctx* c, double dt_cap, double global_speed, const double* gspeed) {
   const Geo& G = c->geo;
   k_tau<<<1, 1, 0, c->stream>>>(G, c->d_src, c->d_ht, c->d_hq, c->d_wt, c->d_wv, c->d_sig,
-                                c->d_sc, dt_cap, global_speed);
+                                c->d_sc, dt_cap, global_speed, gspeed);
   ev(c, 3);
   int nt = G.tiles_x * G.tiles_y;
   if (nt > 0) k_step<<<nt, NTHR, step_smem(), c->stream>>>(G, step_args(c));
@@ -1197,12 +1245,17 @@ int fused_enqueue_phase2(swf_ctx* c, double dt_cap, double global_speed) {
   return cuda_check(c, cudaGetLastError(), "k_step");
 }
 
-int fused_enqueue_phase2(swf_ctx* c, double dt_cap) { return fused_enqueue_phase2(c, dt_cap, -1.0); }
+int fused_enqueue_phase2(swf_ctx* c, double dt_cap) {
+  return fused_enqueue_phase2(c, dt_cap, -1.0, nullptr);
+}
+int fused_enqueue_phase2(swf_ctx* c, double dt_cap, double global_speed) {
+  return fused_enqueue_phase2(c, dt_cap, global_speed, nullptr);
+}
 
 int fused_enqueue_step(swf_ctx* c, double dt_cap) {
   int rc = fused_enqueue_phase1(c, dt_cap);
   if (rc) return rc;
-  return fused_enqueue_phase2(c, dt_cap, -1.0);
+  return fused_enqueue_phase2(c, dt_cap, -1.0, nullptr);
 }
 
 // Zero-copy result write-back for the host-buffer step: the cells of the

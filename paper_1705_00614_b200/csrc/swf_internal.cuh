@@ -110,6 +110,8 @@ struct swf_ctx {
   // stage path
   swf::Scratch* scr = nullptr;
   int mode = 0;  // 0 fused, 1 staged
+  int batch_cur0 = -1;  // asynchronous strip batch: ping-pong index at its start
+  int batch_steps = 0;
   int last_staged = 0;  // which path produced the last diagnostics
   // timing
   bool timing = false;
@@ -143,6 +145,10 @@ int fused_scatter_host(swf_ctx* c, double* hH, double* hHUx, double* hHUy);
 int fused_enqueue_phase1(swf_ctx* c, double dt_cap);
 int fused_enqueue_phase2(swf_ctx* c, double dt_cap);
 int fused_enqueue_phase2(swf_ctx* c, double dt_cap, double global_speed);
+int fused_enqueue_phase2(swf_ctx* c, double dt_cap, double global_speed, const double* gspeed);
+int fused_enqueue_phase1(swf_ctx* c, double dt_cap, int part);
+int fused_local_speed(swf_ctx* c, double* dev_out);
+
 int launch_begin(swf_ctx* c, double dt_cap);  // sources/wind at t_n, reset counters
 int launch_mask(swf_ctx* c);                   // K1 block mask + tile flags
 int launch_tau(swf_ctx* c, double dt_cap);     // tau from speed_bits, then mid scalars

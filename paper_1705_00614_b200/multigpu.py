@@ -136,6 +136,32 @@ class Strip:
     def stream_handle(self) -> int:
         return self._lib.swf_stream(self.ctx) or 0
 
+    # asynchronous steps (include/swf.h "Asynchronous strip steps")
+    def begin_batch(self):
+        self._rc(self._lib.swf_strip_begin_batch(self.ctx))
+
+    def forces(self, part: int, dt_cap: float = 0.0):
+        self._rc(self._lib.swf_strip_forces(self.ctx, float(dt_cap), int(part)))
+
+    def local_speed(self, dev_ptr: int):
+        self._rc(self._lib.swf_strip_local_speed(self.ctx, C.c_void_p(dev_ptr)))
+
+    def finish(self, dev_speed_ptr: int, dt_cap: float = 0.0):
+        self._rc(self._lib.swf_strip_finish(self.ctx, C.c_void_p(dev_speed_ptr), float(dt_cap)))
+
+    def end_batch(self):
+        from ._marshal import info_from_c
+        done = C.c_int()
+        info = A.swf_step_info()
+        self._rc(self._lib.swf_strip_end_batch(self.ctx, C.byref(done), C.byref(info)))
+        return done.value, info_from_c(info)
+
+    def pack_async(self, side: int, dev_ptr: int):
+        self._rc(self._lib.swf_strip_pack_async(self.ctx, side, C.c_void_p(dev_ptr)))
+
+    def unpack_async(self, side: int, dev_ptr: int):
+        self._rc(self._lib.swf_strip_unpack_async(self.ctx, side, C.c_void_p(dev_ptr)))
+
     def set_timing(self, slots: int):
         self._rc(self._lib.swf_set_timing(self.ctx, int(slots)))
 
@@ -213,6 +239,44 @@ def local_step(strips: Sequence[Strip], dt_cap: float = 0.0):
     return [s.phase2(speed, dt_cap) for s in strips]
 
 
+def local_steps_async(strips: Sequence[Strip], n: int, dt_cap: float = 0.0):
+    """n steps of virtual ranks on one device through the asynchronous strip
+    path (interior forces before the exchange, ghost-dependent rows after it,
+    the allreduce-max on the device).  The strips' streams are ordered with
+    device synchronisation here; the per-strip call sequence is exactly the
+    NCCL one (RankStrip.step_async)."""
+    import torch
+    speeds = torch.zeros(len(strips), dtype=torch.float64, device="cuda")
+    gmax = torch.zeros(1, dtype=torch.float64, device="cuda")
+    bufs = {}
+    for r, s in enumerate(strips):
+        for side in (0, 1):
+            if s.count[side]:
+                bufs[(r, side)] = torch.empty(3 * s.count[side], dtype=torch.float64, device="cuda")
+    for s in strips:
+        s.begin_batch()
+    for _ in range(n):
+        for r, s in enumerate(strips):
+            for side in (0, 1):
+                if (r, side) in bufs:
+                    s.pack_async(side, bufs[(r, side)].data_ptr())
+            s.forces(0, dt_cap)
+        torch.cuda.synchronize()
+        for r in range(len(strips) - 1):  # the exchange: neighbour packs -> ghost rows
+            strips[r + 1].unpack_async(0, bufs[(r, 1)].data_ptr())
+            strips[r].unpack_async(1, bufs[(r + 1, 0)].data_ptr())
+        for r, s in enumerate(strips):
+            s.forces(1, dt_cap)
+            s.local_speed(speeds[r:r + 1].data_ptr())
+        torch.cuda.synchronize()
+        torch.max(speeds, dim=0, keepdim=True, out=(gmax, torch.empty(1, dtype=torch.int64, device="cuda")))
+        torch.cuda.synchronize()
+        for s in strips:
+            s.finish(gmax.data_ptr(), dt_cap)
+        torch.cuda.synchronize()
+    return [s.end_batch() for s in strips]
+
+
 # ---------------------------------------------------------------------------
 # bench (torchrun, one rank per GPU)
 # ---------------------------------------------------------------------------
@@ -279,6 +343,51 @@ class RankStrip:
         g = dist_allreduce_max(sp, self.xdev)
         return self.strip.phase2(g, dt_cap)
 
+    # ---- NCCL, asynchronous: no host synchronisation inside a batch -------
+    def _async_setup(self):
+        import torch
+        if getattr(self, "_abufs", None) is not None:
+            return
+        self._stream = torch.cuda.ExternalStream(self.strip.stream_handle(), device=self.dev)
+        self._abufs = {}
+        for side, peer in exchange_plan(self.rank, self.world):
+            n = 3 * self.strip.count[side]
+            self._abufs[side] = (torch.empty(n, dtype=torch.float64, device=self.dev),
+                                 torch.empty(n, dtype=torch.float64, device=self.dev))
+        self._speed = torch.zeros(1, dtype=torch.float64, device=self.dev)
+
+    def begin_async(self):
+        self._async_setup()
+        self.strip.begin_batch()
+
+    def step_async(self, dt_cap: float = 0.0):
+        """One step enqueued on the strip's stream: pack, NCCL send/recv on
+        the comm stream while the interior tile rows' forces run, unpack and
+        the ghost-dependent rows, NCCL allreduce-MAX of the device speed,
+        tau and K4..K8 from the device value."""
+        import torch
+        import torch.distributed as dist
+        with torch.cuda.stream(self._stream):
+            ops = []
+            for side, peer in exchange_plan(self.rank, self.world):
+                sbuf, rbuf = self._abufs[side]
+                self.strip.pack_async(side, sbuf.data_ptr())
+                ops.append(dist.P2POp(dist.isend, sbuf, peer))
+                ops.append(dist.P2POp(dist.irecv, rbuf, peer))
+            works = dist.batch_isend_irecv(ops) if ops else []
+            self.strip.forces(0, dt_cap)  # overlaps the exchange
+            for w in works:
+                w.wait()  # the strip stream waits for the comm stream (device side)
+            for side, (sbuf, rbuf) in self._abufs.items():
+                self.strip.unpack_async(side, rbuf.data_ptr())
+            self.strip.forces(1, dt_cap)
+            self.strip.local_speed(self._speed.data_ptr())
+            dist.all_reduce(self._speed, op=dist.ReduceOp.MAX)
+            self.strip.finish(self._speed.data_ptr(), dt_cap)
+
+    def end_async(self):
+        return self.strip.end_batch()
+
     def gather_state(self):
         """Full-grid state on rank 0 (None elsewhere)."""
         import torch
@@ -311,11 +420,19 @@ def bench_strips(args) -> Optional[dict]:
     full_n, bounds, j0, j1 = rs.n, rs.bounds, rs.j0, rs.j1
     bs = 16
 
+    use_async = rs.backend == "nccl"
+
     def step():
         return rs.step(0.0)
 
-    for _ in range(args.warmup):
-        step()
+    if use_async:  # device-side exchange/allreduce, no host sync per step
+        rs.begin_async()
+        for _ in range(args.warmup):
+            rs.step_async(0.0)
+        rs.end_async()
+    else:
+        for _ in range(args.warmup):
+            step()
     K = args.steps
     strip.set_timing(K)
     stream = torch.cuda.ExternalStream(strip.stream_handle())
@@ -327,9 +444,18 @@ def bench_strips(args) -> Optional[dict]:
     dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    infos = [step() for _ in range(K)]
-    e1.record(stream)
+    if use_async:
+        rs.begin_async()
+        e0.record(stream)
+        for _ in range(K):
+            rs.step_async(0.0)
+        e1.record(stream)
+        done, last_info = rs.end_async()
+        infos = [last_info]
+    else:
+        e0.record(stream)
+        infos = [step() for _ in range(K)]
+        e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     ms_t = torch.tensor([ms], dtype=torch.float64, device=rs.xdev)
@@ -364,7 +490,10 @@ def bench_strips(args) -> Optional[dict]:
         "data": "synthetic (seeded generator, scenarios.py)",
         "config": {"workload": f"{sc.name.split('-')[0]} {full_n}x{full_n} row strips",
                    "cells": N_total, "strips": bounds, "halo_rows": HALO,
-                   "parallelism": f"row strips x{world}, NCCL halo send/recv + allreduce-max",
+                   "parallelism": f"row strips x{world}, " + ("NCCL halo send/recv overlapped with interior "
+                                                                 "forces + device allreduce-max, no host sync"
+                                                                 if use_async else
+                                                                 "halo send/recv + allreduce-max (host-synchronised)"),
                    "l2": "inputs larger than L2"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
                      "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),

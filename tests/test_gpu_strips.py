@@ -12,8 +12,9 @@ from paper_1705_00614_b200 import scenarios as S
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("parts", [2, 3, 4])
-def test_strips_bitwise_equal_single_grid(parts):
+@pytest.mark.parametrize("parts,mode", [(2, "sync"), (3, "sync"), (4, "sync"), (2, "async"),
+                                        (3, "async"), (5, "async")])
+def test_strips_bitwise_equal_single_grid(parts, mode):
     from paper_1705_00614_b200 import CsphTvdStepper
     n = 256
     full = S.floodplain(n, 50.0)
@@ -30,8 +31,12 @@ def test_strips_bitwise_equal_single_grid(parts):
         s = M.Strip(sc, n, j0, j1, sc.global_sources, sc.wind)
         s.upload(sc.state.H, sc.state.HUx, sc.state.HUy, 0.0)
         strips.append((s, sc, w0))
-    for _ in range(25):
-        M.local_step([s for s, _, _ in strips])
+    if mode == "sync":
+        for _ in range(25):
+            M.local_step([s for s, _, _ in strips])
+    else:  # interior forces / exchange / boundary forces / device allreduce
+        res = M.local_steps_async([s for s, _, _ in strips], 25)
+        assert all(done == 25 for done, _ in res)
     H = np.empty(n * n)
     X = np.empty(n * n)
     Y = np.empty(n * n)
