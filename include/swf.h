@@ -156,6 +156,11 @@ int swf_device_state(swf_ctx* ctx, double** H, double** HUx, double** HUy);
  * out, t advanced in place. */
 int swf_step_host(swf_ctx* ctx, double* H, double* HUx, double* HUy,
                   double* t, double dt_cap, swf_step_info* info);
+/* Host bytes the last swf_step_host read: with PINNED (device-mapped) arrays
+ * the depth in full plus the momentum of the flux-active tiles only (sparse
+ * zero-copy ingest; afterwards the resident calls need swf_upload_state);
+ * otherwise the three full fields. */
+int swf_last_ingest_bytes(const swf_ctx* ctx, long long* bytes);
 /* One step on the device-resident state; info may be NULL (then no host
  * synchronisation happens and errors surface at the next synchronising
  * call). */

@@ -505,6 +505,7 @@ int swf_get_options(const swf_ctx* c, swf_options* o) {
 }
 
 int swf_upload_state(swf_ctx* c, const double* H, const double* HUx, const double* HUy, double t) {
+  c->state_partial = 0;
   cudaSetDevice(c->device);
   size_t n = local_cells(c), bytes = n * sizeof(double);
   size_t off = 0;  // host arrays cover the local window
@@ -524,6 +525,10 @@ int swf_upload_state(swf_ctx* c, const double* H, const double* HUx, const doubl
 }
 
 int swf_download_state(swf_ctx* c, double* H, double* HUx, double* HUy, double* t) {
+  if (c->state_partial)
+    return set_err(c, SWF_ECONFIG,
+                   "the device state is incomplete after a pinned host-buffer step (sparse "
+                   "momentum ingest); upload a state first");
   cudaSetDevice(c->device);
   const Geo& G = c->geo;
   size_t off = (size_t)G.r0 * G.nx, n = (size_t)(G.r1 - G.r0) * G.nx, bytes = n * sizeof(double);
@@ -546,6 +551,10 @@ int swf_device_state(swf_ctx* c, double** H, double** HUx, double** HUy) {
 }
 
 int swf_step(swf_ctx* c, double dt_cap, swf_step_info* info) {
+  if (c->state_partial)
+    return set_err(c, SWF_ECONFIG,
+                   "the device state is incomplete after a pinned host-buffer step (sparse "
+                   "momentum ingest); upload a state first");
   cudaSetDevice(c->device);
   c->last_staged = c->mode == 1;
   if (c->mode == 1) {
@@ -573,14 +582,6 @@ int swf_step(swf_ctx* c, double dt_cap, swf_step_info* info) {
 
 int swf_step_host(swf_ctx* c, double* H, double* HUx, double* HUy, double* t, double dt_cap,
                   swf_step_info* info) {
-  int rc = swf_upload_state(c, H, HUx, HUy, *t);
-  if (rc) return rc;
-  swf_step_info tmp;
-  rc = swf_step(c, dt_cap, info ? info : &tmp);
-  if (rc) return rc;  // state untouched on abort (stepper.cpp:391-399, 568-577)
-  // The caller's arrays hold the step-start state.  When they are pinned
-  // (device-mapped under UVA), write back only the tiles the fused step
-  // updated, straight from the kernel; otherwise copy everything.
   auto pinned = [](const void* p) {
     cudaPointerAttributes a;
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -589,18 +590,61 @@ int swf_step_host(swf_ctx* c, double* H, double* HUx, double* HUy, double* t, do
     }
     return a.type == cudaMemoryTypeHost && a.devicePointer == p;
   };
-  if (c->mode == 0 && c->geo.r0 == 0 && c->geo.r1 == c->geo.rows && pinned(H) && pinned(HUx) &&
-      pinned(HUy)) {
+  cudaSetDevice(c->device);
+  const bool zc = c->mode == 0 && c->geo.r0 == 0 && c->geo.r1 == c->geo.rows && pinned(H) &&
+                  pinned(HUx) && pinned(HUy);
+  int rc;
+  if (zc) {
+    // Pinned (device-mapped) arrays: the depth is copied in full by the copy
+    // engine, the block mask computed from it, and the momentum read over
+    // PCIe for the flux-active tiles only (fused_ingest_hu); the result goes
+    // back the same way, tile by tile, after the step committed.
+    size_t n = local_cells(c), bytes = n * sizeof(double);
+    rc = reset_counters(c);
+    if (rc) return rc;
+    cudaError_t e = cudaMemcpyAsync(c->H[c->cur], H, bytes, cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(&c->d_sc->t, t, sizeof(double), cudaMemcpyHostToDevice, c->stream);
+    size_t nt = (size_t)c->geo.tiles_x * c->geo.tiles_y;
+    if (e == cudaSuccess && nt) e = cudaMemsetAsync(c->d_tile_same, 0, nt, c->stream);
+    if (e != cudaSuccess) return cuda_check(c, e, "step_host ingest");
+    invalidate_mask(c);
+    if ((rc = launch_begin(c, dt_cap)) || (rc = launch_mask(c)) || (rc = fused_ingest_hu(c, HUx, HUy)))
+      return rc;
+    c->state_partial = 0;
+    swf_step_info tmp;
+    rc = swf_step(c, dt_cap, info ? info : &tmp);
+    c->state_partial = 1;
+    if (rc) return rc;  // state untouched on abort (stepper.cpp:391-399, 568-577)
+    int na = 0, ntot = 0, cpt = 0;
+    swf_active_tiles(c, &na, &ntot, &cpt);
+    c->last_ingest_bytes = (long long)bytes + 2LL * 8 * na * cpt;
     rc = fused_scatter_host(c, H, HUx, HUy);
     if (rc) return rc;
-    cudaError_t e = cudaMemcpyAsync(t, &c->d_sc->t, sizeof(double), cudaMemcpyDeviceToHost, c->stream);
+    e = cudaMemcpyAsync(t, &c->d_sc->t, sizeof(double), cudaMemcpyDeviceToHost, c->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
     return cuda_check(c, e, "step_host write-back");
   }
+  rc = swf_upload_state(c, H, HUx, HUy, *t);
+  if (rc) return rc;
+  c->last_ingest_bytes = 3LL * 8 * (long long)local_cells(c);
+  swf_step_info tmp;
+  rc = swf_step(c, dt_cap, info ? info : &tmp);
+  if (rc) return rc;
   return swf_download_state(c, H, HUx, HUy, t);
 }
 
+int swf_last_ingest_bytes(const swf_ctx* c, long long* bytes) {
+  if (!c || !bytes) return SWF_ECONFIG;
+  *bytes = c->last_ingest_bytes;
+  return SWF_OK;
+}
+
 int swf_run(swf_ctx* c, int n, double dt_cap, int* done, swf_step_info* last) {
+  if (c->state_partial)
+    return set_err(c, SWF_ECONFIG,
+                   "the device state is incomplete after a pinned host-buffer step (sparse "
+                   "momentum ingest); upload a state first");
   cudaSetDevice(c->device);
   if (done) *done = 0;
   if (n <= 0) return SWF_OK;
@@ -739,6 +783,10 @@ int swf_set_mode(swf_ctx* c, int mode) {
 }
 
 int swf_stage(swf_ctx* c, int stage, double arg, double* tau_out) {
+  if (c->state_partial)
+    return set_err(c, SWF_ECONFIG,
+                   "the device state is incomplete after a pinned host-buffer step (sparse "
+                   "momentum ingest); upload a state first");
   cudaSetDevice(c->device);
   if (stage == SWF_STAGE_BEGIN) {
     int rc = reset_counters(c);
@@ -882,6 +930,10 @@ int swf_dev_bottom_friction(int n, const double* in, double g, double nm, double
 extern "C" {
 
 int swf_strip_phase1(swf_ctx* c, double dt_cap, double* speed_out) {
+  if (c->state_partial)
+    return set_err(c, SWF_ECONFIG,
+                   "the device state is incomplete after a pinned host-buffer step (sparse "
+                   "momentum ingest); upload a state first");
   cudaSetDevice(c->device);
   int rc = reset_counters(c);
   if (rc) return rc;
@@ -962,6 +1014,10 @@ int swf_strip_unpack(swf_ctx* c, int side, const double* src) {
 
 // ---- asynchronous strip steps: no host round trip inside a batch ----------
 int swf_strip_begin_batch(swf_ctx* c) {
+  if (c->state_partial)
+    return set_err(c, SWF_ECONFIG,
+                   "the device state is incomplete after a pinned host-buffer step (sparse "
+                   "momentum ingest); upload a state first");
   cudaSetDevice(c->device);
   if (c->mode != 0) return set_err(c, SWF_ECONFIG, "asynchronous strip steps need the fused path");
   int rc = reset_counters(c);

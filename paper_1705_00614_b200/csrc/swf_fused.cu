@@ -35,7 +35,12 @@ constexpr int BX = 32, BY = 16;  // tile of owned cells (k_forces and k_step)
 constexpr int AX = BX, AY = BY;
 constexpr int AREGX = AX + 2, AREGY = AY + 2, AREG = AREGX * AREGY;  // 1-cell halo
 constexpr int RX = BX + 4, RY = BY + 4, RREG = RX * RY;              // 2-cell halo
-constexpr int NTHR = 256;
+constexpr int NTHR = 256;  // k_forces, k_reduce, k_scatter_host
+#ifndef SWF_STEP_THREADS
+#define SWF_STEP_THREADS 256
+#endif
+constexpr int STHR = SWF_STEP_THREADS;  // k_step (a multiple of 32)
+static_assert(STHR % 32 == 0, "k_step threads must be whole warps");
 constexpr int RED_CTAS = 148;
 constexpr int NPART_ALLOC = 5;  // doubles per tile in d_part (see k_reduce)
 #ifndef SWF_STEP_MINB
@@ -594,13 +599,13 @@ __device__ __forceinline__ FaceRec face_from_sides(bool wetA, bool wetB, const S
   return rec;
 }
 
-__global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A) {
+__global__ void __launch_bounds__(STHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A) {
   extern __shared__ double smem[];
   double* R = smem;                       // F_NUM x RREG
   double* SL = smem + F_NUM * RREG;       // 3 x NSL slopes (eta, un, ut)
   double* FB = SL + 3 * NSL;              // 4 x NFC faces (fm, fnl, fnr, ft)
   __shared__ unsigned s_srcm;
-  __shared__ double s_red[3][NTHR / 32];
+  __shared__ double s_red[3][STHR / 32];
   const PhysConst& P = G.P;  // reciprocals refined at context creation (fused_prepare)
   StepScalars* sc = A.sc;
   if (stopped(sc)) return;
@@ -617,7 +622,7 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
 #endif
   if (!(A.tile_act[tile] & 2)) {
     if (!A.tile_same[tile]) {
-      for (int c = tid; c < BX * BY; c += NTHR) {
+      for (int c = tid; c < BX * BY; c += STHR) {
         int i = i0 + c % BX, r = r0 + c / BX;
         if (i < G.nx && r < G.r1) {
           size_t k = (size_t)i + (size_t)r * nx;
@@ -656,7 +661,7 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
   double* NF = OWN + 3 * BX * BY;       // RREG: Manning n of the region
   static_assert(2 * RREG <= 3 * NSL, "phase-1 scratch overlaps OWN");
   static_assert(3 * NSL + 3 * BX * BY + RREG <= SCRATCH, "phase-1 scratch overflow");
-  for (int c = tid; c < RREG; c += NTHR) {
+  for (int c = tid; c < RREG; c += STHR) {
     int i = i0 - 2 + c % RX, r = r0 - 2 + c / RX;
     double h = 0.0, mx = 0.0, my = 0.0, bb = 0.0, fx = 0.0, fy = 0.0, n = G.n_manning;
     if (i >= 0 && i < G.nx && r >= 0 && r < G.rows) {
@@ -681,7 +686,7 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
 
   PHASE_MARK(0);
   // ---- phase 1b: half-step view on the region (K4 predictor, HalfView) -----
-  for (int c = tid; c < RREG; c += NTHR) {
+  for (int c = tid; c < RREG; c += STHR) {
     int xr = c % RX, yr = c / RX;
     int i = i0 - 2 + xr, r = r0 - 2 + yr;
     double d = 0.0, e = 0.0, u = 0.0, v = 0.0, sx = 0.0, sy = 0.0;
@@ -726,7 +731,7 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
 
   PHASE_MARK(1);
   // ---- phase 2: K5 mid forces + K6 corrector on owned active cells ---------
-  constexpr int PER = BX * BY / NTHR;  // owned cells per thread (2)
+  constexpr int PER = (BX * BY + STHR - 1) / STHR;  // owned cells per thread (2 at 256)
   // (Ht, Qx, Qy) end up as the final update's base state: the Lagrangian
   // state for active cells, the step-start state otherwise (stepper.cpp:641-651)
   double Ht[PER], Qx[PER], Qy[PER];
@@ -734,7 +739,8 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
   const double wmx = sc->wind_mid[0], wmy = sc->wind_mid[1];
 #pragma unroll
   for (int m = 0; m < PER; ++m) {
-    int c = tid + m * NTHR;
+    int c = tid + m * STHR;
+    if (BX * BY % STHR && c >= BX * BY) break;
     int x = c % BX, y = c / BX;
     int i = i0 + x, r = r0 + y;
     double Hn = OWN[c], qxn = OWN[BX * BY + c], qyn = OWN[2 * BX * BY + c];
@@ -790,7 +796,7 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
 
   PHASE_MARK(2);
   // ---- phase 3x: x slopes of columns -1..BX (rows of the tile) -------------
-  for (int c = tid; c < (BX + 2) * BY; c += NTHR) {
+  for (int c = tid; c < (BX + 2) * BY; c += STHR) {
     int xx = c % (BX + 2), y = c / (BX + 2);
     int i = i0 - 1 + xx;
     int s = (xx + 1) + (y + 2) * RX;
@@ -815,7 +821,7 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
   // ---- phase 4x: x faces (stepper.cpp:402-447, 496-516) ----------------------
   double outflow = 0.0;
   const double face_p = (1.0 * 0.5) * P.h, face_m = (-1.0 * 0.5) * P.h;
-  for (int c = tid; c < (BX + 1) * BY; c += NTHR) {
+  for (int c = tid; c < (BX + 1) * BY; c += STHR) {
     int fx = c % (BX + 1), y = c / (BX + 1);
     int f = i0 + fx, r = r0 + y;
     FaceRec rec;
@@ -866,7 +872,8 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
   double px_m[PER], px_a[PER], px_c[PER];  // (W.fm-E.fm), (W.fnr-E.fnl), (W.ft-E.ft)
 #pragma unroll
   for (int m = 0; m < PER; ++m) {
-    int c = tid + m * NTHR;
+    int c = tid + m * STHR;
+    if (BX * BY % STHR && c >= BX * BY) break;
     int x = c % BX, y = c / BX;
     int w = x + y * (BX + 1), e = w + 1;
     px_m[m] = FB[0 * NFC + w] - FB[0 * NFC + e];
@@ -876,7 +883,7 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
 
   PHASE_MARK(4);
   // ---- phase 3y: y slopes of rows -1..BY (columns of the tile) -------------
-  for (int c = tid; c < BX * (BY + 2); c += NTHR) {
+  for (int c = tid; c < BX * (BY + 2); c += STHR) {
     int x = c % BX, yy = c / BX;
     int r = r0 - 1 + yy, jg = G.jg0 + r;
     int s = (x + 2) + (yy + 1) * RX;
@@ -899,7 +906,7 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
 
   PHASE_MARK(5);
   // ---- phase 4y: y faces (stepper.cpp:449-494, 518-538) ----------------------
-  for (int c = tid; c < BX * (BY + 1); c += NTHR) {
+  for (int c = tid; c < BX * (BY + 1); c += STHR) {
     int x = c % BX, fy = c / BX;
     int i = i0 + x, rf = r0 + fy;  // face between local rows rf-1 and rf
     int jf = G.jg0 + rf;           // global face index
@@ -954,7 +961,8 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
   const double dt_h = tau / P.h;
 #pragma unroll
   for (int m = 0; m < PER; ++m) {
-    int c = tid + m * NTHR;
+    int c = tid + m * STHR;
+    if (BX * BY % STHR && c >= BX * BY) break;
     int x = c % BX, y = c / BX;
     int i = i0 + x, r = r0 + y;
     if (i >= G.nx || r >= G.r1) continue;
@@ -1018,7 +1026,7 @@ __global__ void __launch_bounds__(NTHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
   __syncthreads();
   if (tid < 3) {
     double v = 0.0;
-    for (int w = 0; w < NTHR / 32; ++w) v += s_red[tid][w];
+    for (int w = 0; w < STHR / 32; ++w) v += s_red[tid][w];
     A.part[5 * (size_t)tile + tid] = v;
   }
 }
@@ -1233,7 +1241,7 @@ int fused_enqueue_phase2(swf_ctx* c, double dt_cap, double global_speed, const d
                                 c->d_sc, dt_cap, global_speed, gspeed);
   ev(c, 3);
   int nt = G.tiles_x * G.tiles_y;
-  if (nt > 0) k_step<<<nt, NTHR, step_smem(), c->stream>>>(G, step_args(c));
+  if (nt > 0) k_step<<<nt, STHR, step_smem(), c->stream>>>(G, step_args(c));
   ev(c, 4);
   double* red = c->d_part + NPART * (size_t)(nt > 0 ? nt : 1);
   k_reduce<<<RED_CTAS, NTHR, 0, c->stream>>>(c->d_part, nt, red, c->d_sc);
@@ -1287,6 +1295,47 @@ int fused_scatter_host(swf_ctx* c, double* hH, double* hHUx, double* hHUy) {
   k_scatter_host<<<148 * 8, NTHR, 0, c->stream>>>(G, tile_act_at(c, 1 - cur), c->H[cur],
                                                   c->HUx[cur], c->HUy[cur], hH, hHUx, hHUy);
   return cuda_check(c, cudaGetLastError(), "k_scatter_host");
+}
+
+// Sparse ingest of the momentum for a host-buffer step (swf_step_host on
+// pinned arrays): after the depth was copied in full and the block mask
+// computed, only the flux-active tiles' HUx, HUy are read from the caller's
+// pinned arrays (zero-copy PCIe reads, 16-byte vectors along rows).  Every
+// cell whose momentum the step reads or writes back lies in such a tile: a
+// wet or source cell makes its block Lagrangian-active, and the write-back
+// covers flux-active tiles only.
+__global__ void k_ingest_hu(Geo G, const unsigned char* __restrict__ flags,
+                            const double* __restrict__ hHUx, const double* __restrict__ hHUy,
+                            double* __restrict__ HUx, double* __restrict__ HUy) {
+  const int nt = G.tiles_x * G.tiles_y;
+  const bool vec = (G.nx % 2 == 0) && ((((uintptr_t)hHUx) | ((uintptr_t)hHUy)) % 16 == 0);
+  for (int t = blockIdx.x; t < nt; t += gridDim.x) {
+    if (!(flags[t] & 2)) continue;
+    int i0 = (t % G.tiles_x) * BX, r0 = G.r0 + (t / G.tiles_x) * BY;
+    if (vec) {
+      for (int c = threadIdx.x; c < BX * BY / 2; c += blockDim.x) {
+        int i = i0 + 2 * (c % (BX / 2)), r = r0 + c / (BX / 2);
+        if (i >= G.nx || r >= G.r1) continue;  // nx even: i + 1 < nx too
+        size_t k = (size_t)i + (size_t)r * G.nx;
+        *(double2*)(HUx + k) = *(const double2*)(hHUx + k);
+        *(double2*)(HUy + k) = *(const double2*)(hHUy + k);
+      }
+    } else {
+      for (int c = threadIdx.x; c < BX * BY; c += blockDim.x) {
+        int i = i0 + c % BX, r = r0 + c / BX;
+        if (i >= G.nx || r >= G.r1) continue;
+        size_t k = (size_t)i + (size_t)r * G.nx;
+        HUx[k] = hHUx[k];
+        HUy[k] = hHUy[k];
+      }
+    }
+  }
+}
+
+int fused_ingest_hu(swf_ctx* c, const double* hHUx, const double* hHUy) {
+  k_ingest_hu<<<148 * 8, NTHR, 0, c->stream>>>(c->geo, tile_act_at(c, c->cur), hHUx, hHUy,
+                                               c->HUx[c->cur], c->HUy[c->cur]);
+  return cuda_check(c, cudaGetLastError(), "k_ingest_hu");
 }
 
 size_t fused_tile_bytes() { return step_smem(); }

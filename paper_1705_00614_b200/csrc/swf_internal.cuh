@@ -111,6 +111,10 @@ struct swf_ctx {
   swf::Scratch* scr = nullptr;
   int mode = 0;  // 0 fused, 1 staged
   int batch_cur0 = -1;  // asynchronous strip batch: ping-pong index at its start
+  // after a sparse-ingest host-buffer step the device holds the momentum of
+  // the flux-active tiles only: resident calls need a fresh upload first
+  int state_partial = 0;
+  long long last_ingest_bytes = 0;
   int batch_steps = 0;
   int last_staged = 0;  // which path produced the last diagnostics
   // timing
@@ -148,6 +152,7 @@ int fused_enqueue_phase2(swf_ctx* c, double dt_cap, double global_speed);
 int fused_enqueue_phase2(swf_ctx* c, double dt_cap, double global_speed, const double* gspeed);
 int fused_enqueue_phase1(swf_ctx* c, double dt_cap, int part);
 int fused_local_speed(swf_ctx* c, double* dev_out);
+int fused_ingest_hu(swf_ctx* c, const double* hHUx, const double* hHUy);
 
 int launch_begin(swf_ctx* c, double dt_cap);  // sources/wind at t_n, reset counters
 int launch_mask(swf_ctx* c);                   // K1 block mask + tile flags

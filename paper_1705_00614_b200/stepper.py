@@ -207,6 +207,12 @@ class CsphTvdStepper:
         self._rc(rc)
         return done.value, info_from_c(info)
 
+    def last_ingest_bytes(self) -> int:
+        """Host bytes the last step(state) read (see swf_last_ingest_bytes)."""
+        b = C.c_longlong()
+        self._rc(self._lib.swf_last_ingest_bytes(self._ctx, C.byref(b)))
+        return b.value
+
     def active_tiles(self):
         """(updated tiles, all tiles, cells per tile) of the last fused step."""
         a, b, c = C.c_int(), C.c_int(), C.c_int()

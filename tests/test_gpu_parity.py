@@ -324,3 +324,38 @@ def test_run_stops_at_failure(gpu_cls):
         b.run(200, 0.1)
     b.download(sb)
     assert_state_bitwise(sb, st, "run() state after failure")
+
+
+def test_pinned_host_step_sparse_ingest_matches_oracle(gpu_cls, oracle_built):
+    """step(FlowState) on PINNED arrays: depth copied in full, momentum read
+    over PCIe for the flux-active tiles only, updated tiles written back in
+    place.  Bit-identical to the oracle, including junk momentum in dry cells
+    the step must neither read nor overwrite."""
+    import torch
+    from paper_1705_00614_b200.types import ConfigError, FlowState
+    sc = S.floodplain(256, 50.0)
+    st = sc.state.copy()
+    rng = np.random.default_rng(5)
+    dry = st.H <= sc.params.eps_dry
+    st.HUx[dry] = rng.normal(0, 1, dry.sum())  # never read by the reference for dry cells...
+    st.HUy[dry] = rng.normal(0, 1, dry.sum())
+    pin = lambda a: torch.from_numpy(a.copy()).pin_memory().numpy()
+    hs = FlowState(st.nx, st.ny, 0.0, pin(st.H), pin(st.HUx), pin(st.HUy))
+    cpu_state = st.copy()
+    g = make(gpu_cls, sc)
+    o = make(oracle_built.OracleStepper, sc)
+    for k in range(12):
+        ia = g.step(hs)
+        ib = o.step(cpu_state)
+        assert ia.tau == ib.tau, k
+        assert g.last_ingest_bytes() < 3 * 8 * st.H.size
+    assert_state_bitwise(hs, cpu_state, "pinned sparse ingest")
+    with pytest.raises(ConfigError, match="upload"):
+        g.download(FlowState(st.nx, st.ny, 0.0, np.empty_like(st.H), np.empty_like(st.H),
+                             np.empty_like(st.H)))
+    g.upload(hs)  # a fresh upload makes the resident state complete again
+    g.step_resident()
+    o.step(cpu_state)
+    out = FlowState(st.nx, st.ny, 0.0, np.empty_like(st.H), np.empty_like(st.H), np.empty_like(st.H))
+    g.download(out)
+    assert_state_bitwise(out, cpu_state, "resident after pinned steps")
