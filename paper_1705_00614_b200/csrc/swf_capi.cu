@@ -291,6 +291,7 @@ int create_impl(const swf_terrain* T, const swf_params* P, const swf_control* K,
   }
   for (int i = 0; i < 10 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
   if (e == cudaSuccess && fused_prepare(c) != SWF_OK) e = cudaErrorInvalidValue;
+  if (e == cudaSuccess && fused_tile_srcm(c) != SWF_OK) e = cudaErrorInvalidValue;
   if (e != cudaSuccess) {
     rc = cuda_check(nullptr, e, "context allocation");
     swf_destroy(c);
@@ -375,6 +376,7 @@ void swf_destroy(swf_ctx* c) {
   void* ptrs[] = {c->b, c->nf, c->H[0], c->H[1], c->HUx[0], c->HUx[1], c->HUy[0], c->HUy[1],
                   c->fpx, c->fpy, c->d_src, c->d_ht, c->d_hq, c->d_sig, c->d_wt, c->d_wv,
                   c->d_interior, c->d_halo, c->d_bflag, c->d_tile_act, c->d_tile_same,
+                  c->d_tile_srcm,
                   c->d_part, c->d_sc};
   for (void* p : ptrs) cudaFree(p);
   if (c->h_sc) cudaFreeHost(c->h_sc);
@@ -475,6 +477,10 @@ int swf_set_sources(swf_ctx* c, int n, const swf_source* s) {
     }
   }
   c->geo.nsrc = n;
+  if (e == cudaSuccess) {
+    int rc = fused_tile_srcm(c);
+    if (rc) return rc;
+  }
   if (n == 0) stage_clear_sources(c);  // src_.clear_values(), stepper.cpp:169
   invalidate_mask(c);
   drop_graph(c);

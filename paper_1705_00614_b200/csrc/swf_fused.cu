@@ -25,6 +25,8 @@
 // ping-pong buffers.
 #include <cuda_runtime.h>
 
+#include <vector>
+
 #include "swf_internal.cuh"
 
 namespace swf {
@@ -36,6 +38,7 @@ constexpr int AX = BX, AY = BY;
 constexpr int AREGX = AX + 2, AREGY = AY + 2, AREG = AREGX * AREGY;  // 1-cell halo
 constexpr int RX = BX + 4, RY = BY + 4, RREG = RX * RY;              // 2-cell halo
 constexpr int NTHR = 256;  // k_forces, k_reduce, k_scatter_host
+constexpr int MAXBF = 64;  // B-block flags of one tile staged in shared memory
 #ifndef SWF_STEP_THREADS
 #define SWF_STEP_THREADS 256
 #endif
@@ -275,6 +278,7 @@ struct ForcesArgs {
   StepScalars* sc;
   double* cnt_part;  // per-tile diagnostics partials: slots 3, 4 = block counts
   const unsigned char* tile_prev;  // tile flags of the previous step
+  const unsigned* tile_srcm;       // per owned tile (see StepArgs)
   int ra0, ra1, tr_lo, do_mask;
 };
 
@@ -296,8 +300,10 @@ __global__ void __launch_bounds__(NTHR, SWF_FORCES_MINB) k_forces(Geo G, ForcesA
 #endif
   // mask rows (owned rows only)
   const bool mask_tile = A.do_mask && tr >= 0 && tr < G.tiles_y;
+  const bool own_row = tr >= 0 && tr < G.tiles_y;
   if (tid == 0)
-    s_srcm = src_mask_for(G, A.src, i0 - 1, i0 + BX, G.jg0 + rr0 - 1, G.jg0 + rr0 + BY);
+    s_srcm = own_row ? A.tile_srcm[tx + tr * G.tiles_x]
+                     : src_mask_for(G, A.src, i0 - 1, i0 + BX, G.jg0 + rr0 - 1, G.jg0 + rr0 + BY);
   // Dry neighbourhood: if this tile and its 8 neighbours had no flux-active
   // block in the previous step, k_step left all their cells untouched, so
   // this tile's block counts, flags and (empty) forces are unchanged: skip.
@@ -504,6 +510,7 @@ struct StepArgs {
   const unsigned char* bflag;
   const unsigned char* tile_act;
   unsigned char* tile_same;
+  const unsigned* tile_srcm;  // per owned tile: source specs meeting the tile +- 2 cells
   double* part;  // 3 per tile
   StepScalars* sc;
 };
@@ -604,8 +611,8 @@ __global__ void __launch_bounds__(STHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
   double* R = smem;                       // F_NUM x RREG
   double* SL = smem + F_NUM * RREG;       // 3 x NSL slopes (eta, un, ut)
   double* FB = SL + 3 * NSL;              // 4 x NFC faces (fm, fnl, fnr, ft)
-  __shared__ unsigned s_srcm;
   __shared__ double s_red[3][STHR / 32];
+  __shared__ unsigned char s_bf[MAXBF];
   const PhysConst& P = G.P;  // reciprocals refined at context creation (fused_prepare)
   StepScalars* sc = A.sc;
   if (stopped(sc)) return;
@@ -640,12 +647,19 @@ __global__ void __launch_bounds__(STHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
 #ifdef SWF_PHASE_TIMING
   long long t_ph = clock64();
 #endif
-  if (tid == 0)
-    s_srcm = src_mask_for(G, A.src, i0 - 2, i0 + BX + 1, G.jg0 + r0 - 2, G.jg0 + r0 + BY + 1);
-  __syncthreads();
-  const unsigned srcm = s_srcm;
+  // per-tile source masks are precomputed at set_sources (tile +- 2 cells);
+  // every per-step scalar is loaded here, ahead of the region loads
+  const unsigned srcm = A.tile_srcm[tile];
   const double tau = sc->tau;
   const double half_tau = 0.5 * tau;
+  const double wmx = sc->wind_mid[0], wmy = sc->wind_mid[1];
+  // the tile's B-block flags (phase 5), staged once
+  const int bi_lo = i0 / G.bs, bj_lo = (G.jg0 + r0) / G.bs;
+  const int nbi = (min(i0 + BX, G.nx) - 1) / G.bs - bi_lo + 1;
+  const int nbj = (min(G.jg0 + r0 + BY, G.jg0 + G.r1) - 1) / G.bs - bj_lo + 1;
+  const bool bf_staged = nbi * nbj <= MAXBF;
+  if (bf_staged && tid < nbi * nbj)
+    s_bf[tid] = A.bflag[(bi_lo + tid % nbi) + (bj_lo + tid / nbi - G.bj0) * G.nbx];
   const int nsrc = G.nsrc;
   const double* sig_n = A.sig;
   const double* sig_m = A.sig + nsrc;
@@ -736,7 +750,6 @@ __global__ void __launch_bounds__(STHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
   // state for active cells, the step-start state otherwise (stepper.cpp:641-651)
   double Ht[PER], Qx[PER], Qy[PER];
   double srcvol = 0.0;
-  const double wmx = sc->wind_mid[0], wmy = sc->wind_mid[1];
 #pragma unroll
   for (int m = 0; m < PER; ++m) {
     int c = tid + m * STHR;
@@ -969,8 +982,9 @@ __global__ void __launch_bounds__(STHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
     int jg = G.jg0 + r;
     int s = (x + 2) + (y + 2) * RX;
     size_t k = (size_t)i + (size_t)r * nx;
-    int lb = i / G.bs + (jg / G.bs - G.bj0) * G.nbx;
-    bool flux_on = !G.skip || (A.bflag[lb] & 2);
+    unsigned char bfl = bf_staged ? s_bf[(i / G.bs - bi_lo) + (jg / G.bs - bj_lo) * nbi]
+                                  : A.bflag[i / G.bs + (jg / G.bs - G.bj0) * G.nbx];
+    bool flux_on = !G.skip || (bfl & 2);
     if (!flux_on) {  // block skipped by the reference: state unchanged
       A.Ho[k] = Ht[m];  // no active cell in such a block: (Ht, Qx, Qy) = step-start state
       A.HUxo[k] = Qx[m];
@@ -1094,6 +1108,7 @@ StepArgs step_args(swf_ctx* c) {
   A.bflag = c->d_bflag;
   A.tile_act = tile_act_at(c, c->cur);
   A.tile_same = c->d_tile_same;
+  A.tile_srcm = c->d_tile_srcm;
   A.part = c->d_part;
   A.sc = c->d_sc;
   return A;
@@ -1188,6 +1203,7 @@ int fused_enqueue_phase1(swf_ctx* c, double dt_cap, int part) {
   A.bflag = c->d_bflag;
   A.tile_act = tile_act_at(c, c->cur);
   A.tile_prev = tile_act_at(c, 1 - c->cur);
+  A.tile_srcm = c->d_tile_srcm;
   A.sc = c->d_sc;
   A.cnt_part = c->d_part;
   forces_rows(c, A.ra0, A.ra1);
@@ -1352,6 +1368,34 @@ extern "C" int swf_debug_phase_cycles(unsigned long long* out16, int reset) {
 }
 #endif
 int fused_reduce_ctas() { return RED_CTAS; }
+
+// Per-tile source masks (bit s: spec s meets the tile's cells +- 2), the
+// host-side equivalent of src_mask_for, refreshed whenever the specs change.
+int fused_tile_srcm(swf_ctx* c) {
+  const Geo& G = c->geo;
+  size_t nt = (size_t)G.tiles_x * G.tiles_y;
+  std::vector<unsigned> m(nt ? nt : 1, 0u);
+  for (size_t t = 0; t < nt; ++t) {
+    int tx = (int)(t % G.tiles_x), ty = (int)(t / G.tiles_x);
+    int ci0 = tx * BX - 2, ci1 = tx * BX + BX + 1;
+    int cj0 = G.jg0 + G.r0 + ty * BY - 2, cj1 = G.jg0 + G.r0 + ty * BY + BY + 1;
+    unsigned v = 0;
+    if (G.nsrc > 32) {
+      v = 0xffffffffu;
+    } else {
+      for (int q = 0; q < G.nsrc; ++q) {
+        const DevSrc& d = c->h_src[q];
+        if (d.i0 <= ci1 && d.i1 >= ci0 && d.j0 <= cj1 && d.j1 >= cj0) v |= 1u << q;
+      }
+    }
+    m[t] = v;
+  }
+  cudaError_t e = cudaSuccess;
+  if (!c->d_tile_srcm) e = cudaMalloc(&c->d_tile_srcm, m.size() * sizeof(unsigned));
+  if (e == cudaSuccess)
+    e = cudaMemcpy(c->d_tile_srcm, m.data(), m.size() * sizeof(unsigned), cudaMemcpyHostToDevice);
+  return cuda_check(c, e, "tile source masks");
+}
 
 // Kernel attributes must be set outside stream capture (a CUDA graph does not
 // record cudaFuncSetAttribute), so contexts call this at creation.

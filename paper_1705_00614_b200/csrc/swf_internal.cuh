@@ -102,6 +102,7 @@ struct swf_ctx {
   unsigned char* d_bflag = nullptr;  // bit0 lagrangian-active, bit1 flux-active
   unsigned char* d_tile_act = nullptr;  // 2 x tiles: [cur] this step, [1-cur] previous
   unsigned char* d_tile_same = nullptr;  // tile identical in both state buffers
+  unsigned* d_tile_srcm = nullptr;       // per-tile source-spec masks (fused_tile_srcm)
   double* d_part = nullptr;              // per-tile diagnostic partials (3 per tile)
   // scalars
   swf::StepScalars* d_sc = nullptr;
@@ -153,6 +154,7 @@ int fused_enqueue_phase2(swf_ctx* c, double dt_cap, double global_speed, const d
 int fused_enqueue_phase1(swf_ctx* c, double dt_cap, int part);
 int fused_local_speed(swf_ctx* c, double* dev_out);
 int fused_ingest_hu(swf_ctx* c, const double* hHUx, const double* hHUy);
+int fused_tile_srcm(swf_ctx* c);
 
 int launch_begin(swf_ctx* c, double dt_cap);  // sources/wind at t_n, reset counters
 int launch_mask(swf_ctx* c);                   // K1 block mask + tile flags
