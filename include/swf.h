@@ -161,6 +161,10 @@ int swf_step_host(swf_ctx* ctx, double* H, double* HUx, double* HUy,
  * zero-copy ingest; afterwards the resident calls need swf_upload_state);
  * otherwise the three full fields. */
 int swf_last_ingest_bytes(const swf_ctx* ctx, long long* bytes);
+/* Tiles of the last synchronised step whose speculative divisions were
+ * rejected and that were recomputed exactly: counts[0] forces, [1] step
+ * (diagnostics; see the speculative-division note in swf_fused.cu). */
+int swf_debug_redo_counts(const swf_ctx* ctx, int* counts);
 /* One step on the device-resident state; info may be NULL (then no host
  * synchronisation happens and errors surface at the next synchronising
  * call). */
@@ -214,6 +218,9 @@ int swf_dev_hll_face_flux(int n, const double* in, double g, double* out);
 /* the shared-reciprocal division of the kernels against plain IEEE division:
  * in = n x {a, b}, out = n x {rdiv(a, recip_of(b)), a/b} (must be equal). */
 int swf_dev_rdiv(int n, const double* ab, double* out);
+/* the speculative form the fused kernels use: out = n x {q, accepted}; an
+ * accepted q must equal a/b bit for bit (rejected items are redone exactly). */
+int swf_dev_rdiv_spec(int n, const double* ab, double* out);
 /* the libm-compatible cube root used by friction (forcing.hpp:81). */
 int swf_dev_cbrt(int n, const double* x, double* y);
 /* bottom_friction, forcing.cpp:26-28: in = n x {ux,uy,H}, out = n x {fx,fy}. */

@@ -59,6 +59,7 @@ def declare(lib):
     _sig(lib, "swf_dev_hll_face_flux", I, I, PD, D, PD)
     _sig(lib, "swf_dev_cbrt", I, I, PD, PD)
     _sig(lib, "swf_dev_rdiv", I, I, PD, PD)
+    _sig(lib, "swf_dev_rdiv_spec", I, I, PD, PD)
     _sig(lib, "swf_dev_bottom_friction", I, I, PD, D, D, PD)
     _sig(lib, "swf_strip_phase1", I, P, D, PD)
     _sig(lib, "swf_strip_phase2", I, P, D, D, PN)
@@ -67,6 +68,7 @@ def declare(lib):
     _sig(lib, "swf_strip_pack", I, P, I, C.c_void_p)
     _sig(lib, "swf_strip_unpack", I, P, I, C.c_void_p)
     _sig(lib, "swf_last_ingest_bytes", I, P, C.POINTER(C.c_longlong))
+    _sig(lib, "swf_debug_redo_counts", I, P, PI)
     _sig(lib, "swf_strip_begin_batch", I, P)
     _sig(lib, "swf_strip_forces", I, P, D, I)
     _sig(lib, "swf_strip_local_speed", I, P, C.c_void_p)

@@ -79,11 +79,13 @@ def build(force=False, verbose=False):
 
 def build_variant(name, defines):
     """Developer A/B builds: paper_1705_00614_b200/variants/libswf_<name>.so with
-    extra -D flags (select one at run time with SWF_LIB=...)."""
+    extra -D flags or raw nvcc flags (arguments starting with '-'); select one
+    at run time with SWF_LIB=..."""
     vdir = os.path.join(HERE, "variants")
     os.makedirs(vdir, exist_ok=True)
     out = os.path.join(vdir, f"libswf_{name}.so")
-    cmd = [nvcc()] + NVCC_FLAGS + [f"-D{d}" for d in defines] + ["-shared", "-o", out] + \
+    extra = [d if d.startswith("-") else f"-D{d}" for d in defines]
+    cmd = [nvcc()] + NVCC_FLAGS + extra + ["-shared", "-o", out] + \
         [os.path.join(CSRC, s) for s in SOURCES]
     subprocess.run(cmd, check=True, cwd=CSRC)
     return out

@@ -376,7 +376,7 @@ void swf_destroy(swf_ctx* c) {
   void* ptrs[] = {c->b, c->nf, c->H[0], c->H[1], c->HUx[0], c->HUx[1], c->HUy[0], c->HUy[1],
                   c->fpx, c->fpy, c->d_src, c->d_ht, c->d_hq, c->d_sig, c->d_wt, c->d_wv,
                   c->d_interior, c->d_halo, c->d_bflag, c->d_tile_act, c->d_tile_same,
-                  c->d_tile_srcm,
+                  c->d_tile_srcm, c->d_redo_f, c->d_redo_s,
                   c->d_part, c->d_sc};
   for (void* p : ptrs) cudaFree(p);
   if (c->h_sc) cudaFreeHost(c->h_sc);
@@ -640,6 +640,13 @@ int swf_step_host(swf_ctx* c, double* H, double* HUx, double* HUy, double* t, do
   return swf_download_state(c, H, HUx, HUy, t);
 }
 
+int swf_debug_redo_counts(const swf_ctx* c, int* counts) {
+  if (!c || !counts) return SWF_ECONFIG;
+  counts[0] = c->h_sc->redo_n[0];
+  counts[1] = c->h_sc->redo_n[1];
+  return SWF_OK;
+}
+
 int swf_last_ingest_bytes(const swf_ctx* c, long long* bytes) {
   if (!c || !bytes) return SWF_ECONFIG;
   *bytes = c->last_ingest_bytes;
@@ -869,6 +876,16 @@ __global__ void k_rdiv(int n, const double* in, double* out) {
   out[2 * (size_t)i + 1] = a / b;
 }
 
+// speculative mode: out[2i] = fast-path quotient, out[2i+1] = 1.0 if accepted
+__global__ void k_rdiv_spec(int n, const double* in, double* out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double a = in[2 * (size_t)i], b = in[2 * (size_t)i + 1];
+  bool ok = true;
+  out[2 * (size_t)i] = rdiv(a, recip_of(b), &ok);
+  out[2 * (size_t)i + 1] = ok ? 1.0 : 0.0;
+}
+
 __global__ void k_cbrt(int n, const double* x, double* y) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) y[i] = glibc_cbrt(x[i]);
@@ -913,6 +930,12 @@ int swf_dev_hll_face_flux(int n, const double* in, double g, double* out) {
 int swf_dev_rdiv(int n, const double* ab, double* out) {
   return run_kat(2 * (size_t)n, ab, 2 * (size_t)n, out, [&](double* di, double* dout) {
     k_rdiv<<<(n + 255) / 256, 256>>>(n, di, dout);
+  });
+}
+
+int swf_dev_rdiv_spec(int n, const double* ab, double* out) {
+  return run_kat(2 * (size_t)n, ab, 2 * (size_t)n, out, [&](double* di, double* dout) {
+    k_rdiv_spec<<<(n + 255) / 256, 256>>>(n, di, dout);
   });
 }
 

@@ -92,6 +92,8 @@ __global__ void k_begin(Geo G, const DevSrc* src, const double* ht, const double
   sc->wind_n[0] = series_at(wt, wv, G.nwind, 2, 0, t);
   sc->wind_n[1] = series_at(wt, wv, G.nwind, 2, 1, t);
   sc->speed_bits = 0ull;
+  sc->redo_n[0] = 0;
+  sc->redo_n[1] = 0;
   for (int q = 0; q < SPEED_SLOTS; ++q) sc->speed_slots[q] = 0ull;
   sc->lag_act = 0;
   sc->flux_act = 0;
@@ -251,6 +253,20 @@ __device__ __forceinline__ double msig(const Geo& G, const DevSrc* src, const do
 }
 
 // ---------------------------------------------------------------------------
+// Speculative division.  The tile bodies are templates on SPEC.  With SPEC,
+// every rdiv returns its fast-path quotient and clears the thread's flag
+// `sok` when that quotient was not accepted (tiny or denormal operands), so
+// the bodies carry no slow-path branches; a tile with any rejected division
+// is appended to a redo list instead of publishing its CFL speed or error,
+// and a second, exact (SPEC = false) launch recomputes the listed tiles from
+// the same inputs.  Every result is therefore the exact one, bit for bit.
+// ---------------------------------------------------------------------------
+#ifndef SWF_SPECULATE
+#define SWF_SPECULATE 1
+#endif
+#define SP (SPEC ? &sok : (bool*)nullptr)
+
+// ---------------------------------------------------------------------------
 // k_forces: K1 + K2 + K3 on a BX x BY tile with a 1-cell halo.
 //  * K1 (fused when the block size divides 16): interior / clamped-ring wet
 //    counts of the tile's B-blocks (block.cpp:16-61), block flags, tile flags.
@@ -279,20 +295,26 @@ struct ForcesArgs {
   double* cnt_part;  // per-tile diagnostics partials: slots 3, 4 = block counts
   const unsigned char* tile_prev;  // tile flags of the previous step
   const unsigned* tile_srcm;       // per owned tile (see StepArgs)
+  int* redo;                       // tiles whose speculative divisions were rejected
   int ra0, ra1, tr_lo, do_mask;
 };
 
-__global__ void __launch_bounds__(NTHR, SWF_FORCES_MINB) k_forces(Geo G, ForcesArgs A) {
+// redo-list entries: tile column + (tile row + REDO_ROW0) * tiles_x
+constexpr int REDO_ROW0 = 4;
+
+template <bool SPEC>
+__device__ __forceinline__ void forces_tile(const Geo& G, const ForcesArgs& A, const int tx,
+                                            const int tr) {
   __shared__ double s_d[AREG], s_e[AREG], s_u[AREG], s_v[AREG];
   __shared__ unsigned char s_w[AREG];
   __shared__ int s_cnt[3];
   __shared__ unsigned s_srcm;
   __shared__ unsigned long long s_max[NTHR / 32];
   StepScalars* sc = A.sc;
-  if (stopped(sc)) return;
+  if (__syncthreads_or(stopped(sc))) return;
+  bool sok = true;  // every speculative division of this thread accepted
   const PhysConst& P = G.P;  // reciprocals refined at context creation (fused_prepare)
   const int tid = threadIdx.x;
-  const int tx = blockIdx.x % G.tiles_x, tr = (int)(blockIdx.x / G.tiles_x) + A.tr_lo;
   const int i0 = tx * BX, rr0 = G.r0 + tr * BY;
   const size_t nx = G.nx;
 #ifdef SWF_EXP_EXIT_ALL
@@ -424,8 +446,8 @@ __global__ void __launch_bounds__(NTHR, SWF_FORCES_MINB) k_forces(Geo G, ForcesA
     double e = d + s_e[c], u = 0.0, v = 0.0;
     if (d > P.eps) {
       Recip Rd = recip_of(d);
-      u = rdiv(s_u[c], Rd);
-      v = rdiv(s_v[c], Rd);
+      u = rdiv(s_u[c], Rd, SP);
+      v = rdiv(s_v[c], Rd, SP);
     }
     s_e[c] = e;
     s_u[c] = u;
@@ -461,7 +483,7 @@ __global__ void __launch_bounds__(NTHR, SWF_FORCES_MINB) k_forces(Geo G, ForcesA
     double n = G.has_nfield ? A.nf[k] : G.n_manning;
     double ux = s_u[s], uy = s_v[s];
     ForceOut o = cell_forces(d, ux, uy, s_e[s], W, E, S, N, n, P, G.nwind > 0, wx, wy, sg, svx,
-                             svy);
+                             svy, SP);
     A.fpx[k] = o.fx - o.frx;
     A.fpy[k] = o.fy - o.fry;
     m = cfl_speed(m, d, ux, uy, o.fx, o.fy, P.g, P.h);
@@ -473,12 +495,32 @@ __global__ void __launch_bounds__(NTHR, SWF_FORCES_MINB) k_forces(Geo G, ForcesA
     bits = ob > bits ? ob : bits;
   }
   if ((tid & 31) == 0) s_max[tid >> 5] = bits;
-  __syncthreads();
+  const bool any_bad = __syncthreads_or(!sok);  // (also orders the s_max writes)
+  const bool redo = SPEC && any_bad;
   if (tid == 0) {
-    unsigned long long mb = 0;
-    for (int w = 0; w < NTHR / 32; ++w) mb = s_max[w] > mb ? s_max[w] : mb;
-    // spread over SPEED_SLOTS addresses to avoid one contended L2 atomic
-    if (mb) atomicMax(&sc->speed_slots[blockIdx.x % SPEED_SLOTS], mb);
+    if (redo) {  // recomputed exactly by k_forces_redo; publish nothing
+      A.redo[atomicAdd(&sc->redo_n[0], 1)] = tx + (tr + REDO_ROW0) * G.tiles_x;
+    } else {
+      unsigned long long mb = 0;
+      for (int w = 0; w < NTHR / 32; ++w) mb = s_max[w] > mb ? s_max[w] : mb;
+      // spread over SPEED_SLOTS addresses to avoid one contended L2 atomic
+      if (mb) atomicMax(&sc->speed_slots[(tx + tr * 7) & (SPEED_SLOTS - 1)], mb);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(NTHR, SWF_FORCES_MINB) k_forces(Geo G, ForcesArgs A) {
+  const int tx = blockIdx.x % G.tiles_x, tr = (int)(blockIdx.x / G.tiles_x) + A.tr_lo;
+  forces_tile<SWF_SPECULATE != 0>(G, A, tx, tr);
+}
+
+// the tiles with a rejected speculative division, recomputed exactly
+__global__ void __launch_bounds__(NTHR, SWF_FORCES_MINB) k_forces_redo(Geo G, ForcesArgs A) {
+  const int n = *(volatile int*)&A.sc->redo_n[0];
+  for (int q = blockIdx.x; q < n; q += gridDim.x) {
+    int e = A.redo[q];
+    forces_tile<false>(G, A, e % G.tiles_x, e / G.tiles_x - REDO_ROW0);
+    __syncthreads();
   }
 }
 
@@ -511,6 +553,7 @@ struct StepArgs {
   const unsigned char* tile_act;
   unsigned char* tile_same;
   const unsigned* tile_srcm;  // per owned tile: source specs meeting the tile +- 2 cells
+  int* redo;                  // tiles whose speculative divisions were rejected
   double* part;  // 3 per tile
   StepScalars* sc;
 };
@@ -557,7 +600,7 @@ struct Slopes {
 
 __device__ __forceinline__ Slopes cell_slopes(double em, double um, double tm, double sm, double ec,
                                               double uc, double tc, double sc_, double ep, double up,
-                                              double tp, double sp, double h) {
+                                              double tp, double sp, double h, bool* ok = nullptr) {
   // the + side face: in = +1 neighbour, out = -1 neighbour, sgn = +1
   double p_in = 1.0 * h + sp;
   double p_out = -1.0 * h + sm;
@@ -565,9 +608,9 @@ __device__ __forceinline__ Slopes cell_slopes(double em, double um, double tm, d
   double d_out = sc_ - p_out;
   Slopes s;
   Recip Ri = recip_of(d_in), Ro = recip_of(d_out);
-  s.eta = minmod(rdiv(ep - ec, Ri), rdiv(ec - em, Ro));
-  s.un = minmod(rdiv(up - uc, Ri), rdiv(uc - um, Ro));
-  s.ut = minmod(rdiv(tp - tc, Ri), rdiv(tc - tm, Ro));
+  s.eta = minmod(rdiv(ep - ec, Ri, ok), rdiv(ec - em, Ro, ok));
+  s.un = minmod(rdiv(up - uc, Ri, ok), rdiv(uc - um, Ro, ok));
+  s.ut = minmod(rdiv(tp - tc, Ri, ok), rdiv(tc - tm, Ro, ok));
   return s;
 }
 
@@ -606,7 +649,8 @@ __device__ __forceinline__ FaceRec face_from_sides(bool wetA, bool wetB, const S
   return rec;
 }
 
-__global__ void __launch_bounds__(STHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A) {
+template <bool SPEC>
+__device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const int tile) {
   extern __shared__ double smem[];
   double* R = smem;                       // F_NUM x RREG
   double* SL = smem + F_NUM * RREG;       // 3 x NSL slopes (eta, un, ut)
@@ -615,9 +659,10 @@ __global__ void __launch_bounds__(STHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
   __shared__ unsigned char s_bf[MAXBF];
   const PhysConst& P = G.P;  // reciprocals refined at context creation (fused_prepare)
   StepScalars* sc = A.sc;
-  if (stopped(sc)) return;
+  if (__syncthreads_or(stopped(sc))) return;
+  bool sok = true;  // every speculative division of this thread accepted
+  unsigned long long my_err = ERR_NONE;  // published once the tile is known exact
   const int tid = threadIdx.x;
-  const int tile = blockIdx.x;
   const int tx = tile % G.tiles_x, ty = tile / G.tiles_x;
   const int i0 = tx * BX;         // first owned column
   const int r0 = G.r0 + ty * BY;  // first owned local row
@@ -719,13 +764,13 @@ __global__ void __launch_bounds__(STHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
       if (act) {
         bool wet = Hn > P.eps;
         double fx = wet ? SC[c] : 0.0, fy = wet ? SC[RREG + c] : 0.0;
-        predict_cell(Hn, mx, my, sg, fx, fy, NF[c], half_tau, P.eps, P.g, d, mx, my);
+        predict_cell(Hn, mx, my, sg, fx, fy, NF[c], half_tau, P.eps, P.g, d, mx, my, SP);
       }
       e = d + bb;
       if (d > P.eps) {
         Recip Rd = recip_of(d);
-        u = rdiv(mx, Rd);
-        v = rdiv(my, Rd);
+        u = rdiv(mx, Rd, SP);
+        v = rdiv(my, Rd, SP);
       }
       if (act) {
         // shift = 0.5*dr with dr = tau * u12 (stepper.cpp:72-73, 373-379);
@@ -787,12 +832,13 @@ __global__ void __launch_bounds__(STHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
       Nbr S = nb(jg > 0, s - RX), N = nb(jg + 1 < G.ny, s + RX);
       ForceOut o = cell_forces(d, R[F_U * RREG + s], R[F_V * RREG + s], R[F_E * RREG + s], W,
                                E, S, N, n, P, G.nwind > 0, wmx, wmy, nsrc > 0 ? sgm : 0.0, svx,
-                               svy);
+                               svy, SP);
       fmx = o.fx - o.frx;
       fmy = o.fy - o.fry;
     }
     double ht, qx, qy, sv;
-    correct_cell(Hn, qxn, qyn, nsrc > 0, sgm, d, fmx, fmy, n, tau, P.eps, P.g, ht, qx, qy, sv);
+    correct_cell(Hn, qxn, qyn, nsrc > 0, sgm, d, fmx, fmy, n, tau, P.eps, P.g, ht, qx, qy, sv,
+                 SP);
     srcvol += sv;
     // CFL abort (stepper.cpp:378-380, 391-399): dr = tau * u12
     double dx = tau * R[F_U * RREG + s], dy = tau * R[F_V * RREG + s];
@@ -800,7 +846,8 @@ __global__ void __launch_bounds__(STHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
     if (fabs(dx) >= half_h || fabs(dy) >= half_h) {
       int ib = i / G.bs + (jg / G.bs) * G.nbx;
       unsigned long long local = (unsigned long long)((jg % G.bs) * G.bs + (i % G.bs));
-      atomicMin(&sc->err_key, (ERR_CFL << 58) | ((unsigned long long)ib << 24) | local);
+      unsigned long long key = (ERR_CFL << 58) | ((unsigned long long)ib << 24) | local;
+      my_err = key < my_err ? key : my_err;
     }
     Ht[m] = ht;
     Qx[m] = qx;
@@ -819,7 +866,7 @@ __global__ void __launch_bounds__(STHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
                              R[F_SX * RREG + s - 1], R[F_E * RREG + s], R[F_U * RREG + s],
                              R[F_V * RREG + s], R[F_SX * RREG + s], R[F_E * RREG + s + 1],
                              R[F_U * RREG + s + 1], R[F_V * RREG + s + 1], R[F_SX * RREG + s + 1],
-                             P.h);
+                             P.h, SP);
       se = q.eta;
       su = q.un;
       st = q.ut;
@@ -872,7 +919,10 @@ __global__ void __launch_bounds__(STHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
                                   bf);
           }
           rec = face_from_sides(wetA, wetB, L, Rr, P.g);
-          if (!face_finite(rec)) atomicMin(&sc->err_key, fused_flux_key(G, A.bflag, 0, jg, f));
+          if (!face_finite(rec)) {
+            unsigned long long key = fused_flux_key(G, A.bflag, 0, jg, f);
+            my_err = key < my_err ? key : my_err;
+          }
         }
       }
     }
@@ -906,7 +956,7 @@ __global__ void __launch_bounds__(STHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
                              R[F_U * RREG + s - RX], R[F_SY * RREG + s - RX], R[F_E * RREG + s],
                              R[F_V * RREG + s], R[F_U * RREG + s], R[F_SY * RREG + s],
                              R[F_E * RREG + s + RX], R[F_V * RREG + s + RX],
-                             R[F_U * RREG + s + RX], R[F_SY * RREG + s + RX], P.h);
+                             R[F_U * RREG + s + RX], R[F_SY * RREG + s + RX], P.h, SP);
       se = q.eta;
       su = q.un;
       st = q.ut;
@@ -957,7 +1007,10 @@ __global__ void __launch_bounds__(STHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
                                   face_m, bf);
           }
           rec = face_from_sides(wetA, wetB, L, Rr, P.g);
-          if (!face_finite(rec)) atomicMin(&sc->err_key, fused_flux_key(G, A.bflag, 1, i, jf));
+          if (!face_finite(rec)) {
+            unsigned long long key = fused_flux_key(G, A.bflag, 1, i, jf);
+            my_err = key < my_err ? key : my_err;
+          }
         }
       }
     }
@@ -1009,8 +1062,8 @@ __global__ void __launch_bounds__(STHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
         return o;
       };
       double eta_c = R[F_E * RREG + s];
-      double gx = eta_grad_comp(nb(i > 0, s - 1), nb(i + 1 < G.nx, s + 1), eta_c, P);
-      double gy = eta_grad_comp(nb(jg > 0, s - RX), nb(jg + 1 < G.ny, s + RX), eta_c, P);
+      double gx = eta_grad_comp(nb(i > 0, s - 1), nb(i + 1 < G.nx, s + 1), eta_c, P, SP);
+      double gy = eta_grad_comp(nb(jg > 0, s - RX), nb(jg + 1 < G.ny, s + RX), eta_c, P, SP);
       double gh = (P.g * d) * P.h;
       cx = gh * gx;
       cy = gh * gy;
@@ -1042,6 +1095,27 @@ __global__ void __launch_bounds__(STHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
     double v = 0.0;
     for (int w = 0; w < STHR / 32; ++w) v += s_red[tid][w];
     A.part[5 * (size_t)tile + tid] = v;
+  }
+  // a tile with a rejected speculative division is redone exactly (its
+  // outputs and partials are overwritten there); otherwise publish errors
+  const bool any_bad = __syncthreads_or(!sok);
+  const bool redo = SPEC && any_bad;
+  if (redo) {
+    if (tid == 0) A.redo[atomicAdd(&sc->redo_n[1], 1)] = tile;
+  } else if (my_err != ERR_NONE) {
+    atomicMin(&sc->err_key, my_err);
+  }
+}
+
+__global__ void __launch_bounds__(STHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A) {
+  step_tile<SWF_SPECULATE != 0>(G, A, blockIdx.x);
+}
+
+__global__ void __launch_bounds__(STHR, SWF_STEP_MINB) k_step_redo(Geo G, StepArgs A) {
+  const int n = *(volatile int*)&A.sc->redo_n[1];
+  for (int q = blockIdx.x; q < n; q += gridDim.x) {
+    step_tile<false>(G, A, A.redo[q]);
+    __syncthreads();
   }
 }
 
@@ -1109,6 +1183,7 @@ StepArgs step_args(swf_ctx* c) {
   A.tile_act = tile_act_at(c, c->cur);
   A.tile_same = c->d_tile_same;
   A.tile_srcm = c->d_tile_srcm;
+  A.redo = c->d_redo_s;
   A.part = c->d_part;
   A.sc = c->d_sc;
   return A;
@@ -1204,6 +1279,7 @@ int fused_enqueue_phase1(swf_ctx* c, double dt_cap, int part) {
   A.tile_act = tile_act_at(c, c->cur);
   A.tile_prev = tile_act_at(c, 1 - c->cur);
   A.tile_srcm = c->d_tile_srcm;
+  A.redo = c->d_redo_f;
   A.sc = c->d_sc;
   A.cnt_part = c->d_part;
   forces_rows(c, A.ra0, A.ra1);
@@ -1214,6 +1290,7 @@ int fused_enqueue_phase1(swf_ctx* c, double dt_cap, int part) {
   if (part < 0) {
     int ntile = G.tiles_x * (tr_hi - A.tr_lo);
     if (ntile > 0) k_forces<<<ntile, NTHR, 0, c->stream>>>(G, A);
+    if (ntile > 0 && SWF_SPECULATE) k_forces_redo<<<RED_CTAS, NTHR, 0, c->stream>>>(G, A);
   } else {
     // interior tile rows [a, b): their 1-row halo stays inside the owned rows
     int a = G.r0 > 0 ? 1 : 0;
@@ -1231,6 +1308,7 @@ int fused_enqueue_phase1(swf_ctx* c, double dt_cap, int part) {
     } else {
       launch(lo, a);
       launch(b, tr_hi);
+      if (SWF_SPECULATE) k_forces_redo<<<RED_CTAS, NTHR, 0, c->stream>>>(G, A);
     }
   }
   if (part != 0) ev(c, 2);
@@ -1258,6 +1336,8 @@ int fused_enqueue_phase2(swf_ctx* c, double dt_cap, double global_speed, const d
   ev(c, 3);
   int nt = G.tiles_x * G.tiles_y;
   if (nt > 0) k_step<<<nt, STHR, step_smem(), c->stream>>>(G, step_args(c));
+  if (nt > 0 && SWF_SPECULATE)
+    k_step_redo<<<RED_CTAS, STHR, step_smem(), c->stream>>>(G, step_args(c));
   ev(c, 4);
   double* red = c->d_part + NPART * (size_t)(nt > 0 ? nt : 1);
   k_reduce<<<RED_CTAS, NTHR, 0, c->stream>>>(c->d_part, nt, red, c->d_sc);
@@ -1418,12 +1498,23 @@ int fused_prepare(swf_ctx* c) {
     cudaFree(d);
   }
   if (e == cudaSuccess) {
-    c->geo.P.rh.r = r[0];
-    c->geo.P.r2h.r = r[1];
+    // outside the normal range the speculative fast path could mistake
+    // +0 / h; r = 0 makes every such quotient fail acceptance instead
+    double h = c->geo.P.h;
+    bool normal = h >= 0x1p-999 && h <= 0x1p999;
+    c->geo.P.rh.r = normal ? r[0] : 0.0;
+    c->geo.P.r2h.r = normal ? r[1] : 0.0;
   }
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_step, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)step_smem());
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_step_redo, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)step_smem());
+  // redo lists: every owned tile, plus the ghost tile rows k_forces covers
+  size_t nredo = (size_t)c->geo.tiles_x * (c->geo.tiles_y + 2 * REDO_ROW0);
+  if (e == cudaSuccess && !c->d_redo_f) e = cudaMalloc(&c->d_redo_f, nredo * sizeof(int));
+  if (e == cudaSuccess && !c->d_redo_s) e = cudaMalloc(&c->d_redo_s, nredo * sizeof(int));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_step, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e == cudaSuccess)

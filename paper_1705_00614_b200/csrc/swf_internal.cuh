@@ -41,6 +41,7 @@ struct StepScalars {
   double deficit, srcvol, outflow;  // this step's diagnostics (volumes)
   double speed_local;               // strips: local max speed (phase 1 out)
   int mask_valid;  // the tile flags of the previous step describe the current state
+  int redo_n[2];   // tiles queued for the exact redo: [0] k_forces, [1] k_step
 };
 
 enum ErrKind : unsigned long long { ERR_DT = 1, ERR_CFL = 2, ERR_FLUX = 3 };
@@ -103,6 +104,8 @@ struct swf_ctx {
   unsigned char* d_tile_act = nullptr;  // 2 x tiles: [cur] this step, [1-cur] previous
   unsigned char* d_tile_same = nullptr;  // tile identical in both state buffers
   unsigned* d_tile_srcm = nullptr;       // per-tile source-spec masks (fused_tile_srcm)
+  int* d_redo_f = nullptr;  // k_forces tiles to redo exactly (speculative division rejected)
+  int* d_redo_s = nullptr;  // k_step tiles to redo exactly
   double* d_part = nullptr;              // per-tile diagnostic partials (3 per tile)
   // scalars
   swf::StepScalars* d_sc = nullptr;

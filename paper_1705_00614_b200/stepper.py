@@ -213,6 +213,13 @@ class CsphTvdStepper:
         self._rc(self._lib.swf_last_ingest_bytes(self._ctx, C.byref(b)))
         return b.value
 
+    def redo_counts(self):
+        """(forces, step) tiles of the last synchronised step recomputed
+        exactly after a rejected speculative division."""
+        a = (C.c_int * 2)()
+        self._rc(self._lib.swf_debug_redo_counts(self._ctx, a))
+        return a[0], a[1]
+
     def active_tiles(self):
         """(updated tiles, all tiles, cells per tile) of the last fused step."""
         a, b, c = C.c_int(), C.c_int(), C.c_int()

@@ -83,6 +83,17 @@ def test_device_rdiv_matches_division():
     assert_bitwise(out[:, 0], out[:, 1], "rdiv vs a/b")
     with np.errstate(all="ignore"):
         assert_bitwise(out[:, 1], a / b, "device a/b vs IEEE")
+    # the speculative form: every ACCEPTED quotient is the IEEE one; zeros over
+    # finite non-zero divisors are accepted, tiny/denormal operands are not
+    spec = np.empty_like(ab)
+    assert lib().swf_dev_rdiv_spec(ab.shape[0], A.dptr(ab), A.dptr(spec)) == 0
+    acc = spec[:, 1] == 1.0
+    with np.errstate(all="ignore"):
+        q = a / b
+    assert_bitwise(spec[acc, 0], q[acc], "accepted speculative quotient vs a/b")
+    assert acc.mean() > 0.6
+    z = (a == 0) & (np.abs(b) > 2.0 ** -1000) & (np.abs(b) < 2.0 ** 1000)
+    assert acc[z].all()
 
 
 def test_device_friction_known_answer():
@@ -359,3 +370,26 @@ def test_pinned_host_step_sparse_ingest_matches_oracle(gpu_cls, oracle_built):
     out = FlowState(st.nx, st.ny, 0.0, np.empty_like(st.H), np.empty_like(st.H), np.empty_like(st.H))
     g.download(out)
     assert_state_bitwise(out, cpu_state, "resident after pinned steps")
+
+
+def test_speculative_division_redo_path_is_exact(gpu_cls, oracle_built):
+    """Momenta in the subnormal range make the kernels' speculative divisions
+    reject; those tiles are recomputed by the exact redo launches and the
+    result stays bit-identical to the oracle."""
+    sc = S.floodplain(128, 50.0)
+    st = sc.state.copy()
+    wet = np.flatnonzero(st.H > 1e-3)
+    rng = np.random.default_rng(3)
+    pick = rng.choice(wet, 40, replace=False)
+    st.HUx[pick] = 3e-310 * rng.choice([-1.0, 1.0], pick.size)
+    st.HUy[pick[::2]] = -1e-312
+    g = make(gpu_cls, sc)
+    o = make(oracle_built.OracleStepper, sc)
+    a, b = st.copy(), st.copy()
+    redone = 0
+    for _ in range(4):
+        ia, ib = g.step(a), o.step(b)
+        assert ia.tau == ib.tau
+        redone += sum(g.redo_counts())
+    assert redone > 0
+    assert_state_bitwise(a, b, "speculative redo")

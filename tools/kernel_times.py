@@ -30,6 +30,15 @@ def main():
     names = ["begin+mask", "forces", "tau", "-", "-", "-", "step", "reduce+finish"]
     out = {"lib": os.environ.get("SWF_LIB", "default"), "wall_ms": round(wall * 1e3, 3)}
     out.update({names[i]: round(tk[i] * 1e3, 3) for i in (0, 1, 2, 6, 7)})
+    try:
+        st.set_timing(0)
+        st.step_resident()
+        f, s_ = st.redo_counts()
+        na, ntot, _ = st.active_tiles()
+        out["redo_tiles"] = [f, s_]
+        out["active_tiles"] = na
+    except Exception as e:  # older library builds
+        out["redo_tiles"] = str(e)[:40]
     print(json.dumps(out), flush=True)
 
 
