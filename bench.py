@@ -313,8 +313,10 @@ def b200_single(args):
                 "how": "CsphTvdStepper.step(FlowState) on pinned host buffers, every step: H and "
                        "t copied in full (copy engine), the block mask computed on the device, "
                        "HUx/HUy read over PCIe for the flux-active tiles only (every cell whose "
-                       "momentum the step reads or writes back), one fused step, the updated "
-                       "tiles written straight into the pinned host arrays, t read back; "
+                       "momentum the step reads or writes back), one fused step whose k_step "
+                       "writes every updated cell straight into the pinned host arrays (PCIe "
+                       "writes overlapped with the arithmetic; restored on a numerical abort), "
+                       "t read back; d2h counts the flux-active tiles (an upper bound); "
                        "host-timed, synchronised"},
         "gpu_launches": 7 * K,
         "clocks": clk,

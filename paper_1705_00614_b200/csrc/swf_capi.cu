@@ -618,15 +618,30 @@ int swf_step_host(swf_ctx* c, double* H, double* HUx, double* HUy, double* t, do
     if ((rc = launch_begin(c, dt_cap)) || (rc = launch_mask(c)) || (rc = fused_ingest_hu(c, HUx, HUy)))
       return rc;
     c->state_partial = 0;
+    // k_step writes each updated cell into the caller's arrays as it goes
+    // (PCIe writes overlapped with the step's arithmetic)
+    c->wt_host[0] = H;
+    c->wt_host[1] = HUx;
+    c->wt_host[2] = HUy;
     swf_step_info tmp;
     rc = swf_step(c, dt_cap, info ? info : &tmp);
+    c->wt_host[0] = c->wt_host[1] = c->wt_host[2] = nullptr;
     c->state_partial = 1;
-    if (rc) return rc;  // state untouched on abort (stepper.cpp:391-399, 568-577)
+    if (rc) {
+      // numerical abort: put the step-start values back where the step may
+      // have written (state untouched, stepper.cpp:391-399, 568-577)
+      if (rc == SWF_ENUMERICAL) {
+        int rr = fused_restore_host(c, H, HUx, HUy);
+        if (!rr) {
+          cudaError_t e2 = cudaStreamSynchronize(c->stream);
+          if (e2 != cudaSuccess) return cuda_check(c, e2, "step_host restore");
+        }
+      }
+      return rc;
+    }
     int na = 0, ntot = 0, cpt = 0;
     swf_active_tiles(c, &na, &ntot, &cpt);
     c->last_ingest_bytes = (long long)bytes + 2LL * 8 * na * cpt;
-    rc = fused_scatter_host(c, H, HUx, HUy);
-    if (rc) return rc;
     e = cudaMemcpyAsync(t, &c->d_sc->t, sizeof(double), cudaMemcpyDeviceToHost, c->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
     return cuda_check(c, e, "step_host write-back");

@@ -554,6 +554,9 @@ struct StepArgs {
   unsigned char* tile_same;
   const unsigned* tile_srcm;  // per owned tile: source specs meeting the tile +- 2 cells
   int* redo;                  // tiles whose speculative divisions were rejected
+  double* hH;                 // pinned host arrays of a host-buffer step (write-through), or null
+  double* hHUx;
+  double* hHUy;
   double* part;  // 3 per tile
   StepScalars* sc;
 };
@@ -1077,6 +1080,11 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
     A.Ho[k] = H1;
     A.HUxo[k] = qx;
     A.HUyo[k] = qy;
+    if (A.hH) {  // host-buffer step: write the updated cell straight into the caller's arrays
+      A.hH[k] = H1;
+      A.hHUx[k] = qx;
+      A.hHUy[k] = qy;
+    }
   }
   if (tid == 0) A.tile_same[tile] = 0;
 
@@ -1166,6 +1174,9 @@ __global__ void k_finish(const double* red, int nred, StepScalars* sc, double ar
 
 StepArgs step_args(swf_ctx* c) {
   StepArgs A;
+  A.hH = c->wt_host[0];
+  A.hHUx = c->wt_host[1];
+  A.hHUy = c->wt_host[2];
   int cur = c->cur, nxt = 1 - c->cur;
   A.H = c->H[cur];
   A.HUx = c->HUx[cur];
@@ -1383,6 +1394,17 @@ __global__ void k_scatter_host(Geo G, const unsigned char* __restrict__ flags,
       hHUy[k] = HUy[k];
     }
   }
+}
+
+// After an aborted write-through step: the caller's arrays get the step-start
+// state (the buffer the step read) back in every tile the step may have
+// written, so a numerical abort leaves them as they were.
+int fused_restore_host(swf_ctx* c, double* hH, double* hHUx, double* hHUy) {
+  const Geo& G = c->geo;
+  int cur = c->cur;  // not flipped: the failed step read this buffer; its flags are at cur
+  k_scatter_host<<<148 * 8, NTHR, 0, c->stream>>>(G, tile_act_at(c, cur), c->H[cur], c->HUx[cur],
+                                                  c->HUy[cur], hH, hHUx, hHUy);
+  return cuda_check(c, cudaGetLastError(), "k_restore_host");
 }
 
 int fused_scatter_host(swf_ctx* c, double* hH, double* hHUx, double* hHUy) {

@@ -118,6 +118,7 @@ struct swf_ctx {
   // after a sparse-ingest host-buffer step the device holds the momentum of
   // the flux-active tiles only: resident calls need a fresh upload first
   int state_partial = 0;
+  double* wt_host[3] = {nullptr, nullptr, nullptr};  // write-through targets of a host step
   long long last_ingest_bytes = 0;
   int batch_steps = 0;
   int last_staged = 0;  // which path produced the last diagnostics
@@ -150,6 +151,7 @@ int fused_enqueue_step(swf_ctx* c, double dt_cap);
 int fused_prepare(swf_ctx* c);
 int fused_reduce_ctas();
 int fused_scatter_host(swf_ctx* c, double* hH, double* hHUx, double* hHUy);
+int fused_restore_host(swf_ctx* c, double* hH, double* hHUx, double* hHUy);
 int fused_enqueue_phase1(swf_ctx* c, double dt_cap);
 int fused_enqueue_phase2(swf_ctx* c, double dt_cap);
 int fused_enqueue_phase2(swf_ctx* c, double dt_cap, double global_speed);

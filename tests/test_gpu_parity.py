@@ -393,3 +393,21 @@ def test_speculative_division_redo_path_is_exact(gpu_cls, oracle_built):
         redone += sum(g.redo_counts())
     assert redone > 0
     assert_state_bitwise(a, b, "speculative redo")
+
+
+def test_cfl_abort_pinned_write_through_restores_state(gpu_cls, oracle_built):
+    """The pinned host step writes updated cells straight into the caller's
+    arrays during k_step; on a numerical abort they are restored, so the
+    caller's state is untouched, as in the reference."""
+    import torch
+    from paper_1705_00614_b200 import NumericalError
+    from paper_1705_00614_b200.types import FlowState
+    sc = _cfl_case()
+    pin = lambda a: torch.from_numpy(a.copy()).pin_memory().numpy()
+    st = FlowState(sc.state.nx, sc.state.ny, sc.state.t, pin(sc.state.H), pin(sc.state.HUx),
+                   pin(sc.state.HUy))
+    before = st.copy()
+    s = make(gpu_cls, sc)
+    with pytest.raises(NumericalError, match="particle displacement"):
+        s.step(st, 0.1)
+    assert_state_bitwise(st, before, "pinned state changed on abort")
