@@ -376,7 +376,7 @@ void swf_destroy(swf_ctx* c) {
   void* ptrs[] = {c->b, c->nf, c->H[0], c->H[1], c->HUx[0], c->HUx[1], c->HUy[0], c->HUy[1],
                   c->fpx, c->fpy, c->d_src, c->d_ht, c->d_hq, c->d_sig, c->d_wt, c->d_wv,
                   c->d_interior, c->d_halo, c->d_bflag, c->d_tile_act, c->d_tile_same,
-                  c->d_tile_srcm, c->d_redo_f, c->d_redo_s,
+                  c->d_tile_srcm, c->d_redo_f, c->d_redo_s, c->d_list_f, c->d_list_s,
                   c->d_part, c->d_sc};
   for (void* p : ptrs) cudaFree(p);
   if (c->h_sc) cudaFreeHost(c->h_sc);

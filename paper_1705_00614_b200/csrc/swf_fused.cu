@@ -94,6 +94,8 @@ __global__ void k_begin(Geo G, const DevSrc* src, const double* ht, const double
   sc->speed_bits = 0ull;
   sc->redo_n[0] = 0;
   sc->redo_n[1] = 0;
+  sc->list_n[0] = sc->list_n[1] = 0;
+  sc->list_take[0] = sc->list_take[1] = 0;
   for (int q = 0; q < SPEED_SLOTS; ++q) sc->speed_slots[q] = 0ull;
   sc->lag_act = 0;
   sc->flux_act = 0;
@@ -264,6 +266,9 @@ __device__ __forceinline__ double msig(const Geo& G, const DevSrc* src, const do
 #ifndef SWF_SPECULATE
 #define SWF_SPECULATE 1
 #endif
+#ifndef SWF_TILE_LISTS
+#define SWF_TILE_LISTS 1  // work lists + persistent CTAs instead of one CTA per tile
+#endif
 #define SP (SPEC ? &sok : (bool*)nullptr)
 
 // ---------------------------------------------------------------------------
@@ -296,15 +301,18 @@ struct ForcesArgs {
   const unsigned char* tile_prev;  // tile flags of the previous step
   const unsigned* tile_srcm;       // per owned tile (see StepArgs)
   int* redo;                       // tiles whose speculative divisions were rejected
+  int* list;                       // work list of k_flist / k_forces_list
   int ra0, ra1, tr_lo, do_mask;
 };
 
 // redo-list entries: tile column + (tile row + REDO_ROW0) * tiles_x
 constexpr int REDO_ROW0 = 4;
 
+// presel: the tile comes from the work list k_flist built, which already
+// applied the dry-neighbourhood rule below.
 template <bool SPEC>
 __device__ __forceinline__ void forces_tile(const Geo& G, const ForcesArgs& A, const int tx,
-                                            const int tr) {
+                                            const int tr, const bool presel = false) {
   __shared__ double s_d[AREG], s_e[AREG], s_u[AREG], s_v[AREG];
   __shared__ unsigned char s_w[AREG];
   __shared__ int s_cnt[3];
@@ -332,8 +340,8 @@ __device__ __forceinline__ void forces_tile(const Geo& G, const ForcesArgs& A, c
   // Not across a strip boundary (ghost rows change by exchange) and not near
   // a source (sigma(t) can switch a marker on).  Threads 0..8 read one
   // neighbour flag each.
-  const bool may_skip = mask_tile && G.skip && sc->mask_valid && (tr > 0 || G.r0 == 0) &&
-                        (tr < G.tiles_y - 1 || G.r1 == G.rows);
+  const bool may_skip = !presel && mask_tile && G.skip && sc->mask_valid &&
+                        (tr > 0 || G.r0 == 0) && (tr < G.tiles_y - 1 || G.r1 == G.rows);
   bool busy = !may_skip;
   if (may_skip && tid < 9) {
     int x2 = tx + tid % 3 - 1, y2 = tr + tid / 3 - 1;
@@ -514,6 +522,47 @@ __global__ void __launch_bounds__(NTHR, SWF_FORCES_MINB) k_forces(Geo G, ForcesA
   forces_tile<SWF_SPECULATE != 0>(G, A, tx, tr);
 }
 
+// ---- tile work lists (single-context steps) ---------------------------------
+// k_flist: one thread per tile applies the dry-neighbourhood rule of
+// forces_tile and appends the tiles k_forces must visit to A.list; the
+// skipped ones get their flag cleared exactly as forces_tile would.  A
+// persistent k_forces_list grid then takes list entries off an atomic
+// counter, so the ~60 % of C3 tiles that are dry cost one thread, not a CTA.
+__global__ void k_flist(Geo G, ForcesArgs A) {
+  const int nt = G.tiles_x * G.tiles_y;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nt) return;
+  StepScalars* sc = A.sc;
+  const int tx = t % G.tiles_x, tr = t / G.tiles_x;
+  bool busy = !(A.do_mask && G.skip && sc->mask_valid) || A.tile_srcm[t] != 0;
+  for (int q = 0; q < 9 && !busy; ++q) {
+    int x2 = tx + q % 3 - 1, y2 = tr + q / 3 - 1;
+    if (x2 >= 0 && x2 < G.tiles_x && y2 >= 0 && y2 < G.tiles_y)
+      busy = A.tile_prev[x2 + y2 * G.tiles_x] != 0;
+  }
+  if (busy) {
+    A.list[atomicAdd(&sc->list_n[0], 1)] = t;
+  } else {
+    A.tile_act[t] = 0;
+  }
+}
+
+__global__ void __launch_bounds__(NTHR, SWF_FORCES_MINB) k_forces_list(Geo G, ForcesArgs A) {
+  __shared__ int s_next;
+  StepScalars* sc = A.sc;
+  const int n = *(volatile int*)&sc->list_n[0];
+  while (true) {
+    if (threadIdx.x == 0) s_next = atomicAdd(&sc->list_take[0], 1);
+    __syncthreads();
+    const int q = s_next;
+    __syncthreads();
+    if (q >= n) break;
+    const int t = A.list[q];
+    forces_tile<SWF_SPECULATE != 0>(G, A, t % G.tiles_x, t / G.tiles_x, true);
+    __syncthreads();
+  }
+}
+
 // the tiles with a rejected speculative division, recomputed exactly
 __global__ void __launch_bounds__(NTHR, SWF_FORCES_MINB) k_forces_redo(Geo G, ForcesArgs A) {
   const int n = *(volatile int*)&A.sc->redo_n[0];
@@ -554,6 +603,7 @@ struct StepArgs {
   unsigned char* tile_same;
   const unsigned* tile_srcm;  // per owned tile: source specs meeting the tile +- 2 cells
   int* redo;                  // tiles whose speculative divisions were rejected
+  int* list;                  // work list of k_slist / k_step_list
   double* hH;                 // pinned host arrays of a host-buffer step (write-through), or null
   double* hHUx;
   double* hHUy;
@@ -1119,6 +1169,37 @@ __global__ void __launch_bounds__(STHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
   step_tile<SWF_SPECULATE != 0>(G, A, blockIdx.x);
 }
 
+// k_slist: the tiles k_step must visit -- flux-active ones, and inactive
+// ones whose two ping-pong copies still differ; every other tile keeps its
+// state and gets zero diagnostics partials here.
+__global__ void k_slist(Geo G, StepArgs A) {
+  const int nt = G.tiles_x * G.tiles_y;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nt) return;
+  if ((A.tile_act[t] & 2) || !A.tile_same[t]) {
+    A.list[atomicAdd(&A.sc->list_n[1], 1)] = t;
+  } else {
+    A.part[5 * (size_t)t + 0] = 0.0;
+    A.part[5 * (size_t)t + 1] = 0.0;
+    A.part[5 * (size_t)t + 2] = 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(STHR, SWF_STEP_MINB) k_step_list(Geo G, StepArgs A) {
+  __shared__ int s_next;
+  StepScalars* sc = A.sc;
+  const int n = *(volatile int*)&sc->list_n[1];
+  while (true) {
+    if (threadIdx.x == 0) s_next = atomicAdd(&sc->list_take[1], 1);
+    __syncthreads();
+    const int q = s_next;
+    __syncthreads();
+    if (q >= n) break;
+    step_tile<SWF_SPECULATE != 0>(G, A, A.list[q]);
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(STHR, SWF_STEP_MINB) k_step_redo(Geo G, StepArgs A) {
   const int n = *(volatile int*)&A.sc->redo_n[1];
   for (int q = blockIdx.x; q < n; q += gridDim.x) {
@@ -1195,6 +1276,7 @@ StepArgs step_args(swf_ctx* c) {
   A.tile_same = c->d_tile_same;
   A.tile_srcm = c->d_tile_srcm;
   A.redo = c->d_redo_s;
+  A.list = c->d_list_s;
   A.part = c->d_part;
   A.sc = c->d_sc;
   return A;
@@ -1291,6 +1373,7 @@ int fused_enqueue_phase1(swf_ctx* c, double dt_cap, int part) {
   A.tile_prev = tile_act_at(c, 1 - c->cur);
   A.tile_srcm = c->d_tile_srcm;
   A.redo = c->d_redo_f;
+  A.list = c->d_list_f;
   A.sc = c->d_sc;
   A.cnt_part = c->d_part;
   forces_rows(c, A.ra0, A.ra1);
@@ -1300,7 +1383,14 @@ int fused_enqueue_phase1(swf_ctx* c, double dt_cap, int part) {
   A.do_mask = fm ? 1 : 0;
   if (part < 0) {
     int ntile = G.tiles_x * (tr_hi - A.tr_lo);
-    if (ntile > 0) k_forces<<<ntile, NTHR, 0, c->stream>>>(G, A);
+    const bool use_list = SWF_TILE_LISTS && fm && G.r0 == 0 && G.r1 == G.rows &&
+                          A.tr_lo == 0 && tr_hi == G.tiles_y;
+    if (use_list && ntile > 0) {
+      k_flist<<<(ntile + 255) / 256, 256, 0, c->stream>>>(G, A);
+      k_forces_list<<<c->sm_count * SWF_FORCES_MINB, NTHR, 0, c->stream>>>(G, A);
+    } else if (ntile > 0) {
+      k_forces<<<ntile, NTHR, 0, c->stream>>>(G, A);
+    }
     if (ntile > 0 && SWF_SPECULATE) k_forces_redo<<<RED_CTAS, NTHR, 0, c->stream>>>(G, A);
   } else {
     // interior tile rows [a, b): their 1-row halo stays inside the owned rows
@@ -1346,7 +1436,13 @@ int fused_enqueue_phase2(swf_ctx* c, double dt_cap, double global_speed, const d
                                 c->d_sc, dt_cap, global_speed, gspeed);
   ev(c, 3);
   int nt = G.tiles_x * G.tiles_y;
-  if (nt > 0) k_step<<<nt, STHR, step_smem(), c->stream>>>(G, step_args(c));
+  if (nt > 0 && SWF_TILE_LISTS) {
+    StepArgs SA = step_args(c);
+    k_slist<<<(nt + 255) / 256, 256, 0, c->stream>>>(G, SA);
+    k_step_list<<<c->sm_count * SWF_STEP_MINB, STHR, step_smem(), c->stream>>>(G, SA);
+  } else if (nt > 0) {
+    k_step<<<nt, STHR, step_smem(), c->stream>>>(G, step_args(c));
+  }
   if (nt > 0 && SWF_SPECULATE)
     k_step_redo<<<RED_CTAS, STHR, step_smem(), c->stream>>>(G, step_args(c));
   ev(c, 4);
@@ -1533,10 +1629,25 @@ int fused_prepare(swf_ctx* c) {
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_step_redo, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)step_smem());
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_step_list, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)step_smem());
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_step_list, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_forces_list, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e == cudaSuccess) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    c->sm_count = sms > 0 ? sms : 148;
+  }
   // redo lists: every owned tile, plus the ghost tile rows k_forces covers
   size_t nredo = (size_t)c->geo.tiles_x * (c->geo.tiles_y + 2 * REDO_ROW0);
   if (e == cudaSuccess && !c->d_redo_f) e = cudaMalloc(&c->d_redo_f, nredo * sizeof(int));
   if (e == cudaSuccess && !c->d_redo_s) e = cudaMalloc(&c->d_redo_s, nredo * sizeof(int));
+  if (e == cudaSuccess && !c->d_list_f) e = cudaMalloc(&c->d_list_f, nredo * sizeof(int));
+  if (e == cudaSuccess && !c->d_list_s) e = cudaMalloc(&c->d_list_s, nredo * sizeof(int));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_step, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e == cudaSuccess)

@@ -42,6 +42,8 @@ struct StepScalars {
   double speed_local;               // strips: local max speed (phase 1 out)
   int mask_valid;  // the tile flags of the previous step describe the current state
   int redo_n[2];   // tiles queued for the exact redo: [0] k_forces, [1] k_step
+  int list_n[2];   // work-list lengths: [0] k_forces, [1] k_step
+  int list_take[2];  // work-list cursors of the persistent grids
 };
 
 enum ErrKind : unsigned long long { ERR_DT = 1, ERR_CFL = 2, ERR_FLUX = 3 };
@@ -106,6 +108,9 @@ struct swf_ctx {
   unsigned* d_tile_srcm = nullptr;       // per-tile source-spec masks (fused_tile_srcm)
   int* d_redo_f = nullptr;  // k_forces tiles to redo exactly (speculative division rejected)
   int* d_redo_s = nullptr;  // k_step tiles to redo exactly
+  int* d_list_f = nullptr;  // k_forces work list
+  int* d_list_s = nullptr;  // k_step work list
+  int sm_count = 148;
   double* d_part = nullptr;              // per-tile diagnostic partials (3 per tile)
   // scalars
   swf::StepScalars* d_sc = nullptr;

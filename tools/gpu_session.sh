@@ -18,10 +18,11 @@ fi
 timeout 900 python bench.py > "$O/bench.json" 2> "$O/bench.err"
 echo "bench exit $?" >> "$O/bench.err"
 timeout 300 python tools/kernel_times.py C3 10 > "$O/kernel_times.json" 2>&1
+# launch list of resident steps only (the e2e host-buffer steps are PCIe-bound
+# and would distort the kernel shares)
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
-  --log-file "$O/launches.csv" python bench.py --steps 3 --warmup 3 --e2e-steps 1 \
-  --no-cpu-baseline > "$O/launches_bench.log" 2>&1
+  --log-file "$O/launches.csv" python tools/kernel_times.py C3 4 > "$O/launches_bench.log" 2>&1
 timeout 1200 ncu --set full --clock-control none --import-source on \
-  -k regex:'k_step|k_forces' -s 8 -c 2 -o "$O/prof" \
+  -k regex:'^k_(step|forces)$' -s 8 -c 2 -o "$O/prof" \
   python tools/kernel_times.py C3 2 > "$O/ncu_full.log" 2>&1
 echo "done" > "$O/DONE"

@@ -21,13 +21,25 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.environ.get("SWF_LIB") or os.path.join(ROOT, "paper_1705_00614_b200", "libswflood_cuda.so")
 
 
+def _wrapper_lines(src):
+    """Lines of kernel wrappers that only call a *_tile<SPEC> body: attribution
+    skips them and uses the next frame inward."""
+    path = os.path.join(ROOT, "paper_1705_00614_b200", "csrc", src)
+    try:
+        lines = open(path).read().splitlines()
+    except OSError:
+        return set()
+    return {i for i, l in enumerate(lines, 1) if "_tile<" in l}
+
+
 def sass_lines(kernel, cubin_name="swf_fused.sm_100a.cubin", src="swf_fused.cu"):
-    """offset -> (outermost line in src, opcode) for the kernel."""
+    """offset -> (outermost non-wrapper line in src, opcode) for the kernel."""
     d = tempfile.mkdtemp()
     subprocess.run(["cuobjdump", "-xelf", "all", LIB], cwd=d, check=True, capture_output=True)
     txt = subprocess.run(["nvdisasm", "-gi", "-c", os.path.join(d, cubin_name)],
                          capture_output=True, text=True).stdout
-    out, cur, on = {}, None, False
+    skip = _wrapper_lines(src)
+    out, cur, on, chain, fresh = {}, None, False, [], True
     for ln in txt.splitlines():
         if ln.startswith(".text.") or ln.startswith("_Z"):
             on = (kernel in ln) and ln.rstrip().endswith(":") and not ln.startswith(".text.")
@@ -36,10 +48,15 @@ def sass_lines(kernel, cubin_name="swf_fused.sm_100a.cubin", src="swf_fused.cu")
             continue
         m = re.search(r'//## File ".*?/([^/"]+)", line (\d+)(.*)', ln)
         if m:
-            tail = m.group(3)
-            if m.group(1) == src and "inlined at" not in tail:
-                cur = int(m.group(2))
+            if fresh:
+                chain, fresh = [], False
+            if m.group(1) == src:
+                chain.append(int(m.group(2)))  # innermost first, outermost last
+            frames = [l for l in chain if l not in skip]
+            if frames:
+                cur = frames[-1]
             continue
+        fresh = True
         m = re.match(r"\s*/\*([0-9a-f]{4,})\*/\s+(.*?);", ln)
         if m:
             ins = re.sub(r"^@!?U?P\w+\s+", "", m.group(2).strip())
