@@ -318,7 +318,7 @@ def b200_single(args):
                        "writes overlapped with the arithmetic; restored on a numerical abort), "
                        "t read back; d2h counts the flux-active tiles (an upper bound); "
                        "host-timed, synchronised"},
-        "gpu_launches": 7 * K,
+        "gpu_launches": 10 * K,  # begin, flist, forces, forces_redo, tau, slist, step, step_redo, reduce, finish
         "clocks": clk,
         "cpu_baseline": cpu,
     }
@@ -389,10 +389,13 @@ def b200_nested(args):
 
 
 def b200_multi(args):
+    import torch.distributed as dist
     from paper_1705_00614_b200 import multigpu
     line = multigpu.bench_strips(args)
     if line is not None:
         print(json.dumps(line), flush=True)
+    if dist.is_initialized():
+        dist.destroy_process_group()
 
 
 def main():

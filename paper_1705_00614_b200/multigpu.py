@@ -298,6 +298,9 @@ class RankStrip:
         torch.cuda.set_device(self.local)
         self.dev = torch.device("cuda", self.local)
         self.backend = os.environ.get("SWF_DIST_BACKEND", "nccl")
+        # rank 0 prints exactly one JSON line: keep NCCL's version banner off stdout
+        if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+            os.environ["NCCL_DEBUG"] = "WARN"
         if not dist.is_initialized():
             if self.backend == "nccl":
                 dist.init_process_group("nccl", device_id=self.dev)
@@ -477,6 +480,32 @@ def bench_strips(args) -> Optional[dict]:
     tmax = agg[1:2].clone()
     dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     value = N_total * K / (ms_max * 1e-3) / 1e6
+
+    # ---- end to end: every rank steps its strip from pinned host buffers ----
+    E = max(1, getattr(args, "e2e_steps", 1))
+    pin = lambda a: torch.from_numpy(np.array(a, copy=True)).pin_memory().numpy()
+    hH, hX, hY = pin(sc.state.H), pin(sc.state.HUx), pin(sc.state.HUy)
+    t_now = strip.download(hH, hX, hY)
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(E):
+        strip.upload(hH, hX, hY, t_now)  # H2D: the strip window (owned + ghost rows)
+        if use_async:
+            rs.begin_async()
+            rs.step_async(0.0)
+            rs.end_async()
+        else:
+            rs.step(0.0)
+        t_now = strip.download(hH, hX, hY)  # D2H: the owned rows
+    el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=rs.xdev)
+    dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    io = torch.tensor([24.0 * hH.size + 8, 24.0 * n_own + 8], dtype=torch.float64, device=rs.xdev)
+    dist.all_reduce(io, op=dist.ReduceOp.SUM)
+    e2e = {"value": round(N_total * E / float(el.item()) / 1e6, 3), "unit": "Mcells/s",
+           "h2d_bytes_per_step": int(io[0].item()), "d2h_bytes_per_step": int(io[1].item()),
+           "how": "every rank, every step: its strip window (owned + ghost rows) uploaded from "
+                  "pinned host memory, one exchanged step, the owned rows downloaded; "
+                  "host-timed, max over ranks"}
     if rank != 0:
         dist.barrier()
         return None
@@ -499,8 +528,8 @@ def bench_strips(args) -> Optional[dict]:
                      "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
                      "traffic": traffic["bytes_per_launch"] if traffic else None,
                      "kernel": "k_step (fused K4..K8), per GPU", "peak_source": src},
-        "e2e": None,
-        "gpu_launches": 7 * K,
+        "e2e": e2e,
+        "gpu_launches": 12 * K,  # + split forces launches and the device speed for the allreduce
         "clocks": clk,
         "cpu_baseline": None,
     }
