@@ -170,8 +170,16 @@ def cpu_reference(config, seconds, threads=None):
         o.close()
     v = cell_updates / el_total / 1e6
     what = (f"8 diagonal 1024x1024 crops of {config}" if n_full else f"{config} full grid")
+    cpu = "unknown CPU"
+    try:
+        with open("/proc/cpuinfo") as f:
+            cpu = next(l.split(":", 1)[1].strip() for l in f if l.startswith("model name"))
+    except Exception:
+        pass
+    built = ("the reference sources compiled by oracle/Makefile: g++ -O3 -ffp-contract=off "
+             "-fopenmp, no -march" if kind == "reference" else "the C restatement (gcc -O2)")
     sample = (f"{what} (same generator), {steps_total} crop-steps after 1 warm-up each, "
-              f"{el_total:.1f} s, {cores} thread(s)")
+              f"{el_total:.1f} s, {cores} thread(s) of {os.cpu_count()} on {cpu}; {built}")
     return v, cores, ("reference" if kind == "reference" else "port"), sample
 
 

@@ -325,9 +325,6 @@ __device__ __forceinline__ void forces_tile(const Geo& G, const ForcesArgs& A, c
   const int tid = threadIdx.x;
   const int i0 = tx * BX, rr0 = G.r0 + tr * BY;
   const size_t nx = G.nx;
-#ifdef SWF_EXP_EXIT_ALL
-  if (true) return;
-#endif
   // mask rows (owned rows only)
   const bool mask_tile = A.do_mask && tr >= 0 && tr < G.tiles_y;
   const bool own_row = tr >= 0 && tr < G.tiles_y;
@@ -722,9 +719,6 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
   const size_t nx = G.nx;
 
   // ---- inactive tile: keep the step-start state (skip semantics) ----------
-#ifdef SWF_EXP_EXIT_ALL
-  if (true) return;  // developer experiment: pure launch cost of the tile grid
-#endif
   if (!(A.tile_act[tile] & 2)) {
     if (!A.tile_same[tile]) {
       for (int c = tid; c < BX * BY; c += STHR) {
@@ -1282,11 +1276,8 @@ StepArgs step_args(swf_ctx* c) {
   return A;
 }
 
-#ifndef SWF_STEP_SMEM_PAD
-#define SWF_STEP_SMEM_PAD 0  // developer knob: extra bytes to force lower occupancy
-#endif
 constexpr size_t step_smem() {
-  return (size_t)(F_NUM * RREG + SCRATCH) * sizeof(double) + SWF_STEP_SMEM_PAD;
+  return (size_t)(F_NUM * RREG + SCRATCH) * sizeof(double);
 }
 
 void ev(swf_ctx* c, int i) {
