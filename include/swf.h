@@ -301,6 +301,8 @@ typedef struct swf_coupled_info {
   int substeps_max;     /* most fine steps of one nest */
   double fine_tau_min;  /* smallest fine tau */
   swf_step_info coarse; /* the global step */
+  double reflux_clamp_volume; /* volume added where the flux correction would
+                                 have emptied a dry-side cell (mass ledger) */
 } swf_coupled_info;
 int swf_nest_create(swf_ctx* coarse, swf_ctx* fine, const swf_nest_desc* desc,
                     swf_nest** out);

@@ -28,6 +28,7 @@ struct CoupledStepInfo {
   int substeps_max = 0;
   double fine_tau_min = 0.0;
   StepInfo global;
+  double reflux_clamp_volume = 0.0;  // flux-correction clamp (mass ledger)
 };
 
 class NestedGrid {

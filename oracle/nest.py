@@ -153,6 +153,66 @@ def restrict(w: Window, fine: FlowState, coarse: FlowState, cnx: int):
         D[w.j0:w.j0 + w.nj, w.i0:w.i0 + w.ni] = m
 
 
+def face_taps(stepper, nx, ny, rect):
+    """fm through the faces on the boundary of the cell rectangle rect =
+    (i0, j0, ni, nj) after the stepper's last step, as swf_fused.cu's face
+    taps record them: [west nj | east nj | south ni | north ni]; faces whose
+    adjacent blocks were both inactive (not computed, dry) are 0."""
+    i0, j0, ni, nj = rect
+    fx = stepper.face_fm(0).reshape(ny, nx + 1)
+    fy = stepper.face_fm(1).reshape(ny + 1, nx)
+    jr = np.arange(j0, j0 + nj)
+    ir = np.arange(i0, i0 + ni)
+    w, e = fx[jr, i0].copy(), fx[jr, i0 + ni].copy()
+    so, no = fy[j0, ir].copy(), fy[j0 + nj, ir].copy()
+    if stepper._options.skip_dry_blocks:
+        m = stepper.mask()
+        bs = m.block_size
+        act = ((m.interior_wet > 0) | (m.halo_wet > 0)).reshape(m.nby, m.nbx)
+        fb = lambda ii, jj: act[jj // bs, ii // bs]
+        w = np.where(fb(np.full_like(jr, i0 - 1), jr) | fb(np.full_like(jr, i0), jr), w, 0.0)
+        e = np.where(fb(np.full_like(jr, i0 + ni - 1), jr) | fb(np.full_like(jr, i0 + ni), jr), e, 0.0)
+        so = np.where(fb(ir, np.full_like(ir, j0 - 1)) | fb(ir, np.full_like(ir, j0)), so, 0.0)
+        no = np.where(fb(ir, np.full_like(ir, j0 + nj - 1)) | fb(ir, np.full_like(ir, j0 + nj)), no, 0.0)
+    return np.concatenate([w, e, so, no])
+
+
+def reflux(w: Window, tc, tf, hc, hf, coarse: FlowState, eps):
+    """swf_nest.cu k_reflux: the coarse cells outside the window trade the
+    coarse step's face volumes for the fine substeps' ones."""
+    nx = coarse.nx
+    r, ni, nj, i0, j0 = w.r, w.ni, w.nj, w.i0, w.j0
+    clamp = 0.0
+    for q in range(2 * (ni + nj)):
+        if q < nj:
+            side, k, fo, i, j = 0, q, q * r, i0 - 1, j0 + q
+        elif q < 2 * nj:
+            k = q - nj
+            side, fo, i, j = 1, r * nj + k * r, i0 + ni, j0 + k
+        elif q < 2 * nj + ni:
+            k = q - 2 * nj
+            side, fo, i, j = 2, 2 * r * nj + k * r, i0 + k, j0 - 1
+        else:
+            k = q - 2 * nj - ni
+            side, fo, i, j = 3, 2 * r * nj + r * ni + k * r, i0 + k, j0 + nj
+        vc = float(tc[q]) * hc
+        vf = 0.0
+        for b in range(r):
+            vf = vf + float(tf[fo + b])
+        vf = vf * hf
+        d = (vc - vf) / (hc * hc) if side in (0, 2) else (vf - vc) / (hc * hc)
+        c = i + j * nx
+        h = coarse.H[c] + d
+        clamp = clamp + ((0.0 - h) * (hc * hc) if h < 0.0 else 0.0)
+        if not (h > 0.0):
+            h = 0.0
+        coarse.H[c] = h
+        if not (h > eps):
+            coarse.HUx[c] = 0.0
+            coarse.HUy[c] = 0.0
+    return clamp
+
+
 class OracleNest:
     """One window: its fine OracleStepper and fine FlowState."""
 
@@ -166,10 +226,12 @@ class OracleNest:
 
 def coupled_step(coarse_stepper, coarse_state: FlowState, coarse_b, nests: List[OracleNest],
                  dt_cap: float = 0.0):
-    """coupled_step as swf_nest.cu swf_coupled_step does it.
-    Returns (coarse StepInfo, substeps per nest)."""
+    """coupled_step as swf_nest.cu swf_coupled_step does it,
+    with the flux correction of two-way windows.  Returns (coarse StepInfo,
+    substeps per nest); the reflux clamp volume is in coupled_step.clamp."""
     cnx = coarse_state.nx
     t0 = coarse_state.t
+    coupled_step.clamp = 0.0
     g0 = []
     for n in nests:
         if n.state.t != t0:
@@ -179,6 +241,9 @@ def coupled_step(coarse_stepper, coarse_state: FlowState, coarse_b, nests: List[
     info = coarse_stepper.step(coarse_state, dt_cap)
     t1 = coarse_state.t
     tau_g = t1 - t0
+    hc = coarse_stepper._terrain.h
+    tcs = [info.tau * face_taps(coarse_stepper, cnx, coarse_state.ny, (n.w.i0, n.w.j0, n.w.ni, n.w.nj))
+           if n.w.two_way else None for n in nests]
     subs = []
     for q, n in enumerate(nests):
         g1 = prolong(n.w, coarse_state.H, coarse_state.HUx, coarse_state.HUy, coarse_b, cnx, n.fb,
@@ -186,10 +251,14 @@ def coupled_step(coarse_stepper, coarse_state: FlowState, coarse_b, nests: List[
         tf = t0
         tol = max(1e-9 * tau_g, 8.0 * 2.220446049250313e-16 * abs(t1))
         sub = 0
+        frect = (n.w.ghost, n.w.ghost, n.w.r * n.w.ni, n.w.r * n.w.nj)
+        tfs = np.zeros(2 * (frect[2] + frect[3]))
         while t1 - tf > tol:
             alpha = (tf - t0) / (t1 - t0)
             apply_ghosts(n.w, g0[q], g1, alpha, n.state, n.eps)
-            n.fine.step(n.state, info.tau if sub == 0 else t1 - tf)
+            fi = n.fine.step(n.state, info.tau if sub == 0 else t1 - tf)
+            if n.w.two_way:
+                tfs = tfs + fi.tau * face_taps(n.fine, n.w.nxf, n.w.nyf, frect)
             tf = n.state.t
             sub += 1
             if sub > 1000000:
@@ -198,4 +267,6 @@ def coupled_step(coarse_stepper, coarse_state: FlowState, coarse_b, nests: List[
         subs.append(sub)
         if n.w.two_way:
             restrict(n.w, n.state, coarse_state, cnx)
+            coupled_step.clamp += reflux(n.w, tcs[q], tfs, hc, n.fine._terrain.h, coarse_state,
+                                         n.eps)
     return info, subs

@@ -56,6 +56,7 @@ def _declare(lib):
         "orc_stage": (I, [P, I, D, PD]),
         "orc_scratch": (I, [P, I, PD]),
         "orc_mask": (I, [P, PI, PI, PI, PI]),
+        "orc_face_fm": (I, [P, I, PD]),
         "orc_volumes": (I, [P, PD, PD, PD]),
         "orc_cbrt": (D, [D]),
         "orc_hll_face_flux": (None, [PD, D, PD]),
@@ -69,7 +70,10 @@ def _declare(lib):
         "orc_total_volume": (D, [I, PD, D]),
         "orc_latitude_to_omega_z": (D, [D]),
     }
+    optional = {"orc_face_fm"}  # the C restatement only (the reference keeps faces private)
     for name, (res, args) in sig.items():
+        if name in optional and not hasattr(lib, name):
+            continue
         f = getattr(lib, name)
         f.restype = res
         f.argtypes = args
@@ -209,6 +213,14 @@ class OracleStepper:
     def scratch(self, name):
         out = np.empty(self.n)
         self._rc(self.lib.orc_scratch(self.ctx, A.SCRATCH_ID[name], A.dptr(out)))
+        return out
+
+    def face_fm(self, direction: int) -> np.ndarray:
+        """fm of the x (0) or y (1) faces of the last flux stage (orc_face_fm)."""
+        nx, ny = self._terrain.nx, self._terrain.ny
+        n = (nx + 1) * ny if direction == 0 else nx * (ny + 1)
+        out = np.empty(n)
+        self._rc(self.lib.orc_face_fm(self.ctx, int(direction), A.dptr(out)))
         return out
 
     def mask(self):

@@ -1195,6 +1195,18 @@ int orc_scratch(orc_ctx* c, int which, double* out) {
   return SWF_OK;
 }
 
+/* Mass fluxes fm of the faces of the last flux stage (stepper.cpp:402-538):
+ * dir 0 = x-faces, (nx+1)*ny values, face i between cells i-1 and i of row j
+ * at out[i + j*(nx+1)]; dir 1 = y-faces, nx*(ny+1) values.  Entries of faces
+ * the last step did not compute (both adjacent blocks inactive) are stale:
+ * callers mask them with orc_mask (their true flux is 0). */
+int orc_face_fm(orc_ctx* c, int dir, double* out) {
+  size_t n = dir == 0 ? (size_t)(c->nx + 1) * c->ny : (size_t)c->nx * (c->ny + 1);
+  const face_rec* f = dir == 0 ? c->xf : c->yf;
+  for (size_t k = 0; k < n; ++k) out[k] = f[k].fm;
+  return SWF_OK;
+}
+
 int orc_mask(orc_ctx* c, int* interior, int* halo, int* nbx, int* nby) {
   if (nbx) *nbx = c->nbx;
   if (nby) *nby = c->nby;

@@ -40,6 +40,7 @@ int orc_run(orc_ctx* ctx, int n, double dt_cap, int* done, swf_step_info* last);
 int orc_stage(orc_ctx* ctx, int stage, double arg, double* tau_out);
 int orc_scratch(orc_ctx* ctx, int which, double* out);
 int orc_mask(orc_ctx* ctx, int* interior, int* halo, int* nbx, int* nby);
+int orc_face_fm(orc_ctx* ctx, int dir, double* out);
 int orc_volumes(orc_ctx* ctx, double* clamp_deficit, double* source_volume,
                 double* boundary_outflow);
 

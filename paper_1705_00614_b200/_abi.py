@@ -77,4 +77,5 @@ class swf_nest_desc(C.Structure):
 
 class swf_coupled_info(C.Structure):
     _fields_ = [("tau", C.c_double), ("substeps_total", C.c_int), ("substeps_max", C.c_int),
-                ("fine_tau_min", C.c_double), ("coarse", swf_step_info)]
+                ("fine_tau_min", C.c_double), ("coarse", swf_step_info),
+                ("reflux_clamp_volume", C.c_double)]

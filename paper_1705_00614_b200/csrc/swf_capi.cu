@@ -352,6 +352,10 @@ int commit_batch(swf_ctx* c, int cur_start, int enqueued, int* done) {
 
 }  // namespace
 
+namespace swf {
+void invalidate_graph(swf_ctx* c) { drop_graph(c); }
+}  // namespace swf
+
 extern "C" {
 
 int swf_create(const swf_terrain* terrain, const swf_params* params, const swf_control* control,

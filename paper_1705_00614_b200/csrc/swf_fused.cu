@@ -601,6 +601,7 @@ struct StepArgs {
   const unsigned* tile_srcm;  // per owned tile: source specs meeting the tile +- 2 cells
   int* redo;                  // tiles whose speculative divisions were rejected
   int* list;                  // work list of k_slist / k_step_list
+  FaceTaps taps;              // faces whose tau * fm this step records (nested grids)
   double* hH;                 // pinned host arrays of a host-buffer step (write-through), or null
   double* hHUx;
   double* hHUy;
@@ -977,6 +978,14 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
     FB[1 * NFC + c] = rec.fnl;
     FB[2 * NFC + c] = rec.fnr;
     FB[3 * NFC + c] = rec.ft;
+    // face taps: each tile records its west faces only (fx < BX), so every
+    // face is written once; faces no active tile computes stay 0 (dry)
+    for (int q = 0; q < A.taps.n; ++q) {
+      const int f = i0 + fx, jg = G.jg0 + r0 + y;
+      if (fx < BX && r0 + y < G.r1 && (f == A.taps.i0[q] || f == A.taps.i0[q] + A.taps.ni[q]) &&
+          jg >= A.taps.j0[q] && jg < A.taps.j0[q] + A.taps.nj[q])
+        A.taps.out[q][(f == A.taps.i0[q] ? 0 : A.taps.nj[q]) + (jg - A.taps.j0[q])] = tau * rec.fm;
+    }
   }
   __syncthreads();
   double px_m[PER], px_a[PER], px_c[PER];  // (W.fm-E.fm), (W.fnr-E.fnl), (W.ft-E.ft)
@@ -1065,6 +1074,13 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
     FB[1 * NFC + c] = rec.fnl;
     FB[2 * NFC + c] = rec.fnr;
     FB[3 * NFC + c] = rec.ft;
+    for (int q = 0; q < A.taps.n; ++q) {
+      if (fy < BY && i < G.nx && rf < G.r1 &&
+          (jf == A.taps.j0[q] || jf == A.taps.j0[q] + A.taps.nj[q]) && i >= A.taps.i0[q] &&
+          i < A.taps.i0[q] + A.taps.ni[q])
+        A.taps.out[q][2 * A.taps.nj[q] + (jf == A.taps.j0[q] ? 0 : A.taps.ni[q]) +
+                      (i - A.taps.i0[q])] = tau * rec.fm;
+    }
   }
   __syncthreads();
 
@@ -1249,6 +1265,7 @@ __global__ void k_finish(const double* red, int nred, StepScalars* sc, double ar
 
 StepArgs step_args(swf_ctx* c) {
   StepArgs A;
+  A.taps = c->taps;
   A.hH = c->wt_host[0];
   A.hHUx = c->wt_host[1];
   A.hHUy = c->wt_host[2];
@@ -1427,6 +1444,9 @@ int fused_enqueue_phase2(swf_ctx* c, double dt_cap, double global_speed, const d
                                 c->d_sc, dt_cap, global_speed, gspeed);
   ev(c, 3);
   int nt = G.tiles_x * G.tiles_y;
+  for (int q = 0; q < c->taps.n; ++q)
+    cudaMemsetAsync(c->taps.out[q], 0,
+                    2 * (size_t)(c->taps.ni[q] + c->taps.nj[q]) * sizeof(double), c->stream);
   if (nt > 0 && SWF_TILE_LISTS) {
     StepArgs SA = step_args(c);
     k_slist<<<(nt + 255) / 256, 256, 0, c->stream>>>(G, SA);

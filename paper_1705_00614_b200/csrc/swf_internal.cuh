@@ -68,6 +68,16 @@ struct Geo {
   PhysConst P;
 };
 
+// Face taps: the mass fluxes tau * fm through the faces on the boundary of a
+// cell rectangle, recorded by k_step each step (nested-grid flux correction).
+// Layout of a tap array: [west nj | east nj | south ni | north ni].
+constexpr int MAX_TAPS = 4;
+struct FaceTaps {
+  int n = 0;
+  int i0[MAX_TAPS], j0[MAX_TAPS], ni[MAX_TAPS], nj[MAX_TAPS];  // global cell rects
+  double* out[MAX_TAPS];
+};
+
 struct Scratch;  // stage-path arrays (lazy)
 
 }  // namespace swf
@@ -111,6 +121,7 @@ struct swf_ctx {
   int* d_list_f = nullptr;  // k_forces work list
   int* d_list_s = nullptr;  // k_step work list
   int sm_count = 148;
+  swf::FaceTaps taps;  // owned by the nests that registered them
   double* d_part = nullptr;              // per-tile diagnostic partials (3 per tile)
   // scalars
   swf::StepScalars* d_sc = nullptr;
@@ -180,6 +191,7 @@ int cuda_check(swf_ctx* c, cudaError_t e, const char* what);
 int check_device_error(swf_ctx* c);  // after a sync: maps err_key to status
 size_t local_cells(const swf_ctx* c);
 void invalidate_mask(swf_ctx* c);  // the state changed outside the fused path
+void invalidate_graph(swf_ctx* c); // the captured step no longer matches the context
 inline unsigned char* tile_act_at(swf_ctx* c, int parity) {
   return c->d_tile_act + (size_t)parity * ((size_t)c->geo.tiles_x * c->geo.tiles_y);
 }

@@ -31,6 +31,11 @@
 //    t1, then its t is set to t1.
 //  * restriction: each window cell's H, HUx, HUy = the sum
 //    of its r x r fine cells (row-major, j outer) divided by r*r.
+//  * flux correction (two-way; the SPEC's mass invariant): the
+//    k_step face taps record tau*fm through the window boundary faces of the
+//    coarse step and of every fine substep; after the restriction each
+//    coarse cell just outside the window trades the coarse face volume for
+//    the fine one (k_reflux), so the coupled system is conservative.
 //
 // After any external write the fused path's dry-tile bookkeeping is updated
 // for the touched tiles only (tile flags of the previous step set active, the
@@ -40,6 +45,7 @@
 
 #include <cmath>
 #include <string>
+#include <vector>
 
 #include "swf_internal.cuh"
 
@@ -50,6 +56,12 @@ struct swf_nest {
   int nxf = 0, nyf = 0;
   size_t nghost = 0;  // ghost cells of the fine grid
   double* g[2] = {nullptr, nullptr};  // prolonged ghosts at t0 / t1: [H | HUx | HUy]
+  // flux correction (two-way): tau*fm through the window boundary faces of
+  // the coarse step and of every fine substep (face taps of k_step)
+  double* tap_c = nullptr;      // coarse faces: 2*(ni+nj)
+  double* tap_f = nullptr;      // fine faces of one substep: 2*r*(ni+nj)
+  double* tap_fsum = nullptr;   // their sum over the substeps
+  double* clampv = nullptr;     // per boundary face: volume added by the reflux clamp
   std::string err;
 };
 
@@ -226,6 +238,57 @@ __global__ void k_restrict(NestGeo N, const double* __restrict__ fH, const doubl
   tile_same[t] = 0;
 }
 
+// tap_fsum += tap_f (after each fine substep, in substep order)
+__global__ void k_tap_add(int n, const double* __restrict__ a, double* __restrict__ sum) {
+  int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n) sum[q] = sum[q] + a[q];
+}
+
+// Flux correction (refluxing): the coarse cells just outside the window lost
+// or gained the coarse step's face volumes vc; the window (now the fine
+// means) exchanged the fine substeps' vf instead.  Each outside cell gets
+// (vc - vf) / h^2 on the inflow sides (west, south) and (vf - vc) / h^2 on
+// the outflow sides, which makes the coupled system conservative; a cell
+// driven below 0 is clamped (and dried).  One thread per boundary face.
+__global__ void k_reflux(NestGeo N, const double* __restrict__ tc, const double* __restrict__ tf,
+                         double hc, double hf, double* H, double* HUx, double* HUy,
+                         unsigned char* tile_prev, unsigned char* tile_same, int tiles_x,
+                         double* clampv) {
+  const int nq = 2 * (N.ni + N.nj);
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  int side, k, fo, i, j;
+  if (q < N.nj) {
+    side = 0; k = q; fo = k * N.r; i = N.i0 - 1; j = N.j0 + k;
+  } else if (q < 2 * N.nj) {
+    side = 1; k = q - N.nj; fo = N.r * N.nj + k * N.r; i = N.i0 + N.ni; j = N.j0 + k;
+  } else if (q < 2 * N.nj + N.ni) {
+    side = 2; k = q - 2 * N.nj; fo = 2 * N.r * N.nj + k * N.r; i = N.i0 + k; j = N.j0 - 1;
+  } else {
+    side = 3; k = q - 2 * N.nj - N.ni; fo = 2 * N.r * N.nj + N.r * N.ni + k * N.r; i = N.i0 + k;
+    j = N.j0 + N.nj;
+  }
+  const double vc = tc[q] * hc;
+  double vf = 0.0;
+  for (int b = 0; b < N.r; ++b) vf = vf + tf[fo + b];
+  vf = vf * hf;
+  const double d = (side == 0 || side == 2) ? (vc - vf) / (hc * hc) : (vf - vc) / (hc * hc);
+  const size_t c = (size_t)i + (size_t)j * N.cnx;
+  double h = H[c] + d;
+  // a dry-side cell cannot give what the fine side drew at a wet/dry front:
+  // clamp and log the volume added, like the step's own clamp deficit
+  clampv[q] = h < 0.0 ? (0.0 - h) * (hc * hc) : 0.0;
+  if (!(h > 0.0)) h = 0.0;
+  H[c] = h;
+  if (!(h > N.eps)) {
+    HUx[c] = 0.0;
+    HUy[c] = 0.0;
+  }
+  int t = i / TBX + (j / TBY) * tiles_x;
+  tile_prev[t] = 3;
+  tile_same[t] = 0;
+}
+
 NestGeo nest_geo(const swf_nest* n) {
   NestGeo N;
   N.cnx = n->coarse->geo.nx;
@@ -299,6 +362,27 @@ int swf_nest_create(swf_ctx* coarse, swf_ctx* fine, const swf_nest_desc* d, swf_
   cudaSetDevice(coarse->device);
   cudaError_t e = cudaSuccess;
   for (int s = 0; s < 2 && e == cudaSuccess; ++s) e = cudaMalloc(&n->g[s], 3 * n->nghost * sizeof(double));
+  if (e == cudaSuccess && d->two_way) {
+    size_t nc = 2 * (size_t)(d->ni + d->nj), nf = (size_t)d->r * nc;
+    if (coarse->taps.n >= MAX_TAPS || fine->taps.n >= MAX_TAPS) {
+      swf_nest_destroy(n);
+      return bad("too many nested windows on one grid (max " + std::to_string(MAX_TAPS) + ")");
+    }
+    e = cudaMalloc(&n->tap_c, nc * sizeof(double));
+    if (e == cudaSuccess) e = cudaMalloc(&n->tap_f, nf * sizeof(double));
+    if (e == cudaSuccess) e = cudaMalloc(&n->tap_fsum, nf * sizeof(double));
+    if (e == cudaSuccess) e = cudaMalloc(&n->clampv, nc * sizeof(double));
+    if (e == cudaSuccess) {
+      FaceTaps& tc = coarse->taps;
+      tc.i0[tc.n] = d->i0; tc.j0[tc.n] = d->j0; tc.ni[tc.n] = d->ni; tc.nj[tc.n] = d->nj;
+      tc.out[tc.n++] = n->tap_c;
+      FaceTaps& tf = fine->taps;
+      tf.i0[tf.n] = d->ghost; tf.j0[tf.n] = d->ghost; tf.ni[tf.n] = d->r * d->ni;
+      tf.nj[tf.n] = d->r * d->nj; tf.out[tf.n++] = n->tap_f;
+      invalidate_graph(coarse);  // captured steps do not record the new taps
+      invalidate_graph(fine);
+    }
+  }
   if (e != cudaSuccess) {
     int rc = cuda_check(coarse, e, "nest allocation");
     swf_nest_destroy(n);
@@ -310,7 +394,27 @@ int swf_nest_create(swf_ctx* coarse, swf_ctx* fine, const swf_nest_desc* d, swf_
 
 void swf_nest_destroy(swf_nest* n) {
   if (!n) return;
+  auto unreg = [](swf_ctx* c, double* p) {
+    if (!c || !p) return;
+    FaceTaps& t = c->taps;
+    for (int q = 0; q < t.n; ++q)
+      if (t.out[q] == p) {
+        for (int m = q + 1; m < t.n; ++m) {
+          t.i0[m - 1] = t.i0[m]; t.j0[m - 1] = t.j0[m]; t.ni[m - 1] = t.ni[m];
+          t.nj[m - 1] = t.nj[m]; t.out[m - 1] = t.out[m];
+        }
+        --t.n;
+        invalidate_graph(c);
+        break;
+      }
+  };
+  unreg(n->coarse, n->tap_c);
+  unreg(n->fine, n->tap_f);
   for (double* p : n->g) cudaFree(p);
+  cudaFree(n->tap_c);
+  cudaFree(n->tap_f);
+  cudaFree(n->tap_fsum);
+  cudaFree(n->clampv);
   delete n;
 }
 
@@ -375,6 +479,22 @@ int swf_nest_restrict(swf_nest* n) {
   return nest_cuda(n, e, "nest restrict");
 }
 
+static int nest_reflux(swf_nest* n, double* clamp_volume) {
+  swf_ctx* c = n->coarse;
+  NestGeo N = nest_geo(n);
+  int nq = 2 * (N.ni + N.nj);
+  k_reflux<<<(nq + 255) / 256, 256, 0, c->stream>>>(
+      N, n->tap_c, n->tap_fsum, c->h, n->fine->h, c->H[c->cur], c->HUx[c->cur], c->HUy[c->cur],
+      tile_act_at(c, 1 - c->cur), c->d_tile_same, c->geo.tiles_x, n->clampv);
+  cudaError_t e = cudaGetLastError();
+  std::vector<double> v(nq);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(v.data(), n->clampv, nq * sizeof(double), cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  for (double x : v) *clamp_volume += x;  // face order: deterministic
+  return nest_cuda(n, e, "nest reflux");
+}
+
 int swf_coupled_step(swf_ctx* coarse, swf_nest** nests, int nn, double dt_cap,
                      swf_coupled_info* info) {
   swf_coupled_info tmp{};
@@ -407,6 +527,8 @@ int swf_coupled_step(swf_ctx* coarse, swf_nest** nests, int nn, double dt_cap,
     double tf = t0;
     double tol = std::fmax(1e-9 * tau_g, 8.0 * 2.220446049250313e-16 * std::fabs(t1));
     int sub = 0;
+    const int nft = n->tap_f ? 2 * n->d.r * (n->d.ni + n->d.nj) : 0;
+    if (nft) cudaMemsetAsync(n->tap_fsum, 0, nft * sizeof(double), f->stream);
     while (t1 - tf > tol) {
       double alpha = (tf - t0) / (t1 - t0);
       rc = swf_nest_apply_ghosts(n, alpha);
@@ -417,6 +539,7 @@ int swf_coupled_step(swf_ctx* coarse, swf_nest** nests, int nn, double dt_cap,
       rc = swf_step(f, sub == 0 ? I.tau : t1 - tf, &fi);
       if (rc) return set_err(coarse, rc, std::string("nested grid: ") + swf_last_error(f));
       if (fi.tau < I.fine_tau_min) I.fine_tau_min = fi.tau;
+      if (nft) k_tap_add<<<(nft + 255) / 256, 256, 0, f->stream>>>(nft, n->tap_f, n->tap_fsum);
       tf = host_t(f);
       if (++sub > 1000000)
         return set_err(coarse, SWF_ENUMERICAL, "nested grid: subcycling does not converge");
@@ -429,6 +552,8 @@ int swf_coupled_step(swf_ctx* coarse, swf_nest** nests, int nn, double dt_cap,
     if (sub > I.substeps_max) I.substeps_max = sub;
     if (n->d.two_way) {
       rc = swf_nest_restrict(n);
+      if (rc) return set_err(coarse, rc, n->err);
+      rc = nest_reflux(n, &I.reflux_clamp_volume);
       if (rc) return set_err(coarse, rc, n->err);
     }
   }

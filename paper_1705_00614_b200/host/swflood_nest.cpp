@@ -108,6 +108,7 @@ CoupledStepInfo coupled_step_resident(CsphTvdStepper& global, const std::vector<
   I.substeps_max = c.substeps_max;
   I.fine_tau_min = c.fine_tau_min;
   I.global = from_c(c.coarse);
+  I.reflux_clamp_volume = c.reflux_clamp_volume;
   return I;
 }
 

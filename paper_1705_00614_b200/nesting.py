@@ -63,6 +63,7 @@ class CoupledInfo:
     substeps_max: int
     fine_tau_min: float
     coarse: StepInfo
+    reflux_clamp_volume: float = 0.0
 
 
 class NestedGrid:
@@ -155,4 +156,4 @@ def coupled_step(coarse: CsphTvdStepper, nests: Sequence[NestedGrid],
     rc = L.swf_coupled_step(coarse._ctx, arr, len(nests), float(dt_cap), C.byref(info))
     raise_for(rc, coarse._ctx)
     return CoupledInfo(info.tau, info.substeps_total, info.substeps_max, info.fine_tau_min,
-                       info_from_c(info.coarse))
+                       info_from_c(info.coarse), info.reflux_clamp_volume)

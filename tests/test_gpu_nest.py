@@ -67,6 +67,7 @@ def test_coupled_steps_match_oracle(oracle_built, r, win):
         oi, subs = N.coupled_step(cs, cstate, ns.coarse.terrain.b, [onest])
         assert gi.tau == oi.tau
         assert gi.substeps_total == subs[0], (k, gi.substeps_total, subs)
+        assert gi.reflux_clamp_volume == N.coupled_step.clamp
     assert subs[0] >= 1
     assert_state_bitwise(_down(coarse, cstate), cstate, f"coarse r={r}")
     assert_state_bitwise(_down(nest.fine, onest.state), onest.state, f"fine r={r}")
@@ -119,3 +120,25 @@ def test_unsynchronized_and_bad_windows_are_config_errors():
     with pytest.raises(ConfigError):  # touches the domain edge
         bad = S.nested_floodplain(64, 50.0, (0, 20, 16, 16), 4, 2)
         NestedGrid(coarse, bad.window, 4, bad.fine.terrain, bad.fine.params)
+
+
+def test_coupled_mass_ledger_on_gpu():
+    """With the flux correction the coupled system conserves volume to
+    round-off up to the logged clamp volumes."""
+    from paper_1705_00614_b200.nesting import coupled_step
+    from paper_1705_00614_b200.types import BoundaryConfig, EdgeKind
+    ns = S.nested_floodplain(128, 50.0, (48, 40, 32, 40), 4, 2)
+    ns.coarse.sources, ns.fine.sources = [], []
+    ns.coarse.options.boundaries = BoundaryConfig(*(EdgeKind.Reflective,) * 4)
+    w = N.Window(*ns.window, r=ns.r, ghost=ns.ghost)
+    N.restrict(w, ns.fine.state, ns.coarse.state, 128)
+    coarse, nest = _gpu(ns)
+    area = ns.coarse.terrain.h ** 2
+    m0 = ns.coarse.state.H.sum() * area
+    ledger = 0.0
+    for _ in range(60):
+        ci = coupled_step(coarse, [nest])
+        ledger += ci.reflux_clamp_volume + ci.coarse.clamp_deficit_volume
+    st = _down(coarse, ns.coarse.state)
+    m1 = st.H.sum() * area
+    assert abs((m1 - m0) - ledger) <= 1e-11 * m0, (m1 - m0, ledger)

@@ -180,11 +180,9 @@ def test_r1_degenerate_window_matches_global(oracle_built):
     assert_state_bitwise(ns.coarse.state, plain, "r=1")
 
 
-@pytest.mark.slow
 def test_flood_wave_mass_balance(oracle_built):
-    # SPEC.md:392 total system mass over coupled steps (interpolation is not
-    # telescoping; the SPEC's 1e-8 bound is checked on a closed, source-free
-    # system where the window sits in the path of the wave)
+    # SPEC.md:392 total system mass over coupled steps, on a closed,
+    # source-free system where the window sits in the path of the wave
     ns = S.nested_floodplain(64, 50.0, (24, 24, 16, 16), 2, 2)
     for sc in (ns.coarse, ns.fine):
         sc.sources = []
@@ -192,10 +190,19 @@ def test_flood_wave_mass_balance(oracle_built):
                                                EdgeKind.Reflective, EdgeKind.Reflective)
     ns.fine.options.boundaries = BoundaryConfig(EdgeKind.Open, EdgeKind.Open, EdgeKind.Open,
                                                 EdgeKind.Open)
+    w = N.Window(*ns.window, r=ns.r, ghost=ns.ghost)
+    N.restrict(w, ns.fine.state, ns.coarse.state, 64)  # consistent start
     cs, nest = _pair(oracle_built, ns)
-    m0 = ns.coarse.state.H.sum()
+    area = ns.coarse.terrain.h ** 2
+    m0 = ns.coarse.state.H.sum() * area
+    ledger = 0.0
     for _ in range(100):
-        N.coupled_step(cs, ns.coarse.state, ns.coarse.terrain.b, [nest])
-    m1 = ns.coarse.state.H.sum()
-    rel = abs(m1 - m0) / m0
-    assert rel < 1e-2, rel
+        info, _ = N.coupled_step(cs, ns.coarse.state, ns.coarse.terrain.b, [nest])
+        ledger += N.coupled_step.clamp + info.clamp_deficit_volume
+    m1 = ns.coarse.state.H.sum() * area
+    # with the flux correction the coupled system is
+    # conservative to round-off up to the logged clamp volumes (wet/dry fronts
+    # across the window edge); 1.4e-3 relative drift over these 100 steps
+    # without the correction
+    assert abs((m1 - m0) - ledger) <= 1e-11 * m0, (m1 - m0, ledger)
+    assert abs(ledger) < 1e-3 * m0
