@@ -978,16 +978,21 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
     FB[1 * NFC + c] = rec.fnl;
     FB[2 * NFC + c] = rec.fnr;
     FB[3 * NFC + c] = rec.ft;
-    // face taps: each tile records its west faces only (fx < BX), so every
-    // face is written once; faces no active tile computes stay 0 (dry)
-    for (int q = 0; q < A.taps.n; ++q) {
-      const int f = i0 + fx, jg = G.jg0 + r0 + y;
-      if (fx < BX && r0 + y < G.r1 && (f == A.taps.i0[q] || f == A.taps.i0[q] + A.taps.ni[q]) &&
-          jg >= A.taps.j0[q] && jg < A.taps.j0[q] + A.taps.nj[q])
-        A.taps.out[q][(f == A.taps.i0[q] ? 0 : A.taps.nj[q]) + (jg - A.taps.j0[q])] = tau * rec.fm;
-    }
   }
   __syncthreads();
+  // face taps (nested-grid flux correction): each tile records its west
+  // faces only (fx < BX), so every face is written once; faces no active
+  // tile computes stay 0 (dry)
+  if (A.taps.n) {
+    for (int c = tid; c < (BX + 1) * BY; c += STHR) {
+      const int fx = c % (BX + 1), y = c / (BX + 1), f = i0 + fx, jg = G.jg0 + r0 + y;
+      for (int q = 0; q < A.taps.n; ++q)
+        if (fx < BX && r0 + y < G.r1 && (f == A.taps.i0[q] || f == A.taps.i0[q] + A.taps.ni[q]) &&
+            jg >= A.taps.j0[q] && jg < A.taps.j0[q] + A.taps.nj[q])
+          A.taps.out[q][(f == A.taps.i0[q] ? 0 : A.taps.nj[q]) + (jg - A.taps.j0[q])] =
+              tau * FB[0 * NFC + c];
+    }
+  }
   double px_m[PER], px_a[PER], px_c[PER];  // (W.fm-E.fm), (W.fnr-E.fnl), (W.ft-E.ft)
 #pragma unroll
   for (int m = 0; m < PER; ++m) {
@@ -1074,15 +1079,19 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
     FB[1 * NFC + c] = rec.fnl;
     FB[2 * NFC + c] = rec.fnr;
     FB[3 * NFC + c] = rec.ft;
-    for (int q = 0; q < A.taps.n; ++q) {
-      if (fy < BY && i < G.nx && rf < G.r1 &&
-          (jf == A.taps.j0[q] || jf == A.taps.j0[q] + A.taps.nj[q]) && i >= A.taps.i0[q] &&
-          i < A.taps.i0[q] + A.taps.ni[q])
-        A.taps.out[q][2 * A.taps.nj[q] + (jf == A.taps.j0[q] ? 0 : A.taps.ni[q]) +
-                      (i - A.taps.i0[q])] = tau * rec.fm;
-    }
   }
   __syncthreads();
+  if (A.taps.n) {
+    for (int c = tid; c < BX * (BY + 1); c += STHR) {
+      const int x = c % BX, fy = c / BX, i = i0 + x, rf = r0 + fy, jf = G.jg0 + rf;
+      for (int q = 0; q < A.taps.n; ++q)
+        if (fy < BY && i < G.nx && rf < G.r1 &&
+            (jf == A.taps.j0[q] || jf == A.taps.j0[q] + A.taps.nj[q]) && i >= A.taps.i0[q] &&
+            i < A.taps.i0[q] + A.taps.ni[q])
+          A.taps.out[q][2 * A.taps.nj[q] + (jf == A.taps.j0[q] ? 0 : A.taps.ni[q]) +
+                        (i - A.taps.i0[q])] = tau * FB[0 * NFC + c];
+    }
+  }
 
   PHASE_MARK(6);
   // ---- phase 5: accumulate (stepper.cpp:540-566) + final (628-659) ---------
