@@ -37,3 +37,29 @@ def test_dropin_runs_bit_exact():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "dropin ok" in r.stdout
+
+
+NEST_EXE = os.path.join(ROOT, "tests", "native", "nest_io_test")
+
+
+def build_nest_exe():
+    from paper_1705_00614_b200 import build as b
+    b.build()
+    pkg = os.path.join(ROOT, "paper_1705_00614_b200")
+    cmd = ["/usr/bin/g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"),
+           os.path.join(ROOT, "tests", "native", "nest_io_test.cpp"), "-o", NEST_EXE, "-L", pkg,
+           "-lswflood_b200", "-lswflood_cuda", f"-Wl,-rpath,{pkg}"]
+    subprocess.run(cmd, check=True)
+    return NEST_EXE
+
+
+def test_nest_io_program_compiles():
+    assert os.path.exists(build_nest_exe())
+
+
+@pytest.mark.gpu
+def test_nest_io_program_runs(tmp_path):
+    exe = build_nest_exe()
+    r = subprocess.run([exe, str(tmp_path)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "nest_io ok" in r.stdout
