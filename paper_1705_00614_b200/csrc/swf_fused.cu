@@ -520,6 +520,19 @@ __global__ void __launch_bounds__(NTHR, SWF_FORCES_MINB) k_forces(Geo G, ForcesA
 }
 
 // ---- tile work lists (single-context steps) ---------------------------------
+// Warp-aggregated append: one atomic per warp and the lanes' entries in lane
+// order, so the list keeps the tiles' raster order within each warp (spatial
+// neighbours stay close in time and share their halo rows in L2).
+__device__ __forceinline__ void append_ordered(int* list, int* n, bool take, int t) {
+  const unsigned m = __ballot_sync(0xffffffffu, take);
+  if (!m) return;
+  const int lane = threadIdx.x & 31;
+  int base = 0;
+  if (lane == __ffs(m) - 1) base = atomicAdd(n, __popc(m));
+  base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+  if (take) list[base + __popc(m & ((1u << lane) - 1u))] = t;
+}
+
 // k_flist: one thread per tile applies the dry-neighbourhood rule of
 // forces_tile and appends the tiles k_forces must visit to A.list; the
 // skipped ones get their flag cleared exactly as forces_tile would.  A
@@ -528,20 +541,17 @@ __global__ void __launch_bounds__(NTHR, SWF_FORCES_MINB) k_forces(Geo G, ForcesA
 __global__ void k_flist(Geo G, ForcesArgs A) {
   const int nt = G.tiles_x * G.tiles_y;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nt) return;
+  const bool valid = t < nt;  // every lane reaches the warp-wide append
   StepScalars* sc = A.sc;
   const int tx = t % G.tiles_x, tr = t / G.tiles_x;
-  bool busy = !(A.do_mask && G.skip && sc->mask_valid) || A.tile_srcm[t] != 0;
-  for (int q = 0; q < 9 && !busy; ++q) {
+  bool busy = valid && (!(A.do_mask && G.skip && sc->mask_valid) || A.tile_srcm[t] != 0);
+  for (int q = 0; q < 9 && valid && !busy; ++q) {
     int x2 = tx + q % 3 - 1, y2 = tr + q / 3 - 1;
     if (x2 >= 0 && x2 < G.tiles_x && y2 >= 0 && y2 < G.tiles_y)
       busy = A.tile_prev[x2 + y2 * G.tiles_x] != 0;
   }
-  if (busy) {
-    A.list[atomicAdd(&sc->list_n[0], 1)] = t;
-  } else {
-    A.tile_act[t] = 0;
-  }
+  if (valid && !busy) A.tile_act[t] = 0;
+  append_ordered(A.list, &sc->list_n[0], busy, t);
 }
 
 __global__ void __launch_bounds__(NTHR, SWF_FORCES_MINB) k_forces_list(Geo G, ForcesArgs A) {
@@ -1194,10 +1204,10 @@ __global__ void __launch_bounds__(STHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
 __global__ void k_slist(Geo G, StepArgs A) {
   const int nt = G.tiles_x * G.tiles_y;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nt) return;
-  if ((A.tile_act[t] & 2) || !A.tile_same[t]) {
-    A.list[atomicAdd(&A.sc->list_n[1], 1)] = t;
-  } else {
+  const bool valid = t < nt;  // every lane reaches the warp-wide append
+  const bool need = valid && ((A.tile_act[t] & 2) || !A.tile_same[t]);
+  append_ordered(A.list, &A.sc->list_n[1], need, t);
+  if (valid && !need) {
     A.part[5 * (size_t)t + 0] = 0.0;
     A.part[5 * (size_t)t + 1] = 0.0;
     A.part[5 * (size_t)t + 2] = 0.0;

@@ -39,7 +39,10 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-6, "
 
 
 def short(name):
-    return name.split("(")[0].split("::")[-1]
+    """Base kernel name; the persistent work-list launches report as the
+    kernel they run (k_step_list -> k_step, k_forces_list -> k_forces)."""
+    n = name.split("(")[0].split("::")[-1]
+    return n[:-5] if n in ("k_step_list", "k_forces_list") else n
 
 
 def launch_shares(path):
