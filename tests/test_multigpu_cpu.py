@@ -91,3 +91,18 @@ def test_gloo_halo_exchange_and_allreduce(world):
     for rank, ok, speed in res:
         assert ok, f"rank {rank}: ghost rows differ from the neighbour's owned rows"
         assert speed == (world - 1) * 1.5 + 0.25
+
+
+def test_balanced_bounds_equalise_weight():
+    rng = np.random.default_rng(2)
+    w = rng.uniform(0.1, 1.0, 256)
+    w[40:60] *= 8.0  # a busy band
+    for parts in (2, 3, 5, 8):
+        b = M.balanced_bounds(w, parts, 16, 256 * 16)
+        assert b[0][0] == 0 and b[-1][1] == 256 * 16
+        assert all(j0 % 16 == 0 and j0 < j1 for j0, j1 in b)
+        assert all(b[k][1] == b[k + 1][0] for k in range(parts - 1))
+        loads = [w[j0 // 16:j1 // 16].sum() for j0, j1 in b]
+        assert max(loads) / (sum(loads) / parts) < 1.0 + 2 * w.max() * parts / w.sum()
+    eq = M.balanced_bounds(np.ones(64), 4, 16, 1024)
+    assert eq == M.strip_bounds(1024, 4, 16)
