@@ -108,14 +108,17 @@ def peaks():
 
 def ncu_traffic(kernel="k_step"):
     """DRAM bytes per launch of the kernel from the committed ncu --set full
-    capture summary (profiles/), or None."""
+    capture summary (profiles/), with its issue and FP64-pipe utilisation
+    (the resources that actually bound this bit-exact fp64 path), or None."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as f:
             d = json.load(f)
         k = d["kernels"][kernel]
         return {"bytes_per_launch": k["dram_bytes"], "source": d.get("source", p),
-                "cells_per_launch": k.get("cells")}
+                "cells_per_launch": k.get("cells"),
+                "fp64_pipe_pct": round(k["fp64_pipe_pct"], 1),
+                "issue_active_pct": round(k["issue_active_pct"], 1)}
     except Exception:
         return None
 
@@ -315,7 +318,11 @@ def b200_single(args):
                      "forces_kernel_ms": round(t_forces_kernel * 1e3, 4),
                      "kernel_share_of_step": round(t_step_kernel / (ms * 1e-3 / K), 4),
                      "peak_source": peak_src,
-                     "step_frac_of_hbm": round(alg_bytes / (ms * 1e-3 / K) / GB / hbm_peak, 4)},
+                     "step_frac_of_hbm": round(alg_bytes / (ms * 1e-3 / K) / GB / hbm_peak, 4),
+                     "ncu": ({"fp64_pipe_pct": traffic["fp64_pipe_pct"],
+                              "issue_active_pct": traffic["issue_active_pct"],
+                              "source": traffic["source"]} if traffic else None),
+                     "binding": "FP64 issue and dependency latency, not HBM (DESIGN.md section 4)"},
         "e2e": {"value": round(e2e_value, 3), "unit": "Mcells/s",
                 "h2d_bytes_per_step": int(h2d // E), "d2h_bytes_per_step": int(d2h // E),
                 "how": "CsphTvdStepper.step(FlowState) on pinned host buffers, every step: H and "
