@@ -300,8 +300,10 @@ def b200_single(args):
         "n_gpus": 1, "steps": K, "warmup": args.warmup, "ms_per_step": round(ms / K, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generator, scenarios.py)",
-        "config": {"workload": f"{sc.name} {sc.terrain.nx}x{sc.terrain.ny} h={sc.terrain.h} m, all "
-                               "physics (Manning field, wind, Coriolis, viscosity, 3 sources, open east edge)",
+        "config": {"workload": f"{sc.name} {sc.terrain.nx}x{sc.terrain.ny} h={sc.terrain.h} m, " + (
+                       "all physics (Manning field, wind, Coriolis, viscosity, 3 sources, open east edge)"
+                       if args.config in ("C3", "C5") else
+                       f"Manning n={sc.params.n_manning}, reflective edges"),
                    "cells": N, "active_fraction": round(last.active_fraction, 4),
                    "skip_dry_blocks": bool(sc.options.skip_dry_blocks),
                    "parallelism": "single GPU, fused tile kernels",
