@@ -1,28 +1,32 @@
 // swf_fused.cu — the FUSED fast path of one CSPH-TVD step on sm_100a.
 //
-// One step = 5 launches on the context's stream (captured in a CUDA graph
-// for swf_run):
-//   k_begin   1 thread   sources sigma_s(t_n), wind(t_n), counter reset
-//   k_forces  tiles      K1 + K2 + K3: the block mask of the tile's B-blocks
-//                        (block.cpp:16-61) and the fused-tile activity flags,
-//                        forces on wet cells (stores f - f_fric only) and the
-//                        CFL speed (shuffle + one atomicMax per CTA)
-//   k_tau     1 thread   tau = min(dt_max, K h / speed, dt_cap); t_mid,
-//                        wind(t_mid), sigma_s(t_mid)  (stepper.cpp:256-266, 311-319)
-//   k_step    tiles      K4..K8 fused: predictor on the tile + 2-cell halo,
-//                        mid forces + corrector on owned cells, minmod slopes
-//                        once per cell and direction, x- then y-face HLL
-//                        fluxes in shared memory, accumulate, final update
-//                        into the other state buffer (ping-pong)
-//   k_reduce  148 CTAs   fixed-order diagnostics partials; k_finish commits t
-// (block sizes that do not divide 16 use a separate k_mask/k_tiles pair).
+// One step on the context's stream (captured in a CUDA graph for swf_run):
+//   k_begin        1 thread   sources sigma_s(t_n), wind(t_n), counters
+//   k_flist        1 thr/tile dry-neighbourhood rule -> k_forces work list
+//   k_forces_list  persistent K1 + K2 + K3 per listed 32x16 tile: the block
+//                             mask of its B-blocks (block.cpp:16-61) and the
+//                             tile flags, forces on wet cells (f - f_fric
+//                             only), the CFL speed (shuffles + one atomicMax)
+//   k_forces_redo  148 CTAs   tiles with a rejected speculative division, exact
+//   k_tau          1 thread   tau = min(dt_max, K h / speed, dt_cap); t_mid,
+//                             wind(t_mid), sigma_s(t_mid) (stepper.cpp:256-266, 311-319)
+//   k_slist        1 thr/tile k_step work list (active or not-yet-copied tiles)
+//   k_step_list    persistent K4..K8 fused per tile: predictor on the tile + 2-cell
+//                             halo, mid forces + corrector on owned cells, minmod
+//                             slopes once per cell and direction, x- then y-face
+//                             HLL fluxes in shared memory, accumulate, final
+//                             update into the other state buffer (ping-pong)
+//   k_step_redo    148 CTAs   tiles with a rejected speculative division, exact
+//   k_reduce       148 CTAs   fixed-order diagnostics partials; k_finish commits t
+// (block sizes that do not divide 16 use a separate k_mask/k_tiles pair and
+// one CTA per tile; strip contexts split k_forces around the halo exchange).
 //
 // HBM traffic per wet cell-update: k_forces reads H,HUx,HUy,b (+n) and writes
 // 2 doubles; k_step reads H,HUx,HUy,b,f' (+n) and writes H,HUx,HUy — ≈120 B
 // against the 56 B compulsory minimum; the FP64 pipe and its dependency
-// chains, not HBM, bound this path.  Dry tiles cost one read
-// of H in k_forces and, once after they go dry, one copy between the
-// ping-pong buffers.
+// chains, not HBM, bound this path.  Dry tiles cost one
+// thread in each list kernel and, once after they go dry, one copy between
+// the ping-pong buffers.
 #include <cuda_runtime.h>
 
 #include <vector>
@@ -1533,13 +1537,7 @@ int fused_restore_host(swf_ctx* c, double* hH, double* hHUx, double* hHUy) {
   return cuda_check(c, cudaGetLastError(), "k_restore_host");
 }
 
-int fused_scatter_host(swf_ctx* c, double* hH, double* hHUx, double* hHUy) {
-  const Geo& G = c->geo;
-  int cur = c->cur;  // the committed state; its step used the flags of parity 1 - cur
-  k_scatter_host<<<148 * 8, NTHR, 0, c->stream>>>(G, tile_act_at(c, 1 - cur), c->H[cur],
-                                                  c->HUx[cur], c->HUy[cur], hH, hHUx, hHUy);
-  return cuda_check(c, cudaGetLastError(), "k_scatter_host");
-}
+
 
 // Sparse ingest of the momentum for a host-buffer step (swf_step_host on
 // pinned arrays): after the depth was copied in full and the block mask

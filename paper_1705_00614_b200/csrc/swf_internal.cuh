@@ -166,7 +166,6 @@ void stage_free(swf_ctx* c);
 int fused_enqueue_step(swf_ctx* c, double dt_cap);
 int fused_prepare(swf_ctx* c);
 int fused_reduce_ctas();
-int fused_scatter_host(swf_ctx* c, double* hH, double* hHUx, double* hHUy);
 int fused_restore_host(swf_ctx* c, double* hH, double* hHUx, double* hHUy);
 int fused_enqueue_phase1(swf_ctx* c, double dt_cap);
 int fused_enqueue_phase2(swf_ctx* c, double dt_cap);
