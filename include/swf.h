@@ -276,6 +276,16 @@ int swf_strip_finish(swf_ctx* ctx, const double* dev_global_speed, double dt_cap
 int swf_strip_end_batch(swf_ctx* ctx, int* done, swf_step_info* last);
 int swf_strip_pack_async(swf_ctx* ctx, int side, double* dst);
 int swf_strip_unpack_async(swf_ctx* ctx, int side, const double* src);
+/* P2P halo (fused exchange): the base pointers of this context's six state
+ * buffers [H0, H1, HUx0, HUx1, HUy0, HUy1] (for cudaIpcGetMemHandle), and
+ * registration of a neighbour's six buffers mapped into this process (side 0 =
+ * south neighbour, 1 = north; peer_row0 = the global row of the neighbour's
+ * local row 0; bufs6 = NULL unregisters).  With a peer registered, k_step
+ * stores every owned cell within SWF_HALO rows of that strip edge also into
+ * the neighbour's ghost rows of the next-parity buffer and fences, so the
+ * exchange reduces to a stream-ordered token per step (multigpu.py). */
+int swf_device_buffers(swf_ctx* ctx, double** out6);
+int swf_strip_set_peer(swf_ctx* ctx, int side, double* const* bufs6, int peer_row0);
 /* Owned global rows [j0, j1) and the ghost-row counts below/above. */
 int swf_strip_rows(const swf_ctx* ctx, int* j0, int* j1, int* ghost_lo,
                    int* ghost_hi);

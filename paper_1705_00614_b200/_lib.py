@@ -69,6 +69,8 @@ def declare(lib):
     _sig(lib, "swf_strip_unpack", I, P, I, C.c_void_p)
     _sig(lib, "swf_last_ingest_bytes", I, P, C.POINTER(C.c_longlong))
     _sig(lib, "swf_debug_redo_counts", I, P, PI)
+    _sig(lib, "swf_device_buffers", I, P, C.POINTER(C.c_void_p))
+    _sig(lib, "swf_strip_set_peer", I, P, I, C.POINTER(C.c_void_p), I)
     _sig(lib, "swf_strip_begin_batch", I, P)
     _sig(lib, "swf_strip_forces", I, P, D, I)
     _sig(lib, "swf_strip_local_speed", I, P, C.c_void_p)

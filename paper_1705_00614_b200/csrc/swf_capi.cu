@@ -1137,6 +1137,32 @@ int swf_strip_unpack_async(swf_ctx* c, int side, const double* src) {
   return cuda_check(c, e, "strip unpack");
 }
 
+int swf_device_buffers(swf_ctx* c, double** out6) {
+  if (!c || !out6) return SWF_ECONFIG;
+  double* b[6] = {c->H[0], c->H[1], c->HUx[0], c->HUx[1], c->HUy[0], c->HUy[1]};
+  for (int q = 0; q < 6; ++q) out6[q] = b[q];
+  return SWF_OK;
+}
+
+int swf_strip_set_peer(swf_ctx* c, int side, double* const* bufs6, int peer_row0) {
+  if (!c || side < 0 || side > 1) return SWF_ECONFIG;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  if (!bufs6) {
+    c->peer_on[side] = 0;
+  } else {
+    const Geo& G = c->geo;
+    bool has_ghosts = side == 0 ? G.r0 > 0 : G.r1 < G.rows;
+    if (!has_ghosts) return set_err(c, SWF_ECONFIG, "strip_set_peer: no neighbour on that side");
+    for (int f = 0; f < 3; ++f)
+      for (int p = 0; p < 2; ++p) c->peer[side][f][p] = bufs6[2 * f + p];
+    c->peer_drow[side] = G.jg0 - peer_row0;  // neighbour local row = ours + drow
+    c->peer_on[side] = 1;
+  }
+  drop_graph(c);
+  return SWF_OK;
+}
+
 int swf_strip_rows(const swf_ctx* c, int* j0, int* j1, int* glo, int* ghi) {
   const Geo& G = c->geo;
   if (j0) *j0 = G.jg0 + G.r0;

@@ -43,6 +43,7 @@ constexpr int AREGX = AX + 2, AREGY = AY + 2, AREG = AREGX * AREGY;  // 1-cell h
 constexpr int RX = BX + 4, RY = BY + 4, RREG = RX * RY;              // 2-cell halo
 constexpr int NTHR = 256;  // k_forces, k_reduce, k_scatter_host
 constexpr int MAXBF = 64;  // B-block flags of one tile staged in shared memory
+constexpr int HALO_ROWS = SWF_HALO;  // ghost rows per interior strip side (swf.h)
 #ifndef SWF_STEP_THREADS
 #define SWF_STEP_THREADS 256
 #endif
@@ -616,6 +617,11 @@ struct StepArgs {
   int* redo;                  // tiles whose speculative divisions were rejected
   int* list;                  // work list of k_slist / k_step_list
   FaceTaps taps;              // faces whose tau * fm this step records (nested grids)
+  // P2P halo (strips): the neighbours' NEXT-parity state buffers, mapped into
+  // this process; owned rows within HALO of a strip edge are also stored
+  // there, at the neighbour's local row = ours + peer_drow
+  double* peer[2][3];         // [south, north][H, HUx, HUy]
+  int peer_drow[2];
   double* hH;                 // pinned host arrays of a host-buffer step (write-through), or null
   double* hHUx;
   double* hHUy;
@@ -677,6 +683,22 @@ __device__ __forceinline__ Slopes cell_slopes(double em, double um, double tm, d
   s.un = minmod(rdiv(up - uc, Ri, ok), rdiv(uc - um, Ro, ok));
   s.ut = minmod(rdiv(tp - tc, Ri, ok), rdiv(tc - tm, Ro, ok));
   return s;
+}
+
+// The P2P halo write of one owned cell: rows within HALO of a strip edge
+// also go to the neighbour's ghost rows (same parity, its local row index).
+__device__ __forceinline__ void peer_store(const Geo& G, const StepArgs& A, int i, int r,
+                                           double h, double qx, double qy) {
+#pragma unroll
+  for (int side = 0; side < 2; ++side) {
+    if (!A.peer[side][0]) continue;
+    const bool edge = side == 0 ? r < G.r0 + HALO_ROWS : r >= G.r1 - HALO_ROWS;
+    if (!edge) continue;
+    const size_t k = (size_t)i + (size_t)(r + A.peer_drow[side]) * G.nx;
+    A.peer[side][0][k] = h;
+    A.peer[side][1][k] = qx;
+    A.peer[side][2][k] = qy;
+  }
 }
 
 // One side of a face from the cell's slopes (stepper.cpp:112-122).
@@ -743,9 +765,11 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
           A.Ho[k] = A.H[k];
           A.HUxo[k] = A.HUx[k];
           A.HUyo[k] = A.HUy[k];
+          peer_store(G, A, i, r, A.H[k], A.HUx[k], A.HUy[k]);
         }
       }
       if (tid == 0) A.tile_same[tile] = 1;
+      if (A.peer[0][0] || A.peer[1][0]) __threadfence_system();
     }
     if (tid < 3) A.part[5 * (size_t)tile + tid] = 0.0;
     return;
@@ -1128,6 +1152,7 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
       A.Ho[k] = Ht[m];  // no active cell in such a block: (Ht, Qx, Qy) = step-start state
       A.HUxo[k] = Qx[m];
       A.HUyo[k] = Qy[m];
+      peer_store(G, A, i, r, Ht[m], Qx[m], Qy[m]);
       continue;
     }
     int sf = x + y * BX, nf_ = sf + BX;  // S and N face of the cell
@@ -1168,8 +1193,12 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
       A.hHUx[k] = qx;
       A.hHUy[k] = qy;
     }
+    peer_store(G, A, i, r, H1, qx, qy);
   }
   if (tid == 0) A.tile_same[tile] = 0;
+  // the neighbour reads these rows after a stream-ordered token from us:
+  // make the peer stores visible system-wide before this kernel completes
+  if (A.peer[0][0] || A.peer[1][0]) __threadfence_system();
 
   PHASE_MARK(7);
   // ---- per-tile diagnostic partials (deterministic) ------------------------
@@ -1289,6 +1318,10 @@ __global__ void k_finish(const double* red, int nred, StepScalars* sc, double ar
 StepArgs step_args(swf_ctx* c) {
   StepArgs A;
   A.taps = c->taps;
+  for (int side = 0; side < 2; ++side) {
+    for (int f = 0; f < 3; ++f) A.peer[side][f] = c->peer_on[side] ? c->peer[side][f][1 - c->cur] : nullptr;
+    A.peer_drow[side] = c->peer_drow[side];
+  }
   A.hH = c->wt_host[0];
   A.hHUx = c->wt_host[1];
   A.hHUy = c->wt_host[2];

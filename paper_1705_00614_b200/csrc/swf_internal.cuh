@@ -122,6 +122,10 @@ struct swf_ctx {
   int* d_list_s = nullptr;  // k_step work list
   int sm_count = 148;
   swf::FaceTaps taps;  // owned by the nests that registered them
+  // P2P halo: the neighbours' state buffers mapped here ([side][field][parity])
+  double* peer[2][3][2] = {};
+  int peer_on[2] = {0, 0};
+  int peer_drow[2] = {0, 0};
   double* d_part = nullptr;              // per-tile diagnostic partials (3 per tile)
   // scalars
   swf::StepScalars* d_sc = nullptr;

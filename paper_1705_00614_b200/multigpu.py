@@ -179,6 +179,16 @@ class Strip:
     def stream_handle(self) -> int:
         return self._lib.swf_stream(self.ctx) or 0
 
+    # P2P halo (include/swf.h "P2P halo")
+    def device_buffers(self):
+        out = (C.c_void_p * 6)()
+        self._rc(self._lib.swf_device_buffers(self.ctx, out))
+        return [out[q] for q in range(6)]
+
+    def set_peer(self, side: int, ptrs, peer_row0: int):
+        arr = (C.c_void_p * 6)(*ptrs) if ptrs is not None else None
+        self._rc(self._lib.swf_strip_set_peer(self.ctx, side, arr, int(peer_row0)))
+
     # asynchronous steps (include/swf.h "Asynchronous strip steps")
     def begin_batch(self):
         self._rc(self._lib.swf_strip_begin_batch(self.ctx))
@@ -397,6 +407,98 @@ class RankStrip:
         g = dist_allreduce_max(sp, self.xdev)
         return self.strip.phase2(g, dt_cap)
 
+    # ---- P2P halo: k_step stores the boundary rows into the neighbours ----
+    def setup_p2p(self) -> bool:
+        """Map the neighbours' state buffers into this process (CUDA IPC,
+        peer access over NVLink between GPUs, or the same device) and register
+        them with the strip context, so the halo travels inside k_step (peer
+        stores + a system fence) and a step only exchanges a 4-byte token.
+        The ghost rows of the current buffer are filled once by a regular
+        exchange.  Returns False (and keeps the copy exchange) when IPC is
+        unavailable; every rank must agree, so the outcome is allreduced."""
+        import torch
+        import torch.distributed as dist
+        from cuda.bindings import runtime as rt
+        ok = True
+        handles = None
+        try:
+            hs = []
+            for p in self.strip.device_buffers():
+                err, h = rt.cudaIpcGetMemHandle(p)
+                if err != rt.cudaError_t.cudaSuccess:
+                    raise RuntimeError(f"cudaIpcGetMemHandle: {err}")
+                hs.append(bytes(h.reserved))
+            handles = (hs, self.w0)
+        except Exception:
+            ok = False
+        objs = [None] * self.world
+        dist.all_gather_object(objs, (handles, ok))
+        ok = all(o[1] for o in objs)
+        opened = []
+        if ok:
+            try:
+                for side, peer in exchange_plan(self.rank, self.world):
+                    hs, peer_w0 = objs[peer][0]
+                    ptrs = []
+                    for hb in hs:
+                        h = rt.cudaIpcMemHandle_t()
+                        h.reserved = hb
+                        err, dp = rt.cudaIpcOpenMemHandle(h, rt.cudaIpcMemLazyEnablePeerAccess)
+                        if err != rt.cudaError_t.cudaSuccess:
+                            raise RuntimeError(f"cudaIpcOpenMemHandle: {err}")
+                        ptrs.append(int(dp))
+                        opened.append(int(dp))
+                    self.strip.set_peer(side, ptrs, peer_w0)
+            except Exception:
+                ok = False
+        flag = torch.tensor([1.0 if ok else 0.0], dtype=torch.float64, device=self.xdev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        ok = flag.item() == 1.0
+        if not ok:
+            for side in (0, 1):
+                try:
+                    self.strip.set_peer(side, None, 0)
+                except Exception:
+                    pass
+            for dp in opened:
+                rt.cudaIpcCloseMemHandle(dp)
+            self.p2p = False
+            return False
+        # fill the current buffer's ghost rows once
+        dist_exchange(self._pack, self._unpack, self.strip.count, self.rank, self.world, self.xdev)
+        self.p2p = True
+        self._ipc = opened
+        return True
+
+    def _token(self):
+        """The per-step synchronisation of the P2P halo: a 1-element
+        exchange with each neighbour, stream-ordered after this rank's last
+        k_step (whose peer stores it publishes) and before the boundary forces."""
+        import torch
+        import torch.distributed as dist
+        ops = []
+        if not hasattr(self, "_tok"):
+            self._tok = {s: (torch.zeros(1, dtype=torch.float64, device=self.xdev),
+                             torch.zeros(1, dtype=torch.float64, device=self.xdev))
+                         for s, _ in exchange_plan(self.rank, self.world)}
+        for side, peer in exchange_plan(self.rank, self.world):
+            sb, rb = self._tok[side]
+            ops.append(dist.P2POp(dist.isend, sb, peer))
+            ops.append(dist.P2POp(dist.irecv, rb, peer))
+        return dist.batch_isend_irecv(ops) if ops else []
+
+    def step_p2p(self, dt_cap: float = 0.0):
+        """Host-synchronised P2P step (gloo tests): the neighbours' k_step
+        already wrote our ghost rows; the token orders their completion."""
+        import torch
+        torch.cuda.synchronize(self.dev)
+        for w in self._token():
+            w.wait()
+        sp = self.strip.phase1(dt_cap)
+        g = dist_allreduce_max(sp, self.xdev)
+        info = self.strip.phase2(g, dt_cap)
+        return info
+
     # ---- NCCL, asynchronous: no host synchronisation inside a batch -------
     def _async_setup(self):
         import torch
@@ -422,19 +524,28 @@ class RankStrip:
         import torch
         import torch.distributed as dist
         with torch.cuda.stream(self._stream):
-            ops = []
-            for side, peer in exchange_plan(self.rank, self.world):
-                sbuf, rbuf = self._abufs[side]
-                self.strip.pack_async(side, sbuf.data_ptr())
-                ops.append(dist.P2POp(dist.isend, sbuf, peer))
-                ops.append(dist.P2POp(dist.irecv, rbuf, peer))
-            works = dist.batch_isend_irecv(ops) if ops else []
-            self.strip.forces(0, dt_cap)  # overlaps the exchange
-            for w in works:
-                w.wait()  # the strip stream waits for the comm stream (device side)
-            for side, (sbuf, rbuf) in self._abufs.items():
-                self.strip.unpack_async(side, rbuf.data_ptr())
-            self.strip.forces(1, dt_cap)
+            if getattr(self, "p2p", False):
+                # the halo arrived inside the neighbours' k_step (peer stores);
+                # only the ordering token crosses the links here
+                works = self._token()
+                self.strip.forces(0, dt_cap)  # overlaps the token
+                for w in works:
+                    w.wait()
+                self.strip.forces(1, dt_cap)
+            else:
+                ops = []
+                for side, peer in exchange_plan(self.rank, self.world):
+                    sbuf, rbuf = self._abufs[side]
+                    self.strip.pack_async(side, sbuf.data_ptr())
+                    ops.append(dist.P2POp(dist.isend, sbuf, peer))
+                    ops.append(dist.P2POp(dist.irecv, rbuf, peer))
+                works = dist.batch_isend_irecv(ops) if ops else []
+                self.strip.forces(0, dt_cap)  # overlaps the exchange
+                for w in works:
+                    w.wait()  # the strip stream waits for the comm stream (device side)
+                for side, (sbuf, rbuf) in self._abufs.items():
+                    self.strip.unpack_async(side, rbuf.data_ptr())
+                self.strip.forces(1, dt_cap)
             self.strip.local_speed(self._speed.data_ptr())
             dist.all_reduce(self._speed, op=dist.ReduceOp.MAX)
             self.strip.finish(self._speed.data_ptr(), dt_cap)
@@ -475,6 +586,9 @@ def bench_strips(args) -> Optional[dict]:
     bs = 16
 
     use_async = rs.backend == "nccl"
+    # the halo travels inside k_step (peer stores into the neighbours' ghost
+    # rows) unless SWF_HALO=copy or CUDA IPC is unavailable on this box
+    p2p = use_async and os.environ.get("SWF_HALO", "p2p") != "copy" and rs.setup_p2p()
 
     def step():
         return rs.step(0.0)
@@ -570,10 +684,13 @@ def bench_strips(args) -> Optional[dict]:
         "data": "synthetic (seeded generator, scenarios.py)",
         "config": {"workload": f"{sc.name.split('-')[0]} {full_n}x{full_n} row strips",
                    "cells": N_total, "strips": bounds, "halo_rows": HALO,
-                   "parallelism": f"row strips x{world}, " + ("NCCL halo send/recv overlapped with interior "
-                                                                 "forces + device allreduce-max, no host sync"
-                                                                 if use_async else
-                                                                 "halo send/recv + allreduce-max (host-synchronised)"),
+                   "parallelism": f"row strips x{world}, " + (
+                       "P2P halo stored by k_step into the neighbours' ghost rows (CUDA IPC over "
+                       "NVLink) + a 4-byte NCCL token per neighbour overlapped with interior "
+                       "forces + device allreduce-max, no host sync" if p2p else
+                       "NCCL halo send/recv overlapped with interior forces + device "
+                       "allreduce-max, no host sync" if use_async else
+                       "halo send/recv + allreduce-max (host-synchronised)"),
                    "l2": "inputs larger than L2"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
                      "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),

@@ -16,8 +16,14 @@ def main():
     n = int(os.environ.get("SWF_CHECK_N", "512"))
     steps = int(os.environ.get("SWF_CHECK_STEPS", "20"))
     rs = M.RankStrip("C3", n_full=n)
+    p2p = os.environ.get("SWF_HALO") == "p2p"
+    if p2p:
+        assert rs.setup_p2p(), "P2P halo setup failed"
     for _ in range(steps):
-        rs.step()
+        if p2p:
+            rs.step_p2p()
+        else:
+            rs.step()
     got = rs.gather_state()
     ok = 1
     if rs.rank == 0:
@@ -32,7 +38,8 @@ def main():
         (H, X, Y), t = got
         same = all(np.array_equal(a.view(np.int64), b.view(np.int64))
                    for a, b in ((H, st.H), (X, st.HUx), (Y, st.HUy))) and t == st.t
-        print(f"multirank world={rs.world} n={n} steps={steps} bitwise_equal={same} t={t}", flush=True)
+        print(f"multirank world={rs.world} n={n} steps={steps} p2p={p2p} bitwise_equal={same} t={t}",
+              flush=True)
         ok = 1 if same else 0
     flag = [ok]
     dist.broadcast_object_list(flag, src=0)
