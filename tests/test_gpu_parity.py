@@ -411,3 +411,30 @@ def test_cfl_abort_pinned_write_through_restores_state(gpu_cls, oracle_built):
     with pytest.raises(NumericalError, match="particle displacement"):
         s.step(st, 0.1)
     assert_state_bitwise(st, before, "pinned state changed on abort")
+
+
+@pytest.mark.parametrize("nx,ny,bs", [(97, 53, 16), (33, 130, 8), (161, 17, 7)])
+def test_odd_sizes_vs_oracle(gpu_cls, oracle_built, nx, ny, bs):
+    """Partial tiles in both directions, odd row lengths (scalar ingest path),
+    block sizes that do and do not divide the 32x16 tile: bitwise vs the
+    oracle, through the resident path and through pinned host buffers."""
+    import torch
+    from paper_1705_00614_b200.types import FlowState
+    sc = S.floodplain(192, 50.0, window=(11, 23, nx, ny))
+    sc.options.block_size = bs
+    st = sc.state.copy()
+    g = make(gpu_cls, sc)
+    o = make(oracle_built.OracleStepper, sc)
+    a = st.copy()
+    g.upload(a)
+    for _ in range(10):
+        g.step_resident()
+        o.step(st)
+    g.download(a)
+    assert_state_bitwise(a, st, f"{nx}x{ny} resident")
+    pin = lambda v: torch.from_numpy(v.copy()).pin_memory().numpy()
+    hs = FlowState(nx, ny, st.t, pin(st.H), pin(st.HUx), pin(st.HUy))
+    for _ in range(5):
+        g.step(hs)
+        o.step(st)
+    assert_state_bitwise(hs, st, f"{nx}x{ny} pinned")
