@@ -39,7 +39,6 @@ def parse():
     p.add_argument("--no-skip", action="store_true", help="disable dry-block skipping")
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-seconds", type=float, default=15.0)
     return p.parse_args()
 
 
@@ -126,13 +125,19 @@ def ncu_traffic(kernel="k_step"):
 # ---------------------------------------------------------------------------
 # reference CPU arm (and cpu_baseline)
 # ---------------------------------------------------------------------------
-def cpu_reference(config, seconds, threads=None):
-    """Time the reference's CPU implementation on a bounded crop of the
-    workload; returns (mcells_per_s, cores, kind, sample description)."""
+def cpu_reference(config, warmup=5, steps=30, threads=None, crop=2048):
+    """The reference's CPU implementation on a bounded sample of the workload,
+    stepped like the B200 arm: `warmup` untimed steps, then `steps` timed
+    steps, from the same initial state (so both cover the same simulated
+    window of the flood).  The sample is 8 crops of crop^2 cells along the
+    diagonal of the full C3/C5 grid (same generator; the wet/dry mix of the
+    domain is spatially correlated, so one crop is not representative); one
+    "step" steps all 8 crops once.  Returns (Mcell-updates/s, cores, kind,
+    sample description, per-step Mcell/s list)."""
     from oracle import pyorc
     from paper_1705_00614_b200 import scenarios as S
     kind = "reference" if pyorc.available("ref") else "port"
-    if not pyorc.available(kind if kind == "ref" else "orc"):
+    if not pyorc.available("ref" if kind == "reference" else "orc"):
         try:
             pyorc.build(ref=False)
         except Exception:
@@ -142,14 +147,12 @@ def cpu_reference(config, seconds, threads=None):
         cores = 1
     n_full = {"C3": 16384, "C5": 32768}.get(config, 0)
     if n_full:
-        # 8 crops of 1024^2 on the diagonal: the wet/dry mix of the full domain
-        # (~35% wet) is spatially correlated, so one crop is not representative
-        crop = 1024
-        wins = [(k * (n_full // 8) + (n_full // 16) - crop // 2,) * 2 + (crop, crop) for k in range(8)]
+        c = min(crop, n_full // 8)
+        wins = [(k * (n_full // 8) + (n_full // 16) - c // 2,) * 2 + (c, c) for k in range(8)]
         scs = [S.build(config, window=w) for w in wins]
     else:
         scs = [S.build(config)]
-    cell_updates, el_total, steps_total = 0, 0.0, 0
+    steppers = []
     for sc in scs:
         sc.options.workers = cores
         o = pyorc.OracleStepper(sc.terrain, sc.params, sc.control, sc.options,
@@ -159,20 +162,23 @@ def cpu_reference(config, seconds, threads=None):
         if sc.sources:
             o.set_sources(sc.sources)
         o.upload(sc.state)
-        o.run(1)  # warm-up
-        steps, t0 = 0, time.perf_counter()
-        while True:
+        steppers.append(o)
+    cells = sum(sc.cells() for sc in scs)
+    for _ in range(warmup):
+        for o in steppers:
             o.run(1)
-            steps += 1
-            el = time.perf_counter() - t0
-            if el >= seconds / len(scs) or steps >= 500:
-                break
-        cell_updates += sc.cells() * steps
-        el_total += el
-        steps_total += steps
+    per_step, t_all = [], time.perf_counter()
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        for o in steppers:
+            o.run(1)
+        per_step.append(cells / (time.perf_counter() - t0) / 1e6)
+    el = time.perf_counter() - t_all
+    for o in steppers:
         o.close()
-    v = cell_updates / el_total / 1e6
-    what = (f"8 diagonal 1024x1024 crops of {config}" if n_full else f"{config} full grid")
+    v = cells * steps / el / 1e6
+    what = (f"8 diagonal {scs[0].terrain.nx}x{scs[0].terrain.ny} crops of {config}" if n_full
+            else f"{config} full grid")
     cpu = "unknown CPU"
     try:
         with open("/proc/cpuinfo") as f:
@@ -181,28 +187,24 @@ def cpu_reference(config, seconds, threads=None):
         pass
     built = ("the reference sources compiled by oracle/Makefile: g++ -O3 -ffp-contract=off "
              "-fopenmp, no -march" if kind == "reference" else "the C restatement (gcc -O2)")
-    sample = (f"{what} (same generator), {steps_total} crop-steps after 1 warm-up each, "
-              f"{el_total:.1f} s, {cores} thread(s) of {os.cpu_count()} on {cpu}; {built}")
-    return v, cores, ("reference" if kind == "reference" else "port"), sample
+    sample = (f"{what} (same generator, {cells / 1e6:.1f} M cells), {warmup} warm-up + {steps} "
+              f"timed steps from t=0 like the B200 arm, {el:.1f} s, {cores} thread(s) of "
+              f"{os.cpu_count()} on {cpu}; {built}")
+    return v, cores, ("reference" if kind == "reference" else "port"), sample, per_step
 
 
 def reference_arm(args):
+    """bench.py --impl reference: the reference's CPU path with every host
+    thread, W warm-up and K timed steps of the bounded sample (cpu_reference)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    per_step = []
-    cores = kind = sample = None
-    for _ in range(args.warmup):
-        cpu_reference(args.config, seconds=min(3.0, args.cpu_seconds / 4))
-    for _ in range(args.steps):
-        v, cores, kind, sample = cpu_reference(args.config, seconds=max(2.0, args.cpu_seconds / args.steps))
-        per_step.append(v)
-    v = sum(per_step) / len(per_step)
+    v, cores, kind, sample, per_step = cpu_reference(args.config, args.warmup, args.steps)
     line = {"metric": "cell-updates/sec (Mcells/s)", "value": round(v, 3), "unit": "Mcells/s",
             "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config} (bounded crop on host CPU)", "grid": args.config},
+            "config": {"workload": f"{args.config} (bounded sample on host CPU)", "grid": args.config},
             "cpu_baseline": {"value": round(v, 3), "unit": "Mcells/s", "cores": cores,
                              "kind": kind, "sample": sample},
             "e2e": {"value": round(v, 3), "unit": "Mcells/s", "h2d_bytes_per_step": 0,
@@ -288,7 +290,7 @@ def b200_single(args):
     cpu = None
     if not args.no_cpu_baseline:
         try:
-            v, cores, kind, sample = cpu_reference(args.config, args.cpu_seconds)
+            v, cores, kind, sample, _ = cpu_reference(args.config, args.warmup, args.steps)
             cpu = {"value": round(v, 3), "unit": "Mcells/s", "cores": cores, "kind": kind,
                    "sample": sample}
         except Exception as e:  # reported, not fatal
