@@ -639,6 +639,8 @@ def bench_strips(args) -> Optional[dict]:
     per_act = 56 + (8 if sc.params.n_field is not None else 0)
     alg = per_act * n_act + 8 * (n_own - n_act)
     # aggregate kernel-level bandwidth: sum of per-rank algorithmic bytes / max k_step time
+    nact_all = torch.tensor([float(n_act)], dtype=torch.float64, device=rs.xdev)
+    dist.all_reduce(nact_all, op=dist.ReduceOp.SUM)
     agg = torch.tensor([alg, t_kstep], dtype=torch.float64, device=rs.xdev)
     alg_all = agg[0:1].clone()
     dist.all_reduce(alg_all, op=dist.ReduceOp.SUM)
@@ -679,6 +681,7 @@ def bench_strips(args) -> Optional[dict]:
     traffic = ncu_traffic("k_step")
     line = {
         "metric": "cell-updates/sec (Mcells/s)", "value": round(value, 3), "unit": "Mcells/s",
+        "value_active": round(float(nact_all.item()) * K / (ms_max * 1e-3) / 1e6, 3),
         "n_gpus": world, "steps": K, "warmup": args.warmup, "ms_per_step": round(ms_max / K, 4),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generator, scenarios.py)",
