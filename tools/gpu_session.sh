@@ -17,6 +17,8 @@ if [ -z "$SKIP_TESTS" ]; then
 fi
 timeout 900 python bench.py > "$O/bench.json" 2> "$O/bench.err"
 echo "bench exit $?" >> "$O/bench.err"
+timeout 900 python bench.py --impl reference > "$O/reference.json" 2> "$O/reference.err"
+echo "reference exit $?" >> "$O/reference.err"
 timeout 300 python tools/kernel_times.py C3 10 > "$O/kernel_times.json" 2>&1
 # launch list of resident steps only (the e2e host-buffer steps are PCIe-bound
 # and would distort the kernel shares)
