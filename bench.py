@@ -293,6 +293,11 @@ def b200_single(args):
             v, cores, kind, sample, _ = cpu_reference(args.config, args.warmup, args.steps)
             cpu = {"value": round(v, 3), "unit": "Mcells/s", "cores": cores, "kind": kind,
                    "sample": sample}
+            # a 1-core run beside the all-threads one (a shorter
+            # window: 1 warm-up + 2 timed steps of the same 8 crops)
+            v1, _, _, sample1, _ = cpu_reference(args.config, 1, 2, threads=1)
+            cpu["single_core"] = {"value": round(v1, 3), "unit": "Mcells/s", "cores": 1,
+                                  "sample": sample1}
         except Exception as e:  # reported, not fatal
             cpu = {"value": None, "unit": "Mcells/s", "cores": None, "kind": None,
                    "sample": f"unavailable: {e}"}
