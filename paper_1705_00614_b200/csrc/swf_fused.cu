@@ -55,7 +55,7 @@ constexpr int NPART_ALLOC = 5;  // doubles per tile in d_part (see k_reduce)
 #define SWF_STEP_MINB 3  // CTAs per SM the register budget of k_step targets
 #endif
 #ifndef SWF_FORCES_MINB
-#define SWF_FORCES_MINB 5
+#define SWF_FORCES_MINB 6
 #endif
 
 __device__ __forceinline__ bool stopped(const StepScalars* sc) { return sc->err_key != ERR_NONE; }
@@ -258,6 +258,20 @@ __device__ __forceinline__ double msig(const Geo& G, const DevSrc* src, const do
   double vx, vy;
   return msrc(G, src, sig, mask, i, jg, vx, vy);
 }
+
+// Neighbour view over shared-memory planes (depth, eta, ux, uy at index q),
+// read where the force helpers use them: holding the four neighbours' values
+// in registers across cell_forces spilled them (k_forces at its 40-register
+// budget, k_step's phase 2).
+struct SNbr {
+  bool in;
+  const double *d, *e, *u, *v;
+  int q;
+  __device__ __forceinline__ double dep() const { return d[q]; }
+  __device__ __forceinline__ double et() const { return e[q]; }
+  __device__ __forceinline__ double vx() const { return u[q]; }
+  __device__ __forceinline__ double vy() const { return v[q]; }
+};
 
 // ---------------------------------------------------------------------------
 // Speculative division.  The tile bodies are templates on SPEC.  With SPEC,
@@ -476,17 +490,9 @@ __device__ __forceinline__ void forces_tile(const Geo& G, const ForcesArgs& A, c
     double d = s_d[s];
     if (!(d > P.eps)) continue;
     int jg = G.jg0 + r;
-    auto nb = [&](bool in, int q) {
-      Nbr n;
-      n.in = in;
-      n.depth = s_d[q];
-      n.eta = s_e[q];
-      n.ux = s_u[q];
-      n.uy = s_v[q];
-      return n;
-    };
-    Nbr W = nb(i > 0, s - 1), E = nb(i + 1 < G.nx, s + 1);
-    Nbr S = nb(jg > 0, s - AREGX), N = nb(jg + 1 < G.ny, s + AREGX);
+    auto nb = [&](bool in, int q) { return SNbr{in, s_d, s_e, s_u, s_v, q}; };
+    SNbr W = nb(i > 0, s - 1), E = nb(i + 1 < G.nx, s + 1);
+    SNbr S = nb(jg > 0, s - AREGX), N = nb(jg + 1 < G.ny, s + AREGX);
     double sg = 0.0, svx = 0.0, svy = 0.0;
     if (srcm) sg = msrc(G, A.src, A.sig, srcm, i, jg, svx, svy);
     size_t k = (size_t)i + (size_t)r * nx;
@@ -906,16 +912,10 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
     double fmx = 0.0, fmy = 0.0;
     if (d > P.eps) {
       auto nb = [&](bool in, int q) {
-        Nbr o;
-        o.in = in;
-        o.depth = R[F_D * RREG + q];
-        o.eta = R[F_E * RREG + q];
-        o.ux = R[F_U * RREG + q];
-        o.uy = R[F_V * RREG + q];
-        return o;
+        return SNbr{in, R + F_D * RREG, R + F_E * RREG, R + F_U * RREG, R + F_V * RREG, q};
       };
-      Nbr W = nb(i > 0, s - 1), E = nb(i + 1 < G.nx, s + 1);
-      Nbr S = nb(jg > 0, s - RX), N = nb(jg + 1 < G.ny, s + RX);
+      SNbr W = nb(i > 0, s - 1), E = nb(i + 1 < G.nx, s + 1);
+      SNbr S = nb(jg > 0, s - RX), N = nb(jg + 1 < G.ny, s + RX);
       ForceOut o = cell_forces(d, R[F_U * RREG + s], R[F_V * RREG + s], R[F_E * RREG + s], W,
                                E, S, N, n, P, G.nwind > 0, wmx, wmy, nsrc > 0 ? sgm : 0.0, svx,
                                svy, SP);
