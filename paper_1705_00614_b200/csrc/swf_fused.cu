@@ -600,7 +600,8 @@ enum { F_D = 0, F_E, F_U, F_V, F_SX, F_SY, F_B, F_NUM };
 constexpr int NSL = (BX + 2) * BY > BX * (BY + 2) ? (BX + 2) * BY : BX * (BY + 2);  // slopes
 constexpr int NFC = (BX + 1) * BY > BX * (BY + 1) ? (BX + 1) * BY : BX * (BY + 1);  // faces
 constexpr int SCRATCH_A = 3 * NSL + 4 * NFC;               // slopes + faces (phases 3-5)
-constexpr int SCRATCH_B = 3 * NSL + 3 * BX * BY + RREG;    // phase 1-2 staging (see k_step)
+// phase 1-2 staging (see k_step), + the predictor's Manning lambda per owned cell
+constexpr int SCRATCH_B = 3 * NSL + 3 * BX * BY + RREG + BX * BY;
 constexpr int SCRATCH = SCRATCH_A > SCRATCH_B ? SCRATCH_A : SCRATCH_B;
 
 struct StepArgs {
@@ -810,8 +811,11 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
   double* SC = SL;                      // [0,RREG) fpx  [RREG,2RREG) fpy   (phase 1 only)
   double* OWN = SL + 3 * NSL;           // 3 x (BX*BY): H, HUx, HUy at t_n of owned cells
   double* NF = OWN + 3 * BX * BY;       // RREG: Manning n of the region
+  // BX*BY: lambda(H12, n) of owned cells as the predictor evaluated it, or -1
+  double* LAM = NF + RREG;
   static_assert(2 * RREG <= 3 * NSL, "phase-1 scratch overlaps OWN");
-  static_assert(3 * NSL + 3 * BX * BY + RREG <= SCRATCH, "phase-1 scratch overflow");
+  static_assert(3 * NSL + 3 * BX * BY + RREG + BX * BY <= SCRATCH,
+                "phase-1 scratch overflow");
   for (int c = tid; c < RREG; c += STHR) {
     int i = i0 - 2 + c % RX, r = r0 - 2 + c / RX;
     double h = 0.0, mx = 0.0, my = 0.0, bb = 0.0, fx = 0.0, fy = 0.0, n = G.n_manning;
@@ -843,12 +847,14 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
     double d = 0.0, e = 0.0, u = 0.0, v = 0.0, sx = 0.0, sy = 0.0;
     double Hn = R[F_D * RREG + c], mx = R[F_U * RREG + c], my = R[F_V * RREG + c];
     double bb = R[F_B * RREG + c];
-    if (xr >= 2 && xr < BX + 2 && yr >= 2 && yr < BY + 2) {  // owned: keep t_n
-      int o = (xr - 2) + (yr - 2) * BX;
+    const bool owned = xr >= 2 && xr < BX + 2 && yr >= 2 && yr < BY + 2;
+    const int o = (xr - 2) + (yr - 2) * BX;
+    if (owned) {  // keep t_n
       OWN[o] = Hn;
       OWN[BX * BY + o] = mx;
       OWN[2 * BX * BY + o] = my;
     }
+    double lam = -1.0;
     if (i >= 0 && i < G.nx && r >= 0 && r < G.rows) {
       double sg = srcm ? msig(G, A.src, sig_n, srcm, i, G.jg0 + r) : 0.0;
       bool act = Hn > P.eps || sg != 0.0;
@@ -856,7 +862,7 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
       if (act) {
         bool wet = Hn > P.eps;
         double fx = wet ? SC[c] : 0.0, fy = wet ? SC[RREG + c] : 0.0;
-        predict_cell(Hn, mx, my, sg, fx, fy, NF[c], half_tau, P.eps, P.g, d, mx, my, SP);
+        predict_cell(Hn, mx, my, sg, fx, fy, NF[c], half_tau, P.eps, P.g, d, mx, my, SP, &lam);
       }
       e = d + bb;
       if (d > P.eps) {
@@ -877,6 +883,7 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
     R[F_V * RREG + c] = v;
     R[F_SX * RREG + c] = sx;
     R[F_SY * RREG + c] = sy;
+    if (owned) LAM[o] = lam;
   }
   __syncthreads();
 
@@ -910,21 +917,26 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
     double n = NF[s];
     double d = R[F_D * RREG + s];  // H12
     double fmx = 0.0, fmy = 0.0;
+    // lambda depends on (depth, n) only: the predictor's lambda(H12) serves
+    // the mid forces, and the corrector reuses it when Ht == H12 (no source)
+    double lam = LAM[c], Hk = -1.0;
     if (d > P.eps) {
       auto nb = [&](bool in, int q) {
         return SNbr{in, R + F_D * RREG, R + F_E * RREG, R + F_U * RREG, R + F_V * RREG, q};
       };
       SNbr W = nb(i > 0, s - 1), E = nb(i + 1 < G.nx, s + 1);
       SNbr S = nb(jg > 0, s - RX), N = nb(jg + 1 < G.ny, s + RX);
-      ForceOut o = cell_forces(d, R[F_U * RREG + s], R[F_V * RREG + s], R[F_E * RREG + s], W,
-                               E, S, N, n, P, G.nwind > 0, wmx, wmy, nsrc > 0 ? sgm : 0.0, svx,
-                               svy, SP);
+      if (!(lam >= 0.0)) lam = manning_lambda(d, P.g, n);
+      Hk = d;
+      ForceOut o = cell_forces_lam(d, R[F_U * RREG + s], R[F_V * RREG + s], R[F_E * RREG + s],
+                                   W, E, S, N, lam, P, G.nwind > 0, wmx, wmy,
+                                   nsrc > 0 ? sgm : 0.0, svx, svy, SP);
       fmx = o.fx - o.frx;
       fmy = o.fy - o.fry;
     }
     double ht, qx, qy, sv;
     correct_cell(Hn, qxn, qyn, nsrc > 0, sgm, d, fmx, fmy, n, tau, P.eps, P.g, ht, qx, qy, sv,
-                 SP);
+                 SP, Hk, &lam);
     srcvol += sv;
     // CFL abort (stepper.cpp:378-380, 391-399): dr = tau * u12
     double dx = tau * R[F_U * RREG + s], dy = tau * R[F_V * RREG + s];
