@@ -859,14 +859,15 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
       double sg = srcm ? msig(G, A.src, sig_n, srcm, i, G.jg0 + r) : 0.0;
       bool act = Hn > P.eps || sg != 0.0;
       d = Hn;
+      Recip Rd{0.0, 0.0};
       if (act) {
         bool wet = Hn > P.eps;
         double fx = wet ? SC[c] : 0.0, fy = wet ? SC[RREG + c] : 0.0;
-        predict_cell(Hn, mx, my, sg, fx, fy, NF[c], half_tau, P.eps, P.g, d, mx, my, SP, &lam);
+        predict_cell(Hn, mx, my, sg, fx, fy, NF[c], half_tau, P.eps, P.g, d, mx, my, SP, &lam,
+                     &Rd);  // Rd = recip_of(H12) whenever H12 > eps
       }
       e = d + bb;
-      if (d > P.eps) {
-        Recip Rd = recip_of(d);
+      if (d > P.eps) {  // implies act (an inactive cell has d = Hn <= eps)
         u = rdiv(mx, Rd, SP);
         v = rdiv(my, Rd, SP);
       }
