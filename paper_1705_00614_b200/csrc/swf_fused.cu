@@ -1177,13 +1177,7 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
     double cx = 0.0, cy = 0.0;
     if (wet) {
       auto nb = [&](bool in, int q) {
-        Nbr o;
-        o.in = in;
-        o.depth = R[F_D * RREG + q];
-        o.eta = R[F_E * RREG + q];
-        o.ux = 0.0;
-        o.uy = 0.0;
-        return o;
+        return SNbr{in, R + F_D * RREG, R + F_E * RREG, R + F_U * RREG, R + F_V * RREG, q};
       };
       double eta_c = R[F_E * RREG + s];
       double gx = eta_grad_comp(nb(i > 0, s - 1), nb(i + 1 < G.nx, s + 1), eta_c, P, SP);
