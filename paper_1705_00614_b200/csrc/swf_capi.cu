@@ -621,6 +621,10 @@ int swf_step_host(swf_ctx* c, double* H, double* HUx, double* HUy, double* t, do
     invalidate_mask(c);
     if ((rc = launch_begin(c, dt_cap)) || (rc = launch_mask(c)) || (rc = fused_ingest_hu(c, HUx, HUy)))
       return rc;
+    // the tile flags now describe this state: the forces phase visits only
+    // tiles with a wet cell in their blocks or rings (k_flist)
+    e = cudaMemsetAsync(&c->d_sc->mask_fresh, 1, sizeof(int), c->stream);
+    if (e != cudaSuccess) return cuda_check(c, e, "step_host mask");
     c->state_partial = 0;
     // k_step writes each updated cell into the caller's arrays as it goes
     // (PCIe writes overlapped with the step's arithmetic)

@@ -131,6 +131,7 @@ __device__ void mid_scalars(const Geo& G, const DevSrc* src, const double* ht, c
 __global__ void k_tau(Geo G, const DevSrc* src, const double* ht, const double* hq,
                       const double* wt, const double* wv, double* sig, StepScalars* sc,
                       double dt_cap, double global_speed, const double* gspeed) {
+  sc->mask_fresh = 0;  // k_flist has consumed it
   if (stopped(sc)) return;
   unsigned long long mb = sc->speed_bits;
   for (int q = 0; q < SPEED_SLOTS; ++q) mb = sc->speed_slots[q] > mb ? sc->speed_slots[q] : mb;
@@ -555,13 +556,28 @@ __global__ void k_flist(Geo G, ForcesArgs A) {
   const bool valid = t < nt;  // every lane reaches the warp-wide append
   StepScalars* sc = A.sc;
   const int tx = t % G.tiles_x, tr = t / G.tiles_x;
-  bool busy = valid && (!(A.do_mask && G.skip && sc->mask_valid) || A.tile_srcm[t] != 0);
-  for (int q = 0; q < 9 && valid && !busy; ++q) {
-    int x2 = tx + q % 3 - 1, y2 = tr + q / 3 - 1;
-    if (x2 >= 0 && x2 < G.tiles_x && y2 >= 0 && y2 < G.tiles_y)
-      busy = A.tile_prev[x2 + y2 * G.tiles_x] != 0;
+  // host-buffer step: k_mask/k_tiles already flagged this state, so a tile
+  // whose blocks have no wet cell in their interiors or rings (its forces
+  // region is dry) is skipped outright, its block counts zero
+  const bool fresh = A.do_mask && G.skip && sc->mask_fresh;
+  bool busy;
+  if (fresh) {
+    busy = valid && (A.tile_act[t] != 0 || A.tile_srcm[t] != 0);
+  } else {
+    busy = valid && (!(A.do_mask && G.skip && sc->mask_valid) || A.tile_srcm[t] != 0);
+    for (int q = 0; q < 9 && valid && !busy; ++q) {
+      int x2 = tx + q % 3 - 1, y2 = tr + q / 3 - 1;
+      if (x2 >= 0 && x2 < G.tiles_x && y2 >= 0 && y2 < G.tiles_y)
+        busy = A.tile_prev[x2 + y2 * G.tiles_x] != 0;
+    }
   }
-  if (valid && !busy) A.tile_act[t] = 0;
+  if (valid && !busy) {
+    A.tile_act[t] = 0;
+    if (fresh) {
+      A.cnt_part[5 * (size_t)t + 3] = 0.0;
+      A.cnt_part[5 * (size_t)t + 4] = 0.0;
+    }
+  }
   append_ordered(A.list, &sc->list_n[0], busy, t);
 }
 

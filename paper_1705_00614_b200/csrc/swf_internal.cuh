@@ -41,6 +41,8 @@ struct StepScalars {
   double deficit, srcvol, outflow;  // this step's diagnostics (volumes)
   double speed_local;               // strips: local max speed (phase 1 out)
   int mask_valid;  // the tile flags of the previous step describe the current state
+  int mask_fresh;  // != 0: k_mask/k_tiles just flagged the current state (host step);
+                   // cleared by k_tau
   int redo_n[2];   // tiles queued for the exact redo: [0] k_forces, [1] k_step
   int list_n[2];   // work-list lengths: [0] k_forces, [1] k_step
   int list_take[2];  // work-list cursors of the persistent grids

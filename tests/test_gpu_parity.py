@@ -372,6 +372,44 @@ def test_pinned_host_step_sparse_ingest_matches_oracle(gpu_cls, oracle_built):
     assert_state_bitwise(out, cpu_state, "resident after pinned steps")
 
 
+def test_pinned_host_steps_follow_host_side_edits(gpu_cls, oracle_built):
+    """Between pinned host steps the caller edits its arrays anywhere: a
+    puddle poured on dry ground far from the flood, a wet patch drained.  The
+    forces phase of a host step visits only the tiles the fresh block mask
+    flags, so new water must be seen there and drained tiles skipped; state,
+    tau and the block counts stay identical to the oracle."""
+    import torch
+    from paper_1705_00614_b200.types import FlowState
+    sc = S.floodplain(256, 50.0)
+    st = sc.state.copy()
+    pin = lambda a: torch.from_numpy(a.copy()).pin_memory().numpy()
+    hs = FlowState(st.nx, st.ny, 0.0, pin(st.H), pin(st.HUx), pin(st.HUy))
+    cpu_state = st.copy()
+    g = make(gpu_cls, sc)
+    o = make(oracle_built.OracleStepper, sc)
+    H2 = hs.H.reshape(st.ny, st.nx)
+    dry = np.argwhere(H2 <= sc.params.eps_dry)
+    wet = np.argwhere(H2 > sc.params.eps_dry)
+    assert len(dry) and len(wet)
+    for k in range(8):
+        if k == 2:  # a puddle on dry ground (a 3x3 patch around a dry cell)
+            j, i = dry[len(dry) // 3]
+            for a in (hs, cpu_state):
+                a.H.reshape(st.ny, st.nx)[max(j - 1, 0):j + 2, max(i - 1, 0):i + 2] += 0.5
+        if k == 5:  # drain a wet patch
+            j, i = wet[len(wet) // 2]
+            for a in (hs, cpu_state):
+                sl = (slice(max(j - 8, 0), j + 8), slice(max(i - 8, 0), i + 8))
+                a.H.reshape(st.ny, st.nx)[sl] = 0.0
+                a.HUx.reshape(st.ny, st.nx)[sl] = 0.0
+                a.HUy.reshape(st.ny, st.nx)[sl] = 0.0
+        ia = g.step(hs)
+        ib = o.step(cpu_state)
+        assert ia.tau == ib.tau, k
+        assert (ia.lagrangian_blocks, ia.flux_blocks) == (ib.lagrangian_blocks, ib.flux_blocks), k
+    assert_state_bitwise(hs, cpu_state, "pinned steps with host-side edits")
+
+
 def test_speculative_division_redo_path_is_exact(gpu_cls, oracle_built):
     """Momenta in the subnormal range make the kernels' speculative divisions
     reject; those tiles are recomputed by the exact redo launches and the
