@@ -404,8 +404,12 @@ __device__ __forceinline__ void forces_tile(const Geo& G, const ForcesArgs& A, c
   // One warp per block: interior cells and the clamped one-cell ring
   // (corners included, block.cpp:36-56) counted with ballots; no atomics on
   // global counters — the per-tile counts go to the diagnostics partials.
+  // K1 runs on the first min(nbt, 8) warps while the others convert the
+  // region to eta/velocity (independent: K1 reads only the wet flags)
+  const int nbt = (BX / G.bs) * (BY / G.bs);
+  const int k1w = mask_tile ? min(nbt, NTHR / 32) : 0;
   if (mask_tile) {
-    const int bs = G.bs, nbxt = BX / bs, nbyt = BY / bs, nbt = nbxt * nbyt;
+    const int bs = G.bs, nbxt = BX / bs;
     const int rend = min(rr0 + BY, G.r1);
     const int lane = tid & 31, warp = tid >> 5;
     for (int blk = warp; blk < nbt; blk += NTHR / 32) {
@@ -455,30 +459,32 @@ __device__ __forceinline__ void forces_tile(const Geo& G, const ForcesArgs& A, c
         if (f) atomicAdd(&s_cnt[1], 1);
       }
     }
-    __syncthreads();
-    if (tid == 0) {
-      int t = tx + tr * G.tiles_x;
-      A.tile_act[t] = G.skip ? ((s_cnt[0] ? 1 : 0) | (s_cnt[1] ? 2 : 0)) : 3;
-      A.cnt_part[5 * (size_t)t + 3] = s_cnt[0];
-      A.cnt_part[5 * (size_t)t + 4] = s_cnt[1];
-    }
   }
-  if (!anywet) return;
 
   // ---- region momentum -> eta, velocity ---------------------------------------
-  for (int c = tid; c < AREG; c += NTHR) {  // pointwise, in place (same c)
-    double d = s_d[c];
-    double e = d + s_e[c], u = 0.0, v = 0.0;
-    if (d > P.eps) {
-      Recip Rd = recip_of(d);
-      u = rdiv(s_u[c], Rd, SP);
-      v = rdiv(s_v[c], Rd, SP);
+  const int vt0 = k1w < NTHR / 32 ? 32 * k1w : 0;  // first thread of the velocity pass
+  if (anywet && tid >= vt0) {
+    for (int c = tid - vt0; c < AREG; c += NTHR - vt0) {  // pointwise, in place (same c)
+      double d = s_d[c];
+      double e = d + s_e[c], u = 0.0, v = 0.0;
+      if (d > P.eps) {
+        Recip Rd = recip_of(d);
+        u = rdiv(s_u[c], Rd, SP);
+        v = rdiv(s_v[c], Rd, SP);
+      }
+      s_e[c] = e;
+      s_u[c] = u;
+      s_v[c] = v;
     }
-    s_e[c] = e;
-    s_u[c] = u;
-    s_v[c] = v;
   }
   __syncthreads();
+  if (mask_tile && tid == 0) {
+    int t = tx + tr * G.tiles_x;
+    A.tile_act[t] = G.skip ? ((s_cnt[0] ? 1 : 0) | (s_cnt[1] ? 2 : 0)) : 3;
+    A.cnt_part[5 * (size_t)t + 3] = s_cnt[0];
+    A.cnt_part[5 * (size_t)t + 4] = s_cnt[1];
+  }
+  if (!anywet) return;
 
   // ---- K2 forces + K3 speed on wet cells ------------------------------------
   double m = 0.0;
