@@ -202,7 +202,7 @@ def reference_arm(args):
     v, cores, kind, sample, per_step = cpu_reference(args.config, args.warmup, args.steps)
     line = {"metric": "cell-updates/sec (Mcells/s)", "value": round(v, 3), "unit": "Mcells/s",
             "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.config} (bounded sample on host CPU)", "grid": args.config},
             "cpu_baseline": {"value": round(v, 3), "unit": "Mcells/s", "cores": cores,
@@ -307,7 +307,7 @@ def b200_single(args):
         # the same rate over the cells of flux-active blocks
         "value_active": round(n_act * K / (ms * 1e-3) / 1e6, 3),
         "n_gpus": 1, "steps": K, "warmup": args.warmup, "ms_per_step": round(ms / K, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generator, scenarios.py)",
         "config": {"workload": f"{sc.name} {sc.terrain.nx}x{sc.terrain.ny} h={sc.terrain.h} m, " + (
                        "all physics (Manning field, wind, Coriolis, viscosity, 3 sources, open east edge)"
