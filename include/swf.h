@@ -221,6 +221,10 @@ int swf_dev_rdiv(int n, const double* ab, double* out);
 /* the speculative form the fused kernels use: out = n x {q, accepted}; an
  * accepted q must equal a/b bit for bit (rejected items are redone exactly). */
 int swf_dev_rdiv_spec(int n, const double* ab, double* out);
+/* the square root of the fused kernels: out = n x {q, accepted}; an accepted
+ * q must equal the IEEE sqrt(x) bit for bit (the fast path without its slow
+ * branch when built with SWF_SPEC_SQRT, else sqrt itself, always accepted). */
+int swf_dev_sqrt_spec(int n, const double* x, double* out);
 /* the libm-compatible cube root used by friction (forcing.hpp:81). */
 int swf_dev_cbrt(int n, const double* x, double* y);
 /* bottom_friction, forcing.cpp:26-28: in = n x {ux,uy,H}, out = n x {fx,fy}. */

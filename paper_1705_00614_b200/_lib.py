@@ -60,6 +60,7 @@ def declare(lib):
     _sig(lib, "swf_dev_cbrt", I, I, PD, PD)
     _sig(lib, "swf_dev_rdiv", I, I, PD, PD)
     _sig(lib, "swf_dev_rdiv_spec", I, I, PD, PD)
+    _sig(lib, "swf_dev_sqrt_spec", I, I, PD, PD)
     _sig(lib, "swf_dev_bottom_friction", I, I, PD, D, D, PD)
     _sig(lib, "swf_strip_phase1", I, P, D, PD)
     _sig(lib, "swf_strip_phase2", I, P, D, D, PN)

@@ -909,6 +909,16 @@ __global__ void k_rdiv_spec(int n, const double* in, double* out) {
   out[2 * (size_t)i + 1] = ok ? 1.0 : 0.0;
 }
 
+// speculative square root: out[2i] = ssqrt(x, &ok), out[2i+1] = accepted,
+// checked against the IEEE sqrt by the test
+__global__ void k_sqrt_spec(int n, const double* x, double* out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  bool ok = true;
+  out[2 * (size_t)i] = ssqrt(x[i], &ok);
+  out[2 * (size_t)i + 1] = ok ? 1.0 : 0.0;
+}
+
 __global__ void k_cbrt(int n, const double* x, double* y) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) y[i] = glibc_cbrt(x[i]);
@@ -959,6 +969,12 @@ int swf_dev_rdiv(int n, const double* ab, double* out) {
 int swf_dev_rdiv_spec(int n, const double* ab, double* out) {
   return run_kat(2 * (size_t)n, ab, 2 * (size_t)n, out, [&](double* di, double* dout) {
     k_rdiv_spec<<<(n + 255) / 256, 256>>>(n, di, dout);
+  });
+}
+
+int swf_dev_sqrt_spec(int n, const double* x, double* out) {
+  return run_kat((size_t)n, x, 2 * (size_t)n, out, [&](double* di, double* dout) {
+    k_sqrt_spec<<<(n + 255) / 256, 256>>>(n, di, dout);
   });
 }
 

@@ -509,7 +509,7 @@ __device__ __forceinline__ void forces_tile(const Geo& G, const ForcesArgs& A, c
                              svy, SP);
     A.fpx[k] = o.fx - o.frx;
     A.fpy[k] = o.fy - o.fry;
-    m = cfl_speed(m, d, ux, uy, o.fx, o.fy, P.g, P.h);
+    m = cfl_speed(m, d, ux, uy, o.fx, o.fy, P.g, P.h, SP);
   }
   unsigned long long bits = dbits(m);
 #pragma unroll
@@ -753,11 +753,12 @@ __device__ __forceinline__ SideState side_from_slopes(double eta, double un, dou
 }
 
 __device__ __forceinline__ FaceRec face_from_sides(bool wetA, bool wetB, const SideState& L,
-                                                   const SideState& R, double g) {
+                                                   const SideState& R, double g,
+                                                   bool* ok = nullptr) {
   FaceRec rec;
   rec.fm = rec.fnl = rec.fnr = rec.ft = 0.0;
   if (!wetA && !wetB) return rec;
-  FaceFlux F = hll_face_flux(L.hs, L.un, L.ut, R.hs, R.un, R.ut, g);
+  FaceFlux F = hll_face_flux(L.hs, L.un, L.ut, R.hs, R.un, R.ut, g, ok);
   rec.fm = F.fm;
   rec.ft = F.ft;
   rec.fnl = (F.fn - ((0.5 * g) * L.hs) * L.hs) + ((0.5 * g) * L.hcell) * L.hcell;
@@ -1039,7 +1040,7 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
                                   R[F_V * RREG + sa + 1], R[F_SX * RREG + sa + 1], bB, q, face_m,
                                   bf);
           }
-          rec = face_from_sides(wetA, wetB, L, Rr, P.g);
+          rec = face_from_sides(wetA, wetB, L, Rr, P.g, SP);
           if (!face_finite(rec)) {
             unsigned long long key = fused_flux_key(G, A.bflag, 0, jg, f);
             my_err = key < my_err ? key : my_err;
@@ -1140,7 +1141,7 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
                                   R[F_U * RREG + sa + RX], R[F_SY * RREG + sa + RX], bB, q,
                                   face_m, bf);
           }
-          rec = face_from_sides(wetA, wetB, L, Rr, P.g);
+          rec = face_from_sides(wetA, wetB, L, Rr, P.g, SP);
           if (!face_finite(rec)) {
             unsigned long long key = fused_flux_key(G, A.bflag, 1, i, jf);
             my_err = key < my_err ? key : my_err;

@@ -96,6 +96,30 @@ def test_device_rdiv_matches_division():
     assert acc[z].all()
 
 
+def test_device_sqrt_spec():
+    """The kernels' square root (speculative when built with SWF_SPEC_SQRT):
+    every accepted result is the IEEE sqrt bit for bit; zeros and normal
+    operands are accepted, tiny/denormal/negative/special ones are not."""
+    from paper_1705_00614_b200._lib import lib
+    from paper_1705_00614_b200 import _abi as A
+    rng = np.random.default_rng(12)
+    n = 400000
+    x = np.concatenate([2.0 ** rng.uniform(-1074, 1024, n),
+                        rng.uniform(0, 1e4, n), rng.uniform(0.5, 2.0, n),
+                        np.nextafter(2.0 ** rng.integers(-1022, 1023, n), np.inf),
+                        -rng.uniform(0, 10, 1000),
+                        [0.0, -0.0, np.inf, -np.inf, np.nan, 5e-324, 2.0 ** -970,
+                         np.nextafter(2.0 ** -970, 0), 1.7976931348623157e308, 1.0, 4.0]])
+    out = np.empty((x.size, 2))
+    assert lib().swf_dev_sqrt_spec(x.size, A.dptr(x), A.dptr(out)) == 0
+    acc = out[:, 1] == 1.0
+    with np.errstate(all="ignore"):
+        ref = np.sqrt(x)
+    assert_bitwise(out[acc, 0], ref[acc], "accepted sqrt vs IEEE")
+    normal = (x >= 2.0 ** -970) & np.isfinite(x)
+    assert acc[normal].all() and acc[x == 0].all()
+
+
 def test_device_friction_known_answer():
     from paper_1705_00614_b200.stepper import bottom_friction_device
     f = bottom_friction_device(np.array([[1.0, 0.0]]), np.array([1.0]), 9.81, 0.02)
