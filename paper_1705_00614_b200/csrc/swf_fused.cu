@@ -406,21 +406,22 @@ __device__ __forceinline__ void forces_tile(const Geo& G, const ForcesArgs& A, c
   // global counters — the per-tile counts go to the diagnostics partials.
   // K1 runs on the first min(nbt, 8) warps while the others convert the
   // region to eta/velocity (independent: K1 reads only the wet flags)
-  const int nbt = (BX / G.bs) * (BY / G.bs);
+  // (the mask is fused only when bs divides 16: a power of two, so shifts)
+  const int lgb = __ffs(G.bs) - 1;
+  const int nbt = mask_tile ? (BX >> lgb) * (BY >> lgb) : 0;
   const int k1w = mask_tile ? min(nbt, NTHR / 32) : 0;
   if (mask_tile) {
-    const int bs = G.bs, nbxt = BX / bs;
+    const int bs = G.bs, lgx = 5 - lgb, nbxt = BX >> lgb;  // BX = 32 = 2^5
     const int rend = min(rr0 + BY, G.r1);
     const int lane = tid & 31, warp = tid >> 5;
     for (int blk = warp; blk < nbt; blk += NTHR / 32) {
-      int bx = blk % nbxt, by = blk / nbxt;
+      int bx = blk & (nbxt - 1), by = blk >> lgx;
       int bi0 = i0 + bx * bs, br0 = rr0 + by * bs;  // block origin (global col, local row)
       if (bi0 >= G.nx || br0 >= rend) continue;
       int bi1 = min(bi0 + bs - 1, G.nx - 1), br1 = min(br0 + bs - 1, rend - 1);
       int wdt = bi1 - bi0 + 1, hgt = br1 - br0 + 1;
       int in = 0, ring = 0;
-      // bs is a power of two (it divides 16): shifts instead of divisions
-      const int lg = __ffs(bs) - 1;
+      const int lg = lgb;
       for (int p = lane; p < bs * bs; p += 32) {
         int px = p & (bs - 1), py = p >> lg;
         if (px < wdt && py < hgt)
@@ -450,7 +451,7 @@ __device__ __forceinline__ void forces_tile(const Geo& G, const ForcesArgs& A, c
         ring += __shfl_xor_sync(0xffffffffu, ring, o);
       }
       if (lane == 0) {
-        int lb = (bi0 / bs) + ((G.jg0 + br0) / bs - G.bj0) * G.nbx;
+        int lb = (bi0 >> lgb) + (((G.jg0 + br0) >> lgb) - G.bj0) * G.nbx;
         A.interior[lb] = in;
         A.halo[lb] = ring;
         bool l = in > 0, f = l || ring > 0;
@@ -774,6 +775,7 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
   double* FB = SL + 3 * NSL;              // 4 x NFC faces (fm, fnl, fnr, ft)
   __shared__ double s_red[3][STHR / 32];
   __shared__ unsigned char s_bf[MAXBF];
+  __shared__ unsigned short s_bcol[BX], s_brow[BY];  // B-block column / row of each tile column / row
   const PhysConst& P = G.P;  // reciprocals refined at context creation (fused_prepare)
   StepScalars* sc = A.sc;
   if (__syncthreads_or(stopped(sc))) return;
@@ -821,6 +823,9 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
   const bool bf_staged = nbi * nbj <= MAXBF;
   if (bf_staged && tid < nbi * nbj)
     s_bf[tid] = A.bflag[(bi_lo + tid % nbi) + (bj_lo + tid / nbi - G.bj0) * G.nbx];
+  // the block indices phase 5 needs per cell, one division per column / row
+  if (tid >= STHR - BX) s_bcol[tid - (STHR - BX)] = (i0 + tid - (STHR - BX)) / G.bs;
+  else if (tid >= STHR - BX - BY) s_brow[tid - (STHR - BX - BY)] = (G.jg0 + r0 + tid - (STHR - BX - BY)) / G.bs;
   const int nsrc = G.nsrc;
   const double* sig_n = A.sig;
   const double* sig_m = A.sig + nsrc;
@@ -1181,8 +1186,9 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
     int jg = G.jg0 + r;
     int s = (x + 2) + (y + 2) * RX;
     size_t k = (size_t)i + (size_t)r * nx;
-    unsigned char bfl = bf_staged ? s_bf[(i / G.bs - bi_lo) + (jg / G.bs - bj_lo) * nbi]
-                                  : A.bflag[i / G.bs + (jg / G.bs - G.bj0) * G.nbx];
+    const int bc = s_bcol[x], br = s_brow[y];  // i / bs, jg / bs
+    unsigned char bfl = bf_staged ? s_bf[(bc - bi_lo) + (br - bj_lo) * nbi]
+                                  : A.bflag[bc + (br - G.bj0) * G.nbx];
     bool flux_on = !G.skip || (bfl & 2);
     if (!flux_on) {  // block skipped by the reference: state unchanged
       A.Ho[k] = Ht[m];  // no active cell in such a block: (Ht, Qx, Qy) = step-start state
