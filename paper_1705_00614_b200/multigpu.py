@@ -698,7 +698,11 @@ def bench_strips(args) -> Optional[dict]:
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
                      "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
                      "traffic": traffic["bytes_per_launch"] if traffic else None,
-                     "kernel": "k_step (fused K4..K8), per GPU", "peak_source": src},
+                     "kernel": "k_step (fused K4..K8), per GPU", "peak_source": src,
+                     # per-GPU kernel behaviour, from the committed one-GPU ncu capture
+                     "ncu": ({"fp64_pipe_pct": traffic["fp64_pipe_pct"],
+                              "issue_active_pct": traffic["issue_active_pct"],
+                              "source": traffic["source"]} if traffic else None)},
         "e2e": e2e,
         "gpu_launches": 12 * K,  # + split forces launches and the device speed for the allreduce
         "clocks": clk,
