@@ -1330,15 +1330,22 @@ __global__ void k_reduce(const double* part, int ntiles, double* red, const Step
   if (threadIdx.x < NPART) red[NPART * blockIdx.x + threadIdx.x] = s[threadIdx.x][0];
 }
 
+// One CTA: the partials are staged in shared memory by all threads (one
+// round of loads instead of nred dependent ones), then thread 0 sums them in
+// the same fixed order as ever.
 __global__ void k_finish(const double* red, int nred, StepScalars* sc, double area, double h,
                          int counts_from_tiles) {
+  __shared__ double s_red[NPART * RED_CTAS];
   if (stopped(sc)) {
-    if (sc->fail_step < 0) sc->fail_step = sc->steps_done;
+    if (threadIdx.x == 0 && sc->fail_step < 0) sc->fail_step = sc->steps_done;
     return;
   }
+  for (int i = threadIdx.x; i < NPART * nred; i += blockDim.x) s_red[i] = red[i];
+  __syncthreads();
+  if (threadIdx.x != 0) return;
   double w[NPART] = {0.0, 0.0, 0.0, 0.0, 0.0};
   for (int t = 0; t < nred; ++t)
-    for (int q = 0; q < NPART; ++q) w[q] += red[NPART * t + q];
+    for (int q = 0; q < NPART; ++q) w[q] += s_red[NPART * t + q];
   sc->deficit = w[0] * area;
   sc->srcvol = w[1] * area;
   sc->outflow = (w[2] * sc->tau) * h;
@@ -1551,7 +1558,7 @@ int fused_enqueue_phase2(swf_ctx* c, double dt_cap, double global_speed, const d
   ev(c, 4);
   double* red = c->d_part + NPART * (size_t)(nt > 0 ? nt : 1);
   k_reduce<<<RED_CTAS, NTHR, 0, c->stream>>>(c->d_part, nt, red, c->d_sc);
-  k_finish<<<1, 1, 0, c->stream>>>(red, RED_CTAS, c->d_sc, c->h * c->h, c->h,
+  k_finish<<<1, NTHR, 0, c->stream>>>(red, RED_CTAS, c->d_sc, c->h * c->h, c->h,
                                    mask_fused(G) ? 1 : 0);
   ev(c, 5);
   if (c->timing && c->tslots > 0) ++c->tstep;
