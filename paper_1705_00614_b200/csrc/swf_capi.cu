@@ -33,7 +33,11 @@ int cuda_check(swf_ctx* c, cudaError_t e, const char* what) {
 size_t local_cells(const swf_ctx* c) { return (size_t)c->geo.nx * (size_t)c->geo.rows; }
 
 void invalidate_mask(swf_ctx* c) {
-  if (c->d_sc) cudaMemsetAsync(&c->d_sc->mask_valid, 0, sizeof(int), c->stream);
+  if (!c->d_sc) return;
+  cudaMemsetAsync(&c->d_sc->mask_valid, 0, sizeof(int), c->stream);
+  // a host step that failed before k_tau may have left mask_fresh set: the
+  // flags it refers to do not describe a newly uploaded state
+  cudaMemsetAsync(&c->d_sc->mask_fresh, 0, sizeof(int), c->stream);
 }
 
 void fill_block_counts(const swf_ctx* c, const StepScalars* sc, swf_step_info* info) {
