@@ -58,12 +58,39 @@ def build_host(force=False):
         cmd = [_cxx(), "-std=c++20", "-O2", "-fPIC", "-shared", "-I", INCLUDE] + HOST_SRCS + \
             ["-o", HOST_OUT, "-L", HERE, "-lswflood_cuda", "-Wl,-rpath,$ORIGIN"]
         subprocess.run(cmd, check=True)
+    build_pybind(force, hdrs)
     if force or not os.path.exists(CLI_OUT) or any(
             os.path.getmtime(d) > os.path.getmtime(CLI_OUT) for d in [CLI_SRC, HOST_OUT] + hdrs):
         cmd = [_cxx(), "-std=c++20", "-O2", "-I", INCLUDE, CLI_SRC, "-o", CLI_OUT, "-L", HERE,
                "-lswflood_b200", "-lswflood_cuda", "-Wl,-rpath,$ORIGIN"]
         subprocess.run(cmd, check=True)
     return HOST_OUT
+
+
+PYBIND_SRC = os.path.join(HERE, "host", "swflood_pybind.cpp")
+
+
+def pybind_out():
+    import sysconfig
+    return os.path.join(HERE, "swflood_native" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def build_pybind(force=False, hdrs=()):
+    """pybind11 module `swflood_native` over libswflood_b200.so (the
+    reference's missing bindings/ directory); skipped if pybind11 is absent."""
+    try:
+        import pybind11
+    except ImportError:
+        return None
+    import sysconfig
+    out = pybind_out()
+    deps = [PYBIND_SRC, HOST_OUT] + list(hdrs)
+    if force or not os.path.exists(out) or any(os.path.getmtime(d) > os.path.getmtime(out) for d in deps):
+        cmd = [_cxx(), "-std=c++20", "-O2", "-fPIC", "-shared", "-I", INCLUDE,
+               "-I", pybind11.get_include(), "-I", sysconfig.get_paths()["include"], PYBIND_SRC,
+               "-o", out, "-L", HERE, "-lswflood_b200", "-lswflood_cuda", "-Wl,-rpath,$ORIGIN"]
+        subprocess.run(cmd, check=True)
+    return out
 
 
 def build(force=False, verbose=False):

@@ -1,0 +1,103 @@
+"""The pybind11 module `swflood_native` (host/swflood_pybind.cpp): the
+reference's C++ API (grid.hpp, sources.hpp, stepper.hpp) from Python, over
+the C++ drop-in and the CUDA library.  CPU: types, numpy views, error
+mapping, no CPU fallback.  GPU: steps bit-identical to the oracle."""
+import numpy as np
+import pytest
+
+from conftest import has_gpu
+from helpers import assert_state_bitwise, make
+from paper_1705_00614_b200 import scenarios as S
+
+sw = pytest.importorskip("paper_1705_00614_b200.swflood_native")
+
+
+def to_native(sc):
+    """A scenario (paper_1705_00614_b200.types) as swflood_native objects."""
+    T = sw.Terrain(sc.terrain.nx, sc.terrain.ny, sc.terrain.h, sc.terrain.x0, sc.terrain.y0,
+                   sc.terrain.b)
+    P = sw.PhysicalParams()
+    for f in ("g", "n_manning", "nu", "omega_z", "c_a", "rho_air", "rho_water", "eps_dry"):
+        setattr(P, f, getattr(sc.params, f))
+    if sc.params.n_field is not None:
+        P.n_field = sc.params.n_field
+    K = sw.TimestepControl(sc.control.courant, sc.control.dt_max, sc.control.dt_min)
+    O = sw.StepperOptions()
+    O.block_size = sc.options.block_size
+    O.skip_dry_blocks = sc.options.skip_dry_blocks
+    bc = sw.BoundaryConfig()
+    for e in ("west", "east", "south", "north"):
+        setattr(bc, e, sw.EdgeKind(int(getattr(sc.options.boundaries, e))))
+    O.boundaries = bc
+    W = sw.WindForcing([sw.WindSample(s.t, s.wx, s.wy) for s in sc.wind.series])
+    srcs = []
+    for s in sc.sources:
+        n = sw.SourceSpec()
+        n.kind = sw.SourceSpec.Kind(int(s.kind))
+        n.name = s.name
+        n.cells = sw.CellRect(s.cells.i0, s.cells.j0, s.cells.i1, s.cells.j1)
+        n.hydrograph = [sw.HydrographSample(h.t, h.q) for h in s.hydrograph]
+        n.rate = s.rate
+        n.source_velocity = sw.Vec2(s.source_velocity.x, s.source_velocity.y)
+        srcs.append(n)
+    st = sw.FlowState.dry(T)
+    st.H[:], st.HUx[:], st.HUy[:] = sc.state.H, sc.state.HUx, sc.state.HUy
+    st.t = sc.state.t
+    return T, P, K, O, W, srcs, st
+
+
+def test_types_and_views():
+    sc = S.floodplain(64, 50.0)
+    T, P, K, O, W, srcs, st = to_native(sc)
+    assert T.cells() == 64 * 64 and T.idx(3, 2) == 2 * 64 + 3
+    np.testing.assert_array_equal(T.b, sc.terrain.b)
+    v = st.H
+    v[0] = 7.0  # a view onto the C++ vector, not a copy
+    assert st.H[0] == 7.0
+    assert len(W.series) == len(sc.wind.series) and len(srcs) == len(sc.sources)
+    assert srcs[0].discharge_at(0.0) == sc.sources[0].discharge_at(0.0)
+
+
+def test_config_errors_and_no_cpu_fallback():
+    T = sw.Terrain(4, 4, 1.0, 0.0, 0.0, np.zeros(16))
+    with pytest.raises(sw.ConfigError, match="Courant"):
+        sw.CsphTvdStepper(T, sw.PhysicalParams(), sw.TimestepControl(courant=1.5))
+    bad = sw.Terrain(4, 4, 1.0, 0.0, 0.0, np.zeros(15))
+    with pytest.raises(sw.ConfigError, match="bed array size mismatch"):
+        sw.CsphTvdStepper(bad, sw.PhysicalParams(), sw.TimestepControl())
+    if not has_gpu():
+        with pytest.raises(RuntimeError, match="CUDA|device"):
+            sw.CsphTvdStepper(T, sw.PhysicalParams(), sw.TimestepControl())
+
+
+@pytest.mark.gpu
+def test_native_steps_match_oracle(oracle_built):
+    sc = S.floodplain(96, 50.0)
+    T, P, K, O, W, srcs, st = to_native(sc)
+    g = sw.CsphTvdStepper(T, P, K, O)
+    g.set_wind(W)
+    g.set_sources(srcs)
+    o = make(oracle_built.OracleStepper, sc)
+    ref = sc.state.copy()
+    for _ in range(10):
+        a = g.step(st)
+        b = o.step(ref)
+        assert a.tau == b.tau
+        assert (a.lagrangian_blocks, a.flux_blocks) == (b.lagrangian_blocks, b.flux_blocks)
+    out = sc.state.copy()
+    out.H[:], out.HUx[:], out.HUy[:], out.t = st.H, st.HUx, st.HUy, st.t
+    assert_state_bitwise(out, ref, "pybind steps")
+
+
+@pytest.mark.gpu
+def test_native_numerical_error_leaves_state():
+    T = sw.Terrain(64, 8, 1.0, 0.0, 0.0, np.zeros(64 * 8))
+    st = sw.FlowState.dry(T)
+    st.H[:] = 1.0
+    st.HUx[:] = 50.0  # CFL tau ~ 0.5 * 1 / 53 m/s falls below dt_min = 0.05
+    g = sw.CsphTvdStepper(T, sw.PhysicalParams(), sw.TimestepControl(0.5, 10.0, 0.05))
+    before = st.H.copy(), st.HUx.copy()
+    with pytest.raises(sw.NumericalError, match="abort floor"):
+        g.step(st)
+    np.testing.assert_array_equal(st.H, before[0])
+    np.testing.assert_array_equal(st.HUx, before[1])
