@@ -234,8 +234,9 @@ int swf_dev_bottom_friction(int n, const double* in, double g, double n_manning,
 /* ---- row-strip decomposition (multi-GPU) ---- */
 /* A strip context owns global rows [j0, j1) of an nx x ny_global domain and
  * keeps SWF_HALO ghost rows on each interior side.  terrain->ny must equal
- * ny_global and terrain->b the whole global bed (only the strip + ghost rows
- * are copied).  device selects the CUDA device. */
+ * ny_global; terrain->b and params->n_field point at the strip's window, the
+ * global rows [j0 - ghosts, j1 + ghosts) (swf_strip_rows reports the ghost
+ * counts).  device selects the CUDA device. */
 #define SWF_HALO 3
 int swf_create_strip(const swf_terrain* terrain, const swf_params* params,
                      const swf_control* control, const swf_options* options,
@@ -293,6 +294,25 @@ int swf_strip_set_peer(swf_ctx* ctx, int side, double* const* bufs6, int peer_ro
 /* Owned global rows [j0, j1) and the ghost-row counts below/above. */
 int swf_strip_rows(const swf_ctx* ctx, int* j0, int* j1, int* ghost_lo,
                    int* ghost_hi);
+
+/* ---- single-process multi-GPU group (StepperOptions::devices > 1) ----
+ * Replaces CsphTvdStepper's internal one-stream-per-GPU model of SURVEY.md
+ * §8b for callers that drive every GPU from one process: n strip contexts
+ * (swf_create_strip, ascending adjacent rows, each on its own device, devices
+ * may repeat).  The group enables peer access, links neighbours so every
+ * k_step stores its boundary rows into the neighbours' ghost rows, orders the
+ * devices' streams with events (no host synchronisation inside a run) and
+ * max-reduces the CFL speed on the first strip's device.  The strips' ghost
+ * rows must be current when a run starts (upload whole windows).  All strips
+ * commit the same number of steps (the fewest any completed); info = the
+ * group's last step (block counts and volumes summed over the strips). */
+typedef struct swf_group swf_group;
+int swf_group_create(swf_ctx* const* strips, int n, swf_group** out);
+int swf_group_run(swf_group* g, int nsteps, double dt_cap, int* done, swf_step_info* last);
+const char* swf_group_last_error(const swf_group* g);
+void swf_group_destroy(swf_group* g);
+/* number of CUDA devices visible to the process */
+int swf_device_count(int* n);
 
 /* ---- two-level nested grids (SPEC.md [MODULE] nesting) ----
  * The reference ships no code for this module; these entry

@@ -175,6 +175,11 @@ struct StepperOptions {
   bool skip_dry_blocks = true;
   int workers = 1;  // accepted, unused on the GPU
   BoundaryConfig boundaries;
+  // GPUs this stepper drives from the calling process (row strips, one per
+  // device, linked by peer access).  > 1 supports step(),
+  // set_wind/set_sources and control()/options(); the stage API and the
+  // scratch accessors need 1.  Fixed at construction.
+  int devices = 1;
 };
 
 class CsphTvdStepper {
@@ -223,11 +228,14 @@ class CsphTvdStepper {
   double last_source_volume() const;
   double last_boundary_outflow() const;
 
-  swf_ctx* native() const { return ctx_; }  // the C-ABI context (resident API)
+  swf_ctx* native() const { return ctx_; }  // the C-ABI context (resident API; strip 0 if devices > 1)
 
  private:
   void check(int rc) const;
   void sync_config() const;
+  void single(const char* what) const;
+  std::vector<swf_ctx*> contexts() const;
+  StepInfo step_group(FlowState& state, double dt_cap);
   std::span<const double> scratch(int which, std::vector<double>& buf) const;
 
   const Terrain* terrain_;
@@ -235,6 +243,9 @@ class CsphTvdStepper {
   TimestepControl ctl_;
   StepperOptions opt_;
   swf_ctx* ctx_ = nullptr;
+  std::vector<swf_ctx*> strips_;  // devices > 1: one strip context per device
+  swf_group* group_ = nullptr;
+  double group_vol_[3] = {0.0, 0.0, 0.0};
   mutable TimestepControl pushed_ctl_;
   mutable StepperOptions pushed_opt_;
   // host caches for the accessors (filled from the device on demand)

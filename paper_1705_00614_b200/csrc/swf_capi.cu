@@ -8,6 +8,7 @@
 // sm_100a kernels and fails with SWF_ECUDA when no device is usable.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -1193,6 +1194,259 @@ int swf_strip_rows(const swf_ctx* c, int* j0, int* j1, int* glo, int* ghi) {
   if (j1) *j1 = G.jg0 + G.r1;
   if (glo) *glo = G.r0;
   if (ghi) *ghi = G.rows - G.r1;
+  return SWF_OK;
+}
+
+int swf_device_count(int* n) {
+  int k = 0;
+  cudaError_t e = cudaGetDeviceCount(&k);
+  if (n) *n = e == cudaSuccess ? k : 0;
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return set_err(nullptr, SWF_ECUDA, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+  }
+  return SWF_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// single-process multi-GPU group (StepperOptions::devices > 1)
+// ---------------------------------------------------------------------------
+struct swf_group {
+  std::vector<swf_ctx*> s;        // strips, ascending rows
+  std::vector<double*> speed;     // per strip (its device): local CFL speed
+  std::vector<double*> gspeed;    // per strip (its device): the group maximum
+  double** d_in = nullptr;        // on strip 0's device: speed[] / gspeed[] pointers
+  double** d_out = nullptr;
+  std::vector<cudaEvent_t> ev_speed, ev_step;
+  cudaEvent_t ev_max = nullptr;
+  std::string err;
+};
+
+namespace {
+
+// the exact maximum of the strips' speeds (non-negative doubles), written to
+// every strip's device (peer stores)
+__global__ void k_group_max(double* const* in, double* const* out, int n) {
+  if (threadIdx.x != 0) return;
+  double m = 0.0;
+  for (int d = 0; d < n; ++d) m = in[d][0] > m ? in[d][0] : m;
+  for (int d = 0; d < n; ++d) out[d][0] = m;
+}
+
+int group_err(swf_group* g, int rc, const std::string& m) {
+  g->err = m;
+  g_err = m;
+  return rc;
+}
+
+int enable_peer(int a, int b) {
+  if (a == b) return SWF_OK;
+  int can = 0;
+  cudaDeviceCanAccessPeer(&can, a, b);
+  if (!can) return SWF_ECUDA;
+  cudaSetDevice(a);
+  cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    e = cudaSuccess;
+  }
+  return e == cudaSuccess ? SWF_OK : SWF_ECUDA;
+}
+
+}  // namespace
+
+extern "C" {
+
+void swf_group_destroy(swf_group* g) {
+  if (!g) return;
+  for (size_t d = 0; d < g->s.size(); ++d) {
+    cudaSetDevice(g->s[d]->device);
+    cudaStreamSynchronize(g->s[d]->stream);
+    for (int side = 0; side < 2; ++side) swf_strip_set_peer(g->s[d], side, nullptr, 0);
+    if (d < g->speed.size()) cudaFree(g->speed[d]);
+    if (d < g->gspeed.size()) cudaFree(g->gspeed[d]);
+    if (d < g->ev_speed.size()) cudaEventDestroy(g->ev_speed[d]);
+    if (d < g->ev_step.size()) cudaEventDestroy(g->ev_step[d]);
+  }
+  if (!g->s.empty()) {
+    cudaSetDevice(g->s[0]->device);
+    cudaFree(g->d_in);
+    cudaFree(g->d_out);
+    if (g->ev_max) cudaEventDestroy(g->ev_max);
+  }
+  delete g;
+}
+
+int swf_group_create(swf_ctx* const* strips, int n, swf_group** out) {
+  if (!out || !strips || n < 1) return set_err(nullptr, SWF_ECONFIG, "group: no strips");
+  *out = nullptr;
+  for (int d = 0; d < n; ++d) {
+    if (!strips[d]) return set_err(nullptr, SWF_ECONFIG, "group: null strip");
+    const Geo& G = strips[d]->geo;
+    if (d > 0) {
+      const Geo& P = strips[d - 1]->geo;
+      if (P.jg0 + P.r1 != G.jg0 + G.r0 || P.nx != G.nx || P.ny != G.ny)
+        return set_err(nullptr, SWF_ECONFIG, "group: strips must be adjacent rows of one grid");
+    }
+    if (strips[d]->mode != 0) return set_err(nullptr, SWF_ECONFIG, "group: strips need the fused path");
+  }
+  swf_group* g = new swf_group();
+  g->s.assign(strips, strips + n);
+  const int dev0 = strips[0]->device;
+  // peer access: every device with the first (the speed reduction) and with
+  // its neighbours (the halo stores)
+  for (int d = 0; d < n; ++d) {
+    int a = strips[d]->device;
+    int rc = enable_peer(dev0, a) | enable_peer(a, dev0);
+    if (d > 0) rc |= enable_peer(a, strips[d - 1]->device) | enable_peer(strips[d - 1]->device, a);
+    if (rc) {
+      swf_group_destroy(g);
+      return set_err(nullptr, SWF_ECUDA, "group: peer access between the devices is unavailable");
+    }
+  }
+  cudaError_t e = cudaSuccess;
+  g->speed.assign(n, nullptr);
+  g->gspeed.assign(n, nullptr);
+  g->ev_speed.assign(n, nullptr);
+  g->ev_step.assign(n, nullptr);
+  for (int d = 0; d < n && e == cudaSuccess; ++d) {
+    cudaSetDevice(strips[d]->device);
+    e = cudaMalloc(&g->speed[d], sizeof(double));
+    if (e == cudaSuccess) e = cudaMalloc(&g->gspeed[d], sizeof(double));
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g->ev_speed[d], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g->ev_step[d], cudaEventDisableTiming);
+  }
+  if (e == cudaSuccess) {
+    cudaSetDevice(dev0);
+    e = cudaMalloc(&g->d_in, n * sizeof(double*));
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_out, n * sizeof(double*));
+    if (e == cudaSuccess) e = cudaMemcpy(g->d_in, g->speed.data(), n * sizeof(double*), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(g->d_out, g->gspeed.data(), n * sizeof(double*), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g->ev_max, cudaEventDisableTiming);
+  }
+  if (e != cudaSuccess) {
+    std::string m = std::string("group setup: ") + cudaGetErrorString(e);
+    swf_group_destroy(g);
+    return set_err(nullptr, SWF_ECUDA, m);
+  }
+  // each k_step stores its boundary rows into the neighbours' ghost rows
+  for (int d = 0; d < n; ++d) {
+    for (int side = 0; side < 2; ++side) {
+      int nb = side == 0 ? d - 1 : d + 1;
+      if (nb < 0 || nb >= n) continue;
+      double* bufs[6];
+      swf_device_buffers(strips[nb], bufs);
+      int rc = swf_strip_set_peer(strips[d], side, bufs, strips[nb]->geo.jg0);
+      if (rc) {
+        std::string m = strips[d]->err;
+        swf_group_destroy(g);
+        return set_err(nullptr, rc, m);
+      }
+    }
+  }
+  *out = g;
+  return SWF_OK;
+}
+
+const char* swf_group_last_error(const swf_group* g) { return g ? g->err.c_str() : g_err.c_str(); }
+
+int swf_group_run(swf_group* g, int nsteps, double dt_cap, int* done, swf_step_info* last) {
+  if (!g) return set_err(nullptr, SWF_ECONFIG, "group: null");
+  if (done) *done = 0;
+  const int n = (int)g->s.size();
+  std::vector<int> cur0(n);
+  for (int d = 0; d < n; ++d) {
+    swf_ctx* c = g->s[d];
+    if (c->state_partial) return group_err(g, SWF_ECONFIG, "group: upload a state first");
+    if (c->cur != g->s[0]->cur) return group_err(g, SWF_ECONFIG, "group: strips out of step");
+    cudaSetDevice(c->device);
+    int rc = reset_counters(c);
+    if (rc) return group_err(g, rc, c->err);
+    cur0[d] = c->cur;
+  }
+  int rc = SWF_OK;
+  for (int k = 0; k < nsteps && !rc; ++k) {
+    // interior tile rows first (no ghost row read), on every device
+    for (int d = 0; d < n && !rc; ++d) {
+      cudaSetDevice(g->s[d]->device);
+      rc = fused_enqueue_phase1(g->s[d], dt_cap, 0);
+    }
+    // the ghost-dependent rows after the neighbours' previous k_step
+    for (int d = 0; d < n && !rc; ++d) {
+      swf_ctx* c = g->s[d];
+      cudaSetDevice(c->device);
+      if (k > 0)
+        for (int nb = d - 1; nb <= d + 1; nb += 2)
+          if (nb >= 0 && nb < n) cudaStreamWaitEvent(c->stream, g->ev_step[nb], 0);
+      rc = fused_enqueue_phase1(c, dt_cap, 1);
+      if (!rc) rc = fused_local_speed(c, g->speed[d]);
+      if (!rc) cudaEventRecord(g->ev_speed[d], c->stream);
+    }
+    if (rc) break;
+    swf_ctx* c0 = g->s[0];
+    cudaSetDevice(c0->device);
+    for (int d = 0; d < n; ++d) cudaStreamWaitEvent(c0->stream, g->ev_speed[d], 0);
+    k_group_max<<<1, 32, 0, c0->stream>>>(g->d_in, g->d_out, n);
+    cudaEventRecord(g->ev_max, c0->stream);
+    for (int d = 0; d < n && !rc; ++d) {
+      swf_ctx* c = g->s[d];
+      cudaSetDevice(c->device);
+      cudaStreamWaitEvent(c->stream, g->ev_max, 0);
+      rc = fused_enqueue_phase2(c, dt_cap, -1.0, g->gspeed[d]);
+      if (!rc) cudaEventRecord(g->ev_step[d], c->stream);
+    }
+  }
+  // every strip commits the steps all of them completed
+  int ok = nsteps, first_rc = rc, first = -1;
+  std::vector<int> rcs(n);
+  for (int d = 0; d < n; ++d) {
+    swf_ctx* c = g->s[d];
+    cudaSetDevice(c->device);
+    cudaError_t e = cudaStreamSynchronize(c->stream);
+    rcs[d] = e != cudaSuccess ? cuda_check(c, e, "group run") : check_device_error(c);
+    ok = std::min(ok, c->h_sc->steps_done);
+    if (rcs[d] && (first < 0 || (rcs[d] == SWF_ENUMERICAL && rcs[first] != SWF_ENUMERICAL))) first = d;
+  }
+  double t = 0.0;
+  for (int d = 0; d < n; ++d)
+    if (g->s[d]->h_sc->steps_done == ok) t = g->s[d]->h_sc->t;
+  for (int d = 0; d < n; ++d) {
+    swf_ctx* c = g->s[d];
+    cudaSetDevice(c->device);
+    if (c->h_sc->steps_done != ok) {  // discard the steps the others did not finish
+      c->h_sc->t = t;
+      cudaMemcpy(&c->d_sc->t, &t, sizeof(double), cudaMemcpyHostToDevice);
+      invalidate_mask(c);
+    }
+    c->cur = (cur0[d] + ok) & 1;
+    c->h_t = t;
+  }
+  if (done) *done = ok;
+  if (last && ok > 0) {
+    swf_step_info sum{};
+    long long flux_act = 0;
+    for (int d = 0; d < n; ++d) {
+      flux_act += g->s[d]->h_sc->flux_act;
+      swf_step_info a{};
+      fill_fused_info(g->s[d], &a);
+      if (d == 0) {
+        sum = a;
+      } else {
+        sum.lagrangian_blocks += a.lagrangian_blocks;
+        sum.flux_blocks += a.flux_blocks;
+        sum.total_blocks += a.total_blocks;
+        sum.clamp_deficit_volume += a.clamp_deficit_volume;
+        sum.source_volume += a.source_volume;
+        sum.boundary_outflow_volume += a.boundary_outflow_volume;
+      }
+    }
+    sum.active_fraction = sum.total_blocks ? (double)flux_act / sum.total_blocks : 0.0;
+    *last = sum;
+  }
+  if (first_rc) return group_err(g, first_rc, g->s[0]->err);
+  if (first >= 0) return group_err(g, rcs[first], g->s[first]->err);
   return SWF_OK;
 }
 

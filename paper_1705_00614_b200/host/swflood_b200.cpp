@@ -242,13 +242,65 @@ CsphTvdStepper::CsphTvdStepper(const Terrain& terrain, PhysicalParams params,
                params_.n_field.empty() ? nullptr : params_.n_field.data()};
   swf_control k = to_c(ctl_);
   swf_options o = to_c(opt_);
-  int rc = swf_create(&t, &p, &k, &o, &ctx_);
-  if (rc) throw_status(rc, swf_last_error(nullptr));
+  if (opt_.devices < 1) throw ConfigError("stepper: devices must be >= 1");
+  if (opt_.devices == 1) {
+    int rc = swf_create(&t, &p, &k, &o, &ctx_);
+    if (rc) throw_status(rc, swf_last_error(nullptr));
+  } else {
+    // row strips on block boundaries, one per device, windows of the global arrays
+    const int D = opt_.devices, bs = opt_.block_size, nby = (terrain.ny + bs - 1) / bs;
+    if (D > nby) throw ConfigError("stepper: more devices than block rows");
+    int ndev = 0;
+    int rc = swf_device_count(&ndev);
+    if (rc || ndev < 1) throw_status(rc ? rc : SWF_ECUDA, swf_last_error(nullptr));
+    for (int d = 0; d < D; ++d) {
+      int j0 = std::min(terrain.ny, (int)((long long)d * nby / D) * bs);
+      int j1 = std::min(terrain.ny, (int)((long long)(d + 1) * nby / D) * bs);
+      int w0 = std::max(0, j0 - SWF_HALO);
+      swf_terrain tw = t;
+      tw.b = terrain.b.data() + (size_t)w0 * terrain.nx;
+      swf_params pw = p;
+      if (pw.n_field) pw.n_field = params_.n_field.data() + (size_t)w0 * terrain.nx;
+      swf_ctx* c = nullptr;
+      rc = swf_create_strip(&tw, &pw, &k, &o, j0, j1, d % ndev, &c);
+      if (rc) {
+        std::string m = swf_last_error(nullptr);
+        for (swf_ctx* s : strips_) swf_destroy(s);
+        strips_.clear();
+        throw_status(rc, m.c_str());
+      }
+      strips_.push_back(c);
+    }
+    rc = swf_group_create(strips_.data(), D, &group_);
+    if (rc) {
+      std::string m = swf_last_error(nullptr);
+      for (swf_ctx* s : strips_) swf_destroy(s);
+      strips_.clear();
+      throw_status(rc, m.c_str());
+    }
+    ctx_ = strips_[0];
+  }
   pushed_ctl_ = ctl_;
   pushed_opt_ = opt_;
 }
 
-CsphTvdStepper::~CsphTvdStepper() { swf_destroy(ctx_); }
+CsphTvdStepper::~CsphTvdStepper() {
+  if (group_) {
+    swf_group_destroy(group_);
+    for (swf_ctx* s : strips_) swf_destroy(s);
+  } else {
+    swf_destroy(ctx_);
+  }
+}
+
+std::vector<swf_ctx*> CsphTvdStepper::contexts() const {
+  return group_ ? strips_ : std::vector<swf_ctx*>{ctx_};
+}
+
+void CsphTvdStepper::single(const char* what) const {
+  if (group_)
+    throw ConfigError(std::string("stepper: ") + what + " needs StepperOptions::devices == 1");
+}
 
 void CsphTvdStepper::check(int rc) const {
   if (rc) throw_status(rc, swf_last_error(ctx_));
@@ -257,12 +309,14 @@ void CsphTvdStepper::check(int rc) const {
 void CsphTvdStepper::sync_config() const {
   if (!same(ctl_, pushed_ctl_)) {
     swf_control k = to_c(ctl_);
-    check(swf_set_control(ctx_, &k));
+    for (swf_ctx* c : contexts())
+      if (int rc = swf_set_control(c, &k)) throw_status(rc, swf_last_error(c));
     pushed_ctl_ = ctl_;
   }
   if (!same(opt_, pushed_opt_)) {
     swf_options o = to_c(opt_);
-    check(swf_set_options(ctx_, &o));
+    for (swf_ctx* c : contexts())
+      if (int rc = swf_set_options(c, &o)) throw_status(rc, swf_last_error(c));
     pushed_opt_ = opt_;
   }
 }
@@ -275,7 +329,9 @@ void CsphTvdStepper::set_wind(WindForcing wind) {
     x.push_back(s.wx);
     y.push_back(s.wy);
   }
-  check(swf_set_wind(ctx_, (int)t.size(), t.data(), x.data(), y.data()));
+  for (swf_ctx* c : contexts())
+    if (int rc = swf_set_wind(c, (int)t.size(), t.data(), x.data(), y.data()))
+      throw_status(rc, swf_last_error(c));
 }
 
 void CsphTvdStepper::set_sources(std::vector<SourceSpec> sources) {
@@ -296,13 +352,15 @@ void CsphTvdStepper::set_sources(std::vector<SourceSpec> sources) {
                            ts.data(), qs.data(), s.rate, s.source_velocity.x,
                            s.source_velocity.y});
   }
-  check(swf_set_sources(ctx_, (int)v.size(), v.data()));
+  for (swf_ctx* c : contexts())
+    if (int rc = swf_set_sources(c, (int)v.size(), v.data())) throw_status(rc, swf_last_error(c));
 }
 
 StepInfo CsphTvdStepper::step(FlowState& state, double dt_cap) {
   if (state.nx != terrain_->nx || state.ny != terrain_->ny)
     throw ConfigError("stepper: state does not match the terrain grid");
   sync_config();
+  if (group_) return step_group(state, dt_cap);
   swf_step_info ci{};
   check(swf_step_host(ctx_, state.H.data(), state.HUx.data(), state.HUy.data(), &state.t, dt_cap,
                       &ci));
@@ -322,7 +380,54 @@ StepInfo CsphTvdStepper::step(FlowState& state, double dt_cap) {
   return s;
 }
 
+// devices > 1: every strip uploads its window (owned + ghost rows) straight
+// from the caller's arrays, the group steps once, the owned rows come back;
+// on an error the caller's state is untouched
+StepInfo CsphTvdStepper::step_group(FlowState& state, double dt_cap) {
+  const size_t nx = (size_t)terrain_->nx;
+  for (swf_ctx* c : strips_) {
+    int j0, j1, glo, ghi;
+    swf_strip_rows(c, &j0, &j1, &glo, &ghi);
+    size_t off = (size_t)(j0 - glo) * nx;
+    if (int rc = swf_upload_state(c, state.H.data() + off, state.HUx.data() + off,
+                                  state.HUy.data() + off, state.t))
+      throw_status(rc, swf_last_error(c));
+  }
+  int done = 0;
+  swf_step_info ci{};
+  if (int rc = swf_group_run(group_, 1, dt_cap, &done, &ci))
+    throw_status(rc, swf_group_last_error(group_));
+  std::vector<double> h, x, y;
+  double t = state.t;
+  for (swf_ctx* c : strips_) {
+    int j0, j1, glo, ghi;
+    swf_strip_rows(c, &j0, &j1, &glo, &ghi);
+    size_t rows = (size_t)(glo + (j1 - j0) + ghi), own = (size_t)(j1 - j0) * nx;
+    h.resize(rows * nx);
+    x.resize(rows * nx);
+    y.resize(rows * nx);
+    if (int rc = swf_download_state(c, h.data(), x.data(), y.data(), &t))
+      throw_status(rc, swf_last_error(c));
+    size_t src = (size_t)glo * nx, dst = (size_t)j0 * nx;
+    std::copy(h.begin() + src, h.begin() + src + own, state.H.begin() + dst);
+    std::copy(x.begin() + src, x.begin() + src + own, state.HUx.begin() + dst);
+    std::copy(y.begin() + src, y.begin() + src + own, state.HUy.begin() + dst);
+  }
+  state.t = t;
+  StepInfo s;
+  s.tau = ci.tau;
+  s.active_fraction = ci.active_fraction;
+  s.lagrangian_blocks = ci.lagrangian_blocks;
+  s.flux_blocks = ci.flux_blocks;
+  s.total_blocks = ci.total_blocks;
+  s.clamp_deficit_volume = group_vol_[0] = ci.clamp_deficit_volume;
+  s.source_volume = group_vol_[1] = ci.source_volume;
+  s.boundary_outflow_volume = group_vol_[2] = ci.boundary_outflow_volume;
+  return s;
+}
+
 void CsphTvdStepper::begin_step(const FlowState& state) {
+  single("the stage API");
   if (state.nx != terrain_->nx || state.ny != terrain_->ny)
     throw ConfigError("stepper: state does not match the terrain grid");
   sync_config();
@@ -330,31 +435,35 @@ void CsphTvdStepper::begin_step(const FlowState& state) {
   check(swf_stage(ctx_, SWF_STAGE_BEGIN, 0.0, nullptr));
 }
 
-void CsphTvdStepper::compute_forces(const FlowState&) { check(swf_stage(ctx_, SWF_STAGE_FORCES, 0.0, nullptr)); }
+void CsphTvdStepper::compute_forces(const FlowState&) { single("the stage API"); check(swf_stage(ctx_, SWF_STAGE_FORCES, 0.0, nullptr)); }
 
 double CsphTvdStepper::compute_dt(const FlowState&, double dt_cap) const {
+  single("the stage API");
   double tau = 0.0;
   check(swf_stage(ctx_, SWF_STAGE_DT, dt_cap, &tau));
   return tau;
 }
 
-void CsphTvdStepper::predictor(const FlowState&, double tau) { check(swf_stage(ctx_, SWF_STAGE_PREDICTOR, tau, nullptr)); }
-void CsphTvdStepper::mid_forces(const FlowState&, double tau) { check(swf_stage(ctx_, SWF_STAGE_MID_FORCES, tau, nullptr)); }
-void CsphTvdStepper::corrector(const FlowState&, double tau) { check(swf_stage(ctx_, SWF_STAGE_CORRECTOR, tau, nullptr)); }
-void CsphTvdStepper::flux(const FlowState&, double tau) { check(swf_stage(ctx_, SWF_STAGE_FLUX, tau, nullptr)); }
+void CsphTvdStepper::predictor(const FlowState&, double tau) { single("the stage API"); check(swf_stage(ctx_, SWF_STAGE_PREDICTOR, tau, nullptr)); }
+void CsphTvdStepper::mid_forces(const FlowState&, double tau) { single("the stage API"); check(swf_stage(ctx_, SWF_STAGE_MID_FORCES, tau, nullptr)); }
+void CsphTvdStepper::corrector(const FlowState&, double tau) { single("the stage API"); check(swf_stage(ctx_, SWF_STAGE_CORRECTOR, tau, nullptr)); }
+void CsphTvdStepper::flux(const FlowState&, double tau) { single("the stage API"); check(swf_stage(ctx_, SWF_STAGE_FLUX, tau, nullptr)); }
 
 void CsphTvdStepper::final_update(FlowState& state, double tau) {
+  single("the stage API");
   check(swf_stage(ctx_, SWF_STAGE_FINAL, tau, nullptr));
   check(swf_download_state(ctx_, state.H.data(), state.HUx.data(), state.HUy.data(), &state.t));
 }
 
 std::span<const double> CsphTvdStepper::scratch(int which, std::vector<double>& buf) const {
+  single("the scratch accessors");
   buf.resize(terrain_->cells());
   check(swf_download_scratch(ctx_, which, buf.data()));
   return buf;
 }
 
 const BlockMask& CsphTvdStepper::mask() const {
+  single("mask()");
   int nbx = 0, nby = 0;
   check(swf_download_mask(ctx_, nullptr, nullptr, &nbx, &nby));
   mask_.block_size = opt_.block_size;
@@ -369,6 +478,7 @@ const BlockMask& CsphTvdStepper::mask() const {
 }
 
 const SourceField& CsphTvdStepper::step_sources() const {
+  single("the scratch accessors");
   src_.resize(terrain_->nx, terrain_->ny);
   check(swf_download_scratch(ctx_, SWF_SCR_SIGMA, src_.sigma.data()));
   check(swf_download_scratch(ctx_, SWF_SCR_SRC_VX, src_.vx.data()));
@@ -378,6 +488,7 @@ const SourceField& CsphTvdStepper::step_sources() const {
 }
 
 const ForceField& CsphTvdStepper::forces_n() const {
+  single("the scratch accessors");
   f_n_.resize(terrain_->nx, terrain_->ny);
   check(swf_download_scratch(ctx_, SWF_SCR_FN_FX, f_n_.fx.data()));
   check(swf_download_scratch(ctx_, SWF_SCR_FN_FY, f_n_.fy.data()));
@@ -388,6 +499,7 @@ const ForceField& CsphTvdStepper::forces_n() const {
 }
 
 const ForceField& CsphTvdStepper::forces_mid() const {
+  single("the scratch accessors");
   f_mid_.resize(terrain_->nx, terrain_->ny);
   check(swf_download_scratch(ctx_, SWF_SCR_FM_FX, f_mid_.fx.data()));
   check(swf_download_scratch(ctx_, SWF_SCR_FM_FY, f_mid_.fy.data()));
@@ -408,16 +520,19 @@ std::span<const double> CsphTvdStepper::flux_momentum_x() const { return scratch
 std::span<const double> CsphTvdStepper::flux_momentum_y() const { return scratch(SWF_SCR_FVY, buf_[8]); }
 
 double CsphTvdStepper::last_clamp_deficit() const {
+  if (group_) return group_vol_[0];
   double v = 0.0;
   check(swf_last_volumes(ctx_, &v, nullptr, nullptr));
   return v;
 }
 double CsphTvdStepper::last_source_volume() const {
+  if (group_) return group_vol_[1];
   double v = 0.0;
   check(swf_last_volumes(ctx_, nullptr, &v, nullptr));
   return v;
 }
 double CsphTvdStepper::last_boundary_outflow() const {
+  if (group_) return group_vol_[2];
   double v = 0.0;
   check(swf_last_volumes(ctx_, nullptr, nullptr, &v));
   return v;

@@ -177,7 +177,8 @@ PYBIND11_MODULE(swflood_native, m) {
       .def_readwrite("block_size", &StepperOptions::block_size)
       .def_readwrite("skip_dry_blocks", &StepperOptions::skip_dry_blocks)
       .def_readwrite("workers", &StepperOptions::workers)
-      .def_readwrite("boundaries", &StepperOptions::boundaries);
+      .def_readwrite("boundaries", &StepperOptions::boundaries)
+      .def_readwrite("devices", &StepperOptions::devices);
   py::class_<StageTimings>(m, "StageTimings")
       .def_readonly("mask", &StageTimings::mask)
       .def_readonly("forces", &StageTimings::forces)

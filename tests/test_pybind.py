@@ -101,3 +101,49 @@ def test_native_numerical_error_leaves_state():
         g.step(st)
     np.testing.assert_array_equal(st.H, before[0])
     np.testing.assert_array_equal(st.HUx, before[1])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("devices", [2, 3])
+def test_native_multi_device_group_matches_oracle(oracle_built, devices):
+    """StepperOptions.devices > 1: the stepper drives one row strip per device
+    from this process (swf_group_*: peer-linked strips, event-ordered streams,
+    device-side speed max).  With one GPU the strips share it -- the same code
+    path; results stay bit-identical to the single-grid oracle."""
+    sc = S.floodplain(128, 50.0)
+    T, P, K, O, W, srcs, st = to_native(sc)
+    O.devices = devices
+    g = sw.CsphTvdStepper(T, P, K, O)
+    g.set_wind(W)
+    g.set_sources(srcs)
+    o = make(oracle_built.OracleStepper, sc)
+    ref = sc.state.copy()
+    for _ in range(8):
+        a = g.step(st)
+        b = o.step(ref)
+        assert a.tau == b.tau
+        assert (a.lagrangian_blocks, a.flux_blocks, a.total_blocks) == \
+            (b.lagrangian_blocks, b.flux_blocks, b.total_blocks)
+        assert a.active_fraction == b.active_fraction
+    out = sc.state.copy()
+    out.H[:], out.HUx[:], out.HUy[:], out.t = st.H, st.HUx, st.HUy, st.t
+    assert_state_bitwise(out, ref, f"{devices}-device group")
+    with pytest.raises(sw.ConfigError, match="devices == 1"):
+        g.begin_step(st)
+
+
+@pytest.mark.gpu
+def test_native_multi_device_abort_leaves_state():
+    T = sw.Terrain(64, 64, 1.0, 0.0, 0.0, np.zeros(64 * 64))
+    st = sw.FlowState.dry(T)
+    st.H[:] = 1.0
+    st.HUx[:] = 50.0
+    O = sw.StepperOptions()
+    O.devices = 2
+    g = sw.CsphTvdStepper(T, sw.PhysicalParams(), sw.TimestepControl(0.5, 10.0, 0.05), O)
+    before = st.H.copy(), st.HUx.copy(), st.t
+    with pytest.raises(sw.NumericalError, match="abort floor"):
+        g.step(st)
+    np.testing.assert_array_equal(st.H, before[0])
+    np.testing.assert_array_equal(st.HUx, before[1])
+    assert st.t == before[2]
