@@ -295,6 +295,19 @@ int swf_strip_set_peer(swf_ctx* ctx, int side, double* const* bufs6, int peer_ro
 int swf_strip_rows(const swf_ctx* ctx, int* j0, int* j1, int* ghost_lo,
                    int* ghost_hi);
 
+/* Host-buffer step of a strip from PINNED window arrays (rows = its window,
+ * the caller's own layout): phase 1 copies the depth window, computes the
+ * block mask, reads the momentum of the flux-active owned tiles and of every
+ * ghost row over PCIe, runs the forces and returns the strip's CFL speed;
+ * the caller max-reduces it over the strips; phase 2 finishes the step with
+ * the global speed, k_step writing every updated owned cell straight into the
+ * caller's arrays (restored on a numerical abort); *t = the new time.  The
+ * device copy is incomplete afterwards (upload before resident steps). */
+int swf_strip_host_phase1(swf_ctx* ctx, double* H, double* HUx, double* HUy, const double* t,
+                          double dt_cap, double* speed_out);
+int swf_strip_host_phase2(swf_ctx* ctx, double* H, double* HUx, double* HUy, double* t,
+                          double global_speed, double dt_cap, swf_step_info* info);
+
 /* ---- single-process multi-GPU group (StepperOptions::devices > 1) ----
  * Replaces CsphTvdStepper's internal one-stream-per-GPU model of SURVEY.md
  * §8b for callers that drive every GPU from one process: n strip contexts

@@ -77,6 +77,8 @@ def declare(lib):
     _sig(lib, "swf_strip_local_speed", I, P, C.c_void_p)
     _sig(lib, "swf_strip_finish", I, P, C.c_void_p, D)
     _sig(lib, "swf_strip_end_batch", I, P, PI, PN)
+    _sig(lib, "swf_strip_host_phase1", I, P, C.c_void_p, C.c_void_p, C.c_void_p, PD, D, PD)
+    _sig(lib, "swf_strip_host_phase2", I, P, C.c_void_p, C.c_void_p, C.c_void_p, PD, D, D, PN)
     _sig(lib, "swf_strip_pack_async", I, P, I, C.c_void_p)
     _sig(lib, "swf_strip_unpack_async", I, P, I, C.c_void_p)
     PND = C.POINTER(A.swf_nest_desc)

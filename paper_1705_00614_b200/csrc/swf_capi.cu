@@ -1040,6 +1040,70 @@ int swf_strip_phase2(swf_ctx* c, double global_speed, double dt_cap, swf_step_in
   return SWF_OK;
 }
 
+// ---- host-buffer step of a strip (pinned window arrays) ----------------------
+static bool host_mapped(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost && a.devicePointer == p;
+}
+
+int swf_strip_host_phase1(swf_ctx* c, double* H, double* HUx, double* HUy, const double* t,
+                          double dt_cap, double* speed_out) {
+  cudaSetDevice(c->device);
+  if (c->mode != 0) return set_err(c, SWF_ECONFIG, "strip host step needs the fused path");
+  if (!host_mapped(H) || !host_mapped(HUx) || !host_mapped(HUy))
+    return set_err(c, SWF_ECONFIG, "strip host step needs pinned (device-mapped) window arrays");
+  const Geo& G = c->geo;
+  int rc = reset_counters(c);
+  if (rc) return rc;
+  size_t n = local_cells(c), bytes = n * sizeof(double);
+  cudaError_t e = cudaMemcpyAsync(c->H[c->cur], H, bytes, cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(&c->d_sc->t, t, sizeof(double), cudaMemcpyHostToDevice, c->stream);
+  // the ghost rows' momentum in full (their tiles belong to the neighbours)
+  size_t nx = (size_t)G.nx, lo = (size_t)G.r0 * nx, hi0 = (size_t)G.r1 * nx;
+  for (int f = 0; f < 2 && e == cudaSuccess; ++f) {
+    double* dev = f == 0 ? c->HUx[c->cur] : c->HUy[c->cur];
+    const double* host = f == 0 ? HUx : HUy;
+    if (lo) e = cudaMemcpyAsync(dev, host, lo * sizeof(double), cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess && n > hi0)
+      e = cudaMemcpyAsync(dev + hi0, host + hi0, (n - hi0) * sizeof(double), cudaMemcpyHostToDevice,
+                          c->stream);
+  }
+  size_t nt = (size_t)G.tiles_x * G.tiles_y;
+  if (e == cudaSuccess && nt) e = cudaMemsetAsync(c->d_tile_same, 0, nt, c->stream);
+  if (e != cudaSuccess) return cuda_check(c, e, "strip host ingest");
+  invalidate_mask(c);
+  if ((rc = launch_begin(c, dt_cap)) || (rc = launch_mask(c)) || (rc = fused_ingest_hu(c, HUx, HUy)))
+    return rc;
+  c->state_partial = 0;
+  c->last_ingest_bytes = (long long)bytes + 16LL * (long long)(lo + (n - hi0));
+  return swf_strip_phase1(c, dt_cap, speed_out);
+}
+
+int swf_strip_host_phase2(swf_ctx* c, double* H, double* HUx, double* HUy, double* t,
+                          double global_speed, double dt_cap, swf_step_info* info) {
+  cudaSetDevice(c->device);
+  c->wt_host[0] = H;
+  c->wt_host[1] = HUx;
+  c->wt_host[2] = HUy;
+  int rc = swf_strip_phase2(c, global_speed, dt_cap, info);
+  c->wt_host[0] = c->wt_host[1] = c->wt_host[2] = nullptr;
+  c->state_partial = 1;
+  if (rc) {
+    if (rc == SWF_ENUMERICAL && !fused_restore_host(c, H, HUx, HUy)) cudaStreamSynchronize(c->stream);
+    return rc;
+  }
+  int na = 0, ntot = 0, cpt = 0;
+  swf_active_tiles(c, &na, &ntot, &cpt);
+  c->last_ingest_bytes += 2LL * 8 * na * cpt;
+  if (t) *t = c->h_t;
+  return SWF_OK;
+}
+
 int swf_strip_halo_ptrs(swf_ctx* c, int side, double** send3, double** recv3, size_t* count) {
   const Geo& G = c->geo;
   int ghosts = side == 0 ? G.r0 : G.rows - G.r1;

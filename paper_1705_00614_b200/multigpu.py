@@ -176,6 +176,37 @@ class Strip:
         self._rc(self._lib.swf_strip_phase2(self.ctx, float(speed), float(dt_cap), C.byref(info)))
         return info_from_c(info)
 
+    # host-buffer step from pinned window arrays (include/swf.h)
+    def host_phase1(self, H, HUx, HUy, t: float, dt_cap: float = 0.0) -> float:
+        """H/HUx/HUy: pinned arrays whose first element is the window's first
+        cell (views into a pinned global array are fine)."""
+        s = C.c_double()
+        tt = C.c_double(t)
+        self._rc(self._lib.swf_strip_host_phase1(
+            self.ctx, H.ctypes.data, HUx.ctypes.data, HUy.ctypes.data, C.byref(tt),
+            float(dt_cap), C.byref(s)))
+        return s.value
+
+    def host_phase2(self, H, HUx, HUy, speed: float, dt_cap: float = 0.0):
+        from ._marshal import info_from_c
+        info = A.swf_step_info()
+        t = C.c_double()
+        self._rc(self._lib.swf_strip_host_phase2(
+            self.ctx, H.ctypes.data, HUx.ctypes.data, HUy.ctypes.data, C.byref(t), float(speed),
+            float(dt_cap), C.byref(info)))
+        return t.value, info_from_c(info)
+
+    def last_ingest_bytes(self) -> int:
+        v = C.c_longlong()
+        self._rc(self._lib.swf_last_ingest_bytes(self.ctx, C.byref(v)))
+        return v.value
+
+    def active_tiles(self):
+        """(flux-active tiles, tiles, cells per tile) of the last step."""
+        a, n, c = C.c_int(), C.c_int(), C.c_int()
+        self._rc(self._lib.swf_active_tiles(self.ctx, C.byref(a), C.byref(n), C.byref(c)))
+        return a.value, n.value, c.value
+
     def stream_handle(self) -> int:
         return self._lib.swf_stream(self.ctx) or 0
 
@@ -653,25 +684,36 @@ def bench_strips(args) -> Optional[dict]:
     pin = lambda a: torch.from_numpy(np.array(a, copy=True)).pin_memory().numpy()
     hH, hX, hY = pin(sc.state.H), pin(sc.state.HUx), pin(sc.state.HUy)
     t_now = strip.download(hH, hX, hY)
+
+    def host_step(t):
+        # the strip's host-buffer step: window depth in full, momentum of the
+        # flux-active owned tiles and the ghost rows over PCIe, the speeds
+        # max-reduced, k_step writing the owned cells back in place
+        sp = strip.host_phase1(hH, hX, hY, t)
+        g = dist_allreduce_max(sp, rs.xdev)
+        t, _ = strip.host_phase2(hH, hX, hY, g)
+        return t
+
+    t_now = host_step(t_now)  # warm-up of the host path
     dist.barrier()
+    h2d = d2h = 0
     t0 = time.perf_counter()
     for _ in range(E):
-        strip.upload(hH, hX, hY, t_now)  # H2D: the strip window (owned + ghost rows)
-        if use_async:
-            rs.begin_async()
-            rs.step_async(0.0)
-            rs.end_async()
-        else:
-            rs.step(0.0)
-        t_now = strip.download(hH, hX, hY)  # D2H: the owned rows
+        t_now = host_step(t_now)
+        na, _, cpt = strip.active_tiles()
+        h2d += strip.last_ingest_bytes() + 8
+        d2h += 3 * 8 * na * cpt + 8
     el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=rs.xdev)
     dist.all_reduce(el, op=dist.ReduceOp.MAX)
-    io = torch.tensor([24.0 * hH.size + 8, 24.0 * n_own + 8], dtype=torch.float64, device=rs.xdev)
+    io = torch.tensor([h2d / E, d2h / E], dtype=torch.float64, device=rs.xdev)
     dist.all_reduce(io, op=dist.ReduceOp.SUM)
     e2e = {"value": round(N_total * E / float(el.item()) / 1e6, 3), "unit": "Mcells/s",
            "h2d_bytes_per_step": int(io[0].item()), "d2h_bytes_per_step": int(io[1].item()),
-           "how": "every rank, every step: its strip window (owned + ghost rows) uploaded from "
-                  "pinned host memory, one exchanged step, the owned rows downloaded; "
+           "how": "every rank, every step, from its pinned window of the host state "
+                  "(swf_strip_host_phase1/2): depth copied in full, momentum of the "
+                  "flux-active tiles and ghost rows read over PCIe, CFL speed max-reduced "
+                  "across ranks, k_step writing the updated owned cells straight into the "
+                  "pinned arrays; d2h counts the flux-active tiles (an upper bound); "
                   "host-timed, max over ranks"}
     if rank != 0:
         dist.barrier()

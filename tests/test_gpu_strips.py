@@ -54,3 +54,41 @@ def test_strips_bitwise_equal_single_grid(parts, mode):
     assert_bitwise(H, st.H, "H")
     assert_bitwise(X, st.HUx, "HUx")
     assert_bitwise(Y, st.HUy, "HUy")
+
+
+@pytest.mark.parametrize("parts", [2, 3])
+def test_strip_host_steps_from_pinned_windows(parts):
+    """The strips' host-buffer step (swf_strip_host_phase1/2): every strip
+    reads its window from ONE pinned global state (depth in full, momentum of
+    its flux-active tiles and ghost rows), the speeds are max-reduced, and
+    each k_step writes its owned cells back in place -- bit-identical to the
+    single-grid run."""
+    import torch
+    from paper_1705_00614_b200 import CsphTvdStepper
+    n = 256
+    full = S.floodplain(n, 50.0)
+    one = make(CsphTvdStepper, full)
+    ref = full.state.copy()
+    one.upload(ref)
+    one.run(12)
+    one.download(ref)
+    pin = lambda a: torch.from_numpy(np.array(a, copy=True)).pin_memory().numpy()
+    H, X, Y = pin(full.state.H), pin(full.state.HUx), pin(full.state.HUy)
+    bounds = M.strip_bounds(n, parts, full.options.block_size)
+    strips = []
+    for j0, j1 in bounds:
+        w0, w1 = M.window_rows(j0, j1, n)
+        sc = S.floodplain(n, 50.0, window=(0, w0, n, w1 - w0))
+        strips.append((M.Strip(sc, n, j0, j1, sc.global_sources, sc.wind), w0 * n))
+    t = 0.0
+    for _ in range(12):
+        sp = [s.host_phase1(H[o:], X[o:], Y[o:], t) for s, o in strips]
+        g = max(sp)
+        ts = [s.host_phase2(H[o:], X[o:], Y[o:], g)[0] for s, o in strips]
+        assert len(set(ts)) == 1
+        t = ts[0]
+        assert all(s.last_ingest_bytes() < 3 * 8 * H.size for s, _ in strips)
+    assert t == ref.t
+    assert_bitwise(H, ref.H, "H")
+    assert_bitwise(X, ref.HUx, "HUx")
+    assert_bitwise(Y, ref.HUy, "HUy")
