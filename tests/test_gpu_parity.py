@@ -500,3 +500,22 @@ def test_odd_sizes_vs_oracle(gpu_cls, oracle_built, nx, ny, bs):
         g.step(hs)
         o.step(st)
     assert_state_bitwise(hs, st, f"{nx}x{ny} pinned")
+
+
+@pytest.mark.parametrize("n,win", [(40960, (0, 20000, 40960, 40)), (8192, (4000, 0, 5, 8192))])
+def test_extreme_aspect_ratios_vs_oracle(gpu_cls, oracle_built, n, win):
+    """Ragged extremes: a 40960-wide, 40-row band (long rows, one partial tile
+    row, 1280 tiles per row) and a 5-wide, 8192-tall column (one partial tile
+    column): bitwise vs the oracle."""
+    sc = S.floodplain(n, 50.0, window=win)
+    st = sc.state.copy()
+    g = make(gpu_cls, sc)
+    o = make(oracle_built.OracleStepper, sc)
+    a = st.copy()
+    g.upload(a)
+    for _ in range(6):
+        ia = g.step_resident()
+        ib = o.step(st)
+        assert ia.tau == ib.tau
+    g.download(a)
+    assert_state_bitwise(a, st, f"{sc.terrain.nx}x{sc.terrain.ny}")
