@@ -56,3 +56,5 @@ def test_config_errors_before_device():
         CsphTvdStepper(Terrain(4, 4, 1.0, 0.0, 0.0, b), PhysicalParams(), TimestepControl())
     with pytest.raises(ConfigError, match="block size"):
         CsphTvdStepper(T, PhysicalParams(), TimestepControl(), StepperOptions(block_size=0))
+    with pytest.raises(ConfigError, match="nx and ny must be >= 1"):  # empty grid
+        CsphTvdStepper(Terrain(0, 4, 1.0, 0.0, 0.0, np.zeros(0)), PhysicalParams(), TimestepControl())

@@ -519,3 +519,22 @@ def test_extreme_aspect_ratios_vs_oracle(gpu_cls, oracle_built, n, win):
         assert ia.tau == ib.tau
     g.download(a)
     assert_state_bitwise(a, st, f"{sc.terrain.nx}x{sc.terrain.ny}")
+
+
+@pytest.mark.parametrize("nx,ny", [(1, 1), (1, 9), (9, 1), (2, 2)])
+def test_degenerate_grids_vs_oracle(gpu_cls, oracle_built, nx, ny):
+    """The smallest grids (a single cell, one row, one column): every cell is
+    a domain-edge cell of one partial tile; bitwise vs the oracle."""
+    from paper_1705_00614_b200.types import (FlowState, PhysicalParams, StepperOptions, Terrain,
+                                             TimestepControl)
+    n = nx * ny
+    T = Terrain(nx, ny, 2.0, 0.0, 0.0, np.linspace(0.0, 0.3, n))
+    P = PhysicalParams(n_manning=0.03, nu=0.5)
+    st = FlowState(nx, ny, 0.0, np.linspace(1.0, 0.2, n), np.full(n, 0.1), np.full(n, -0.05))
+    g = gpu_cls(T, P, TimestepControl(dt_max=0.05), StepperOptions())
+    o = oracle_built.OracleStepper(T, P, TimestepControl(dt_max=0.05), StepperOptions())
+    a, b = st.copy(), st.copy()
+    for _ in range(20):
+        ia, ib = g.step(a), o.step(b)
+        assert ia.tau == ib.tau
+    assert_state_bitwise(a, b, f"{nx}x{ny}")
