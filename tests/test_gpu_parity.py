@@ -538,3 +538,35 @@ def test_degenerate_grids_vs_oracle(gpu_cls, oracle_built, nx, ny):
         ia, ib = g.step(a), o.step(b)
         assert ia.tau == ib.tau
     assert_state_bitwise(a, b, f"{nx}x{ny}")
+
+
+@pytest.mark.parametrize("what", ["nan_momentum", "inf_momentum", "nan_two_cells"])
+def test_non_finite_state_raises_like_the_reference(gpu_cls, oracle_built, what):
+    """Non-finite momenta in wet cells ("nulls" of this domain): the step
+    aborts with the reference's non-finite-flux error naming the same cell
+    (raise_pending_error, stepper.cpp:568-577), on the fused and the staged
+    path, and leaves the state untouched."""
+    from paper_1705_00614_b200 import NumericalError
+    sc = S.floodplain(96, 50.0)
+    st = sc.state.copy()
+    wet = np.flatnonzero(st.H > 0.5)
+    k = wet[len(wet) // 2]
+    if what == "nan_momentum":
+        st.HUx[k] = np.nan
+    elif what == "inf_momentum":
+        st.HUy[k] = np.inf
+    else:
+        st.HUx[k] = np.nan
+        st.HUy[wet[len(wet) // 3]] = np.nan
+    o = make(oracle_built.OracleStepper, sc, kind="orc")
+    with pytest.raises(NumericalError) as eo:
+        o.step(st.copy())
+    for mode in (0, 1):
+        g = make(gpu_cls, sc, mode=mode)
+        a = st.copy()
+        before = a.copy()
+        with pytest.raises(NumericalError) as eg:
+            g.step(a)
+        assert str(eg.value) == str(eo.value), (mode, str(eg.value), str(eo.value))
+        np.testing.assert_array_equal(a.H, before.H)
+        np.testing.assert_array_equal(np.isnan(a.HUx), np.isnan(before.HUx))
