@@ -58,3 +58,22 @@ def test_config_errors_before_device():
         CsphTvdStepper(T, PhysicalParams(), TimestepControl(), StepperOptions(block_size=0))
     with pytest.raises(ConfigError, match="nx and ny must be >= 1"):  # empty grid
         CsphTvdStepper(Terrain(0, 4, 1.0, 0.0, 0.0, np.zeros(0)), PhysicalParams(), TimestepControl())
+
+
+def test_more_than_int32_cells_is_a_config_error():
+    """The reference indexes cells with int (grid.hpp:27): grids above 2^31-1
+    cells are rejected at creation, before any device or bed access."""
+    import ctypes as C
+    import numpy as np
+    from paper_1705_00614_b200 import _abi as A
+    from paper_1705_00614_b200._lib import lib
+    L = lib()
+    b = np.zeros(1)
+    t = A.swf_terrain(50000, 50000, 1.0, 0.0, 0.0, A.dptr(b))
+    p = A.swf_params(9.81, 0.02, 0.0, 0.0, 1e-3, 1.2, 1000.0, 1e-6, A.PD())
+    k = A.swf_control(0.5, 10.0, 1e-9)
+    o = A.swf_options(16, 1, 1, 0, 0, 0, 0)
+    ctx = C.c_void_p()
+    rc = L.swf_create(C.byref(t), C.byref(p), C.byref(k), C.byref(o), C.byref(ctx))
+    assert rc == 1  # SWF_ECONFIG
+    assert b"2^31-1" in L.swf_last_error(None)
