@@ -275,8 +275,12 @@ int create_impl(const swf_terrain* T, const swf_params* P, const swf_control* K,
     if (e == cudaSuccess) e = cudaMemset(c->HUx[s], 0, bytes);
     if (e == cudaSuccess) e = cudaMemset(c->HUy[s], 0, bytes);
   }
+  // f' is written for wet cells only, but k_step stages it for its whole
+  // region (and discards it for dry cells): start from defined values
   if (e == cudaSuccess) e = cudaMalloc(&c->fpx, bytes);
   if (e == cudaSuccess) e = cudaMalloc(&c->fpy, bytes);
+  if (e == cudaSuccess) e = cudaMemset(c->fpx, 0, bytes);
+  if (e == cudaSuccess) e = cudaMemset(c->fpy, 0, bytes);
   size_t nt = (size_t)G.tiles_x * G.tiles_y;
   if (e == cudaSuccess) e = cudaMalloc(&c->d_tile_act, 2 * (nt ? nt : 1));
   if (e == cudaSuccess) e = cudaMemset(c->d_tile_act, 0, 2 * (nt ? nt : 1));
@@ -285,6 +289,8 @@ int create_impl(const swf_terrain* T, const swf_params* P, const swf_control* K,
   // per-tile diagnostic partials, then the k_reduce partials
   if (e == cudaSuccess)
     e = cudaMalloc(&c->d_part, 5 * ((nt ? nt : 1) + (size_t)fused_reduce_ctas()) * sizeof(double));
+  if (e == cudaSuccess)
+    e = cudaMemset(c->d_part, 0, 5 * ((nt ? nt : 1) + (size_t)fused_reduce_ctas()) * sizeof(double));
   if (e == cudaSuccess) e = cudaMalloc(&c->d_sig, 2 * sizeof(double));
   if (e == cudaSuccess) e = cudaMalloc(&c->d_sc, sizeof(StepScalars));
   if (e == cudaSuccess) e = cudaMallocHost(&c->h_sc, sizeof(StepScalars));
