@@ -42,12 +42,18 @@ def test_device_cbrt_matches_glibc(oracle_built):
 def test_device_hll_matches_oracle(oracle_built):
     from paper_1705_00614_b200.stepper import hll_face_flux_device
     rng = np.random.default_rng(7)
-    n = 40000
+    n = 200000
     x = np.column_stack([rng.uniform(0, 5, n), rng.normal(0, 3, n), rng.normal(0, 1, n),
                          rng.uniform(0, 5, n), rng.normal(0, 3, n), rng.normal(0, 1, n)])
     x[: n // 4, 0] = 0.0  # dry left
     x[n // 4: n // 2, 3] = 0.0  # dry right
     x[n // 2: n // 2 + 100, [0, 3]] = 0.0  # dry/dry
+    e = slice(n // 2 + 100, n // 2 + 40000)  # depths around the dry threshold
+    x[e, 0] = rng.uniform(0, 3e-6, e.stop - e.start)
+    x[e, 3] = rng.uniform(0, 3e-6, e.stop - e.start)
+    w = slice(n // 2 + 40000, n // 2 + 60000)  # wide dynamic range
+    x[w, 0] = 10.0 ** rng.uniform(-8, 3, w.stop - w.start)
+    x[w, 1] = rng.normal(0, 1, w.stop - w.start) * 10.0 ** rng.uniform(-6, 2, w.stop - w.start)
     got = hll_face_flux_device(x, 9.81)
     lib = oracle_built.load("orc")
     o3 = (C.c_double * 3)()
