@@ -323,6 +323,7 @@ struct ForcesArgs {
   int* redo;                       // tiles whose speculative divisions were rejected
   int* list;                       // work list of k_flist / k_forces_list
   int ra0, ra1, tr_lo, do_mask;
+  int lr0, lr1;                    // tile rows the work list covers (strips: ghost rows too)
 };
 
 // redo-list entries: tile column + (tile row + REDO_ROW0) * tiles_x
@@ -558,31 +559,38 @@ __device__ __forceinline__ void append_ordered(int* list, int* n, bool take, int
 // persistent k_forces_list grid then takes list entries off an atomic
 // counter, so the ~60 % of C3 tiles that are dry cost one thread, not a CTA.
 __global__ void k_flist(Geo G, ForcesArgs A) {
-  const int nt = G.tiles_x * G.tiles_y;
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool valid = t < nt;  // every lane reaches the warp-wide append
+  const int nt = G.tiles_x * (A.lr1 - A.lr0);
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;  // list index: relative to row lr0
   StepScalars* sc = A.sc;
-  const int tx = t % G.tiles_x, tr = t / G.tiles_x;
+  const int tx = t % G.tiles_x, tr = t / G.tiles_x + A.lr0;
+  // a strip's ghost tile rows and the tile rows next to its edges are always
+  // visited (their halo changes by exchange), like forces_tile's own rule
+  const bool own = tr >= 0 && tr < G.tiles_y;
+  const bool edge = !own || (tr == 0 && G.r0 > 0) || (tr == G.tiles_y - 1 && G.r1 < G.rows);
+  const int tt = own ? tx + tr * G.tiles_x : 0;  // owned-tile index
+  const bool valid = t < nt;  // every lane reaches the warp-wide append
   // host-buffer step: k_mask/k_tiles already flagged this state, so a tile
   // whose blocks have no wet cell in their interiors or rings (its forces
   // region is dry) is skipped outright, its block counts zero
   const bool fresh = A.do_mask && G.skip && sc->mask_fresh;
   bool busy;
-  if (fresh) {
-    busy = valid && (A.tile_act[t] != 0 || A.tile_srcm[t] != 0);
+  if (edge) {
+    busy = valid;
+  } else if (fresh) {
+    busy = valid && (A.tile_act[tt] != 0 || A.tile_srcm[tt] != 0);
   } else {
-    busy = valid && (!(A.do_mask && G.skip && sc->mask_valid) || A.tile_srcm[t] != 0);
+    busy = valid && (!(A.do_mask && G.skip && sc->mask_valid) || A.tile_srcm[tt] != 0);
     for (int q = 0; q < 9 && valid && !busy; ++q) {
       int x2 = tx + q % 3 - 1, y2 = tr + q / 3 - 1;
       if (x2 >= 0 && x2 < G.tiles_x && y2 >= 0 && y2 < G.tiles_y)
         busy = A.tile_prev[x2 + y2 * G.tiles_x] != 0;
     }
   }
-  if (valid && !busy) {
-    A.tile_act[t] = 0;
+  if (valid && !busy) {  // (never an edge or ghost tile)
+    A.tile_act[tt] = 0;
     if (fresh) {
-      A.cnt_part[5 * (size_t)t + 3] = 0.0;
-      A.cnt_part[5 * (size_t)t + 4] = 0.0;
+      A.cnt_part[5 * (size_t)tt + 3] = 0.0;
+      A.cnt_part[5 * (size_t)tt + 4] = 0.0;
     }
   }
   append_ordered(A.list, &sc->list_n[0], busy, t);
@@ -599,7 +607,7 @@ __global__ void __launch_bounds__(NTHR, SWF_FORCES_MINB) k_forces_list(Geo G, Fo
     __syncthreads();
     if (q >= n) break;
     const int t = A.list[q];
-    forces_tile<SWF_SPECULATE != 0>(G, A, t % G.tiles_x, t / G.tiles_x, true);
+    forces_tile<SWF_SPECULATE != 0>(G, A, t % G.tiles_x, t / G.tiles_x + A.lr0, true);
     __syncthreads();
   }
 }
@@ -1488,16 +1496,27 @@ int fused_enqueue_phase1(swf_ctx* c, double dt_cap, int part) {
   int tr_hi = (A.ra1 - G.r0 + BY - 1) / BY;
   if (tr_hi < G.tiles_y) tr_hi = G.tiles_y;
   A.do_mask = fm ? 1 : 0;
+  A.lr0 = A.tr_lo;
+  A.lr1 = tr_hi;
+  // the work list + persistent grid (k_flist / k_forces_list) over tile rows
+  // [r_first, r_end); one CTA per tile when the mask is not fused
+  auto listed = [&](int r_first, int r_end) {
+    if (r_end <= r_first) return;
+    ForcesArgs B = A;
+    B.lr0 = r_first;
+    B.lr1 = r_end;
+    int ntile = G.tiles_x * (r_end - r_first);
+    if (SWF_TILE_LISTS && fm) {
+      k_flist<<<(ntile + 255) / 256, 256, 0, c->stream>>>(G, B);
+      k_forces_list<<<c->sm_count * SWF_FORCES_MINB, NTHR, 0, c->stream>>>(G, B);
+    } else {
+      B.tr_lo = r_first;
+      k_forces<<<ntile, NTHR, 0, c->stream>>>(G, B);
+    }
+  };
   if (part < 0) {
     int ntile = G.tiles_x * (tr_hi - A.tr_lo);
-    const bool use_list = SWF_TILE_LISTS && fm && G.r0 == 0 && G.r1 == G.rows &&
-                          A.tr_lo == 0 && tr_hi == G.tiles_y;
-    if (use_list && ntile > 0) {
-      k_flist<<<(ntile + 255) / 256, 256, 0, c->stream>>>(G, A);
-      k_forces_list<<<c->sm_count * SWF_FORCES_MINB, NTHR, 0, c->stream>>>(G, A);
-    } else if (ntile > 0) {
-      k_forces<<<ntile, NTHR, 0, c->stream>>>(G, A);
-    }
+    listed(A.tr_lo, tr_hi);
     if (ntile > 0 && SWF_SPECULATE) k_forces_redo<<<RED_CTAS, NTHR, 0, c->stream>>>(G, A);
   } else {
     // interior tile rows [a, b): their 1-row halo stays inside the owned rows
@@ -1512,7 +1531,7 @@ int fused_enqueue_phase1(swf_ctx* c, double dt_cap, int part) {
       k_forces<<<G.tiles_x * (r_end - r_first), NTHR, 0, c->stream>>>(G, B);
     };
     if (part == 0) {
-      launch(a, b);
+      listed(a, b);  // interior rows: the list (one list per step, k_begin reset it)
     } else {
       launch(lo, a);
       launch(b, tr_hi);
