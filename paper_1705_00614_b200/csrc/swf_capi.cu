@@ -1085,6 +1085,10 @@ int swf_strip_host_phase1(swf_ctx* c, double* H, double* HUx, double* HUy, const
   invalidate_mask(c);
   if ((rc = launch_begin(c, dt_cap)) || (rc = launch_mask(c)) || (rc = fused_ingest_hu(c, HUx, HUy)))
     return rc;
+  // the owned tiles' flags describe this state: the forces list skips the
+  // dry ones (ghost and edge tile rows are always visited)
+  e = cudaMemsetAsync(&c->d_sc->mask_fresh, 1, sizeof(int), c->stream);
+  if (e != cudaSuccess) return cuda_check(c, e, "strip host mask");
   c->state_partial = 0;
   c->last_ingest_bytes = (long long)bytes + 16LL * (long long)(lo + (n - hi0));
   return swf_strip_phase1(c, dt_cap, speed_out);
