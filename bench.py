@@ -146,7 +146,12 @@ def cpu_reference(config, warmup=5, steps=30, threads=None, crop=2048):
     if kind != "reference":
         cores = 1
     n_full = {"C3": 16384, "C5": 32768}.get(config, 0)
-    if n_full:
+    if config == "C5W":  # the weak-scaling band: 8 crops along its 4096 rows
+        c = min(crop, S.WEAK_ROWS // 2)
+        wins = [(k * 4096 + 2048 - c // 2, S.WEAK_ROWS // 2 - c // 2, c, c) for k in range(8)]
+        scs = [S.build("C5", window=w) for w in wins]
+        n_full = 32768
+    elif n_full:
         c = min(crop, n_full // 8)
         wins = [(k * (n_full // 8) + (n_full // 16) - c // 2,) * 2 + (c, c) for k in range(8)]
         scs = [S.build(config, window=w) for w in wins]
@@ -177,7 +182,8 @@ def cpu_reference(config, warmup=5, steps=30, threads=None, crop=2048):
     for o in steppers:
         o.close()
     v = cells * steps / el / 1e6
-    what = (f"8 diagonal {scs[0].terrain.nx}x{scs[0].terrain.ny} crops of {config}" if n_full
+    what = (f"8 {'band' if config == 'C5W' else 'diagonal'} {scs[0].terrain.nx}x"
+            f"{scs[0].terrain.ny} crops of {config}" if n_full
             else f"{config} full grid")
     cpu = "unknown CPU"
     try:
@@ -202,7 +208,8 @@ def reference_arm(args):
     v, cores, kind, sample, per_step = cpu_reference(args.config, args.warmup, args.steps)
     line = {"metric": "cell-updates/sec (Mcells/s)", "value": round(v, 3), "unit": "Mcells/s",
             "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
+            "ms_per_step": None, "higher_is_better": True,
+            "scaling": "weak" if args.config == "C5W" else "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.config} (bounded sample on host CPU)", "grid": args.config},
             "cpu_baseline": {"value": round(v, 3), "unit": "Mcells/s", "cores": cores,
@@ -307,11 +314,15 @@ def b200_single(args):
         # the same rate over the cells of flux-active blocks
         "value_active": round(n_act * K / (ms * 1e-3) / 1e6, 3),
         "n_gpus": 1, "steps": K, "warmup": args.warmup, "ms_per_step": round(ms / K, 4),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "weak" if args.config == "C5W" else "strong",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generator, scenarios.py)",
-        "config": {"workload": f"{sc.name} {sc.terrain.nx}x{sc.terrain.ny} h={sc.terrain.h} m, " + (
+        "config": {"workload": ("C5W weak scaling, one GPU's share: " if args.config == "C5W" else "")
+                   + f"{sc.name} {sc.terrain.nx}x{sc.terrain.ny} h={sc.terrain.h} m, " + (
                        "all physics (Manning field, wind, Coriolis, viscosity, 3 sources, open east edge)"
                        if args.config in ("C3", "C5") else
+                       f"all physics (Manning field, wind, Coriolis, viscosity, {len(sc.sources)} "
+                       "sources in the band, open east edge)" if args.config == "C5W" else
                        f"Manning n={sc.params.n_manning}, reflective edges"),
                    "cells": N, "active_fraction": round(last.active_fraction, 4),
                    "skip_dry_blocks": bool(sc.options.skip_dry_blocks),

@@ -391,7 +391,10 @@ class RankStrip:
             else:
                 dist.init_process_group(self.backend)
         self.xdev = self.dev if self.backend == "nccl" else torch.device("cpu")
-        self.n = n_full or {"C3": 16384, "C5": 32768, "C2": 2048}[config]
+        self.weak = config == "C5W"
+        self.n = n_full or {"C3": 16384, "C5": 32768, "C2": 2048, "C5W": 32768}[config]
+        # rows of the global grid: square, or 4096 per GPU for weak scaling
+        self.ny = S.WEAK_ROWS * self.world if self.weak else self.n
         # strips balanced by the initial activity of each block row (the wet
         # area is unevenly spread over the rows; equal row counts would leave
         # the busiest strip ~18 % above the mean at 8 GPUs on C3)
@@ -400,10 +403,13 @@ class RankStrip:
             wts = row_weights(config, self.n, 16, device=f"cuda:{self.local}")
             self.bounds = balanced_bounds(wts, self.world, 16, self.n)
         else:
-            self.bounds = strip_bounds(self.n, self.world, 16)
+            self.bounds = strip_bounds(self.ny, self.world, 16)
         self.j0, self.j1 = self.bounds[self.rank]
-        self.w0, self.w1 = window_rows(self.j0, self.j1, self.n)
-        if config in ("C3", "C5") and n_full:
+        self.w0, self.w1 = window_rows(self.j0, self.j1, self.ny)
+        if self.weak:
+            sc = S.build("C5", device=f"cuda:{self.local}",
+                         window=(0, self.w0, self.n, self.w1 - self.w0))
+        elif config in ("C3", "C5") and n_full:
             sc = S.floodplain(self.n, 50.0, window=(0, self.w0, self.n, self.w1 - self.w0),
                               device=f"cuda:{self.local}")
         else:
@@ -412,8 +418,8 @@ class RankStrip:
         if no_skip:
             sc.options.skip_dry_blocks = False
         self.sc = sc
-        self.strip = Strip(sc, self.n, self.j0, self.j1, sc.global_sources, sc.wind,
-                           device=self.local)
+        srcs = S.clip_sources(sc.global_sources, self.n, self.ny) if self.weak else sc.global_sources
+        self.strip = Strip(sc, self.ny, self.j0, self.j1, srcs, sc.wind, device=self.local)
         self.strip.upload(sc.state.H, sc.state.HUx, sc.state.HUy, 0.0)
 
     def _pack(self, side, t):
@@ -598,7 +604,7 @@ class RankStrip:
         if self.rank != 0:
             return None
         n = self.n
-        out = [np.empty(n * n) for _ in range(3)]
+        out = [np.empty(n * self.ny) for _ in range(3)]
         for j0, j1, o, _ in objs:
             m = (j1 - j0) * n
             for q in range(3):
@@ -609,11 +615,13 @@ class RankStrip:
 def bench_strips(args) -> Optional[dict]:
     import torch
     import torch.distributed as dist
+    from .scenarios import WEAK_ROWS as S_WEAK
 
     rs = RankStrip(args.config, no_skip=args.no_skip)
     rank, world, dev, strip, sc = rs.rank, rs.world, rs.dev, rs.strip, rs.sc
     local = rs.local
     full_n, bounds, j0, j1 = rs.n, rs.bounds, rs.j0, rs.j1
+    full_ny = rs.ny
     bs = 16
 
     use_async = rs.backend == "nccl"
@@ -664,7 +672,7 @@ def bench_strips(args) -> Optional[dict]:
     tk = strip.timing_read(K)
     t_kstep = float(tk[:, 6].mean())
     last = infos[-1]
-    N_total = full_n * full_n
+    N_total = full_n * full_ny
     n_own = (j1 - j0) * full_n
     n_act = min(n_own, last.flux_blocks * bs * bs) if sc.options.skip_dry_blocks else n_own
     per_act = 56 + (8 if sc.params.n_field is not None else 0)
@@ -725,9 +733,11 @@ def bench_strips(args) -> Optional[dict]:
         "metric": "cell-updates/sec (Mcells/s)", "value": round(value, 3), "unit": "Mcells/s",
         "value_active": round(float(nact_all.item()) * K / (ms_max * 1e-3) / 1e6, 3),
         "n_gpus": world, "steps": K, "warmup": args.warmup, "ms_per_step": round(ms_max / K, 4),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded generator, scenarios.py)",
-        "config": {"workload": f"{sc.name.split('-')[0]} {full_n}x{full_n} row strips",
+        "higher_is_better": True, "scaling": "weak" if rs.weak else "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded generator, scenarios.py)",
+        "config": {"workload": (f"C5W weak scaling: {full_n}x{full_ny} ({S_WEAK} rows per GPU) "
+                                "row strips" if rs.weak else
+                                f"{sc.name.split('-')[0]} {full_n}x{full_n} row strips"),
                    "cells": N_total, "strips": bounds, "halo_rows": HALO,
                    "parallelism": f"row strips x{world}, " + (
                        "P2P halo stored by k_step into the neighbours' ghost rows (CUDA IPC over "

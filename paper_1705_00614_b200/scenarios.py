@@ -284,4 +284,24 @@ def build(config: str, device: str = "cpu", window=None) -> Scenario:
         return nested_floodplain(device=device)
     if config == "C5":
         return floodplain(32768, 25.0, window=window, device=device)
+    if config == "C5W":  # weak scaling, one GPU's share: 32768 x 4096 rows of C5
+        return floodplain(32768, 25.0, window=window or (0, 0, 32768, WEAK_ROWS), device=device)
     raise ValueError(config)
+
+
+# rows per GPU of the weak-scaling configuration (BASELINE.json config 5)
+WEAK_ROWS = 4096
+
+
+def clip_sources(specs, nx: int, ny: int):
+    """Global source specs restricted to an nx x ny domain (the weak-scaling
+    grids are the first rows of the C5 generator; sources outside are dropped,
+    partial ones clipped)."""
+    out = []
+    for s in specs:
+        a0, b0 = max(s.cells.i0, 0), max(s.cells.j0, 0)
+        a1, b1 = min(s.cells.i1, nx - 1), min(s.cells.j1, ny - 1)
+        if a0 <= a1 and b0 <= b1:
+            out.append(SourceSpec(s.kind, s.name, CellRect(a0, b0, a1, b1), list(s.hydrograph),
+                                  s.rate, s.source_velocity))
+    return out
