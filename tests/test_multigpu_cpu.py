@@ -106,3 +106,17 @@ def test_balanced_bounds_equalise_weight():
         assert max(loads) / (sum(loads) / parts) < 1.0 + 2 * w.max() * parts / w.sum()
     eq = M.balanced_bounds(np.ones(64), 4, 16, 1024)
     assert eq == M.strip_bounds(1024, 4, 16)
+
+
+def test_weak_scaling_sources_clipped_to_the_band():
+    """C5W (weak scaling) keeps the C5 generator's first 4096*N rows; its
+    sources are clipped to them (scenarios.clip_sources)."""
+    from paper_1705_00614_b200 import scenarios as S
+    from paper_1705_00614_b200.types import CellRect, SourceKind, SourceSpec, Vec2
+    specs = [SourceSpec(SourceKind.Discharge, "a", CellRect(1, 10, 4, 20), [], 0.0, Vec2()),
+             SourceSpec(SourceKind.Rain, "b", CellRect(5, 4090, 9, 5000), [], 1e-6, Vec2()),
+             SourceSpec(SourceKind.Rain, "c", CellRect(5, 9000, 9, 9100), [], 1e-6, Vec2())]
+    out = S.clip_sources(specs, 32768, 4096)
+    assert [s.name for s in out] == ["a", "b"]
+    assert (out[1].cells.j0, out[1].cells.j1) == (4090, 4095)
+    assert S.WEAK_ROWS == 4096
