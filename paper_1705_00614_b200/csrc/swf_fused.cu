@@ -41,7 +41,11 @@ constexpr int BX = 32, BY = 16;  // tile of owned cells (k_forces and k_step)
 constexpr int AX = BX, AY = BY;
 constexpr int AREGX = AX + 2, AREGY = AY + 2, AREG = AREGX * AREGY;  // 1-cell halo
 constexpr int RX = BX + 4, RY = BY + 4, RREG = RX * RY;              // 2-cell halo
-constexpr int NTHR = 256;  // k_forces, k_reduce, k_scatter_host
+constexpr int NTHR = 256;  // k_reduce, k_scatter_host, k_ingest_hu, k_finish
+#ifndef SWF_FORCES_THREADS
+#define SWF_FORCES_THREADS 128
+#endif
+constexpr int FTHR = SWF_FORCES_THREADS;  // k_forces (whole warps)
 constexpr int MAXBF = 64;  // B-block flags of one tile staged in shared memory
 constexpr int HALO_ROWS = SWF_HALO;  // ghost rows per interior strip side (swf.h)
 #ifndef SWF_STEP_THREADS
@@ -55,7 +59,7 @@ constexpr int NPART_ALLOC = 5;  // doubles per tile in d_part (see k_reduce)
 #define SWF_STEP_MINB 3  // CTAs per SM the register budget of k_step targets
 #endif
 #ifndef SWF_FORCES_MINB
-#define SWF_FORCES_MINB 6
+#define SWF_FORCES_MINB 9
 #endif
 
 __device__ __forceinline__ bool stopped(const StepScalars* sc) { return sc->err_key != ERR_NONE; }
@@ -338,7 +342,7 @@ __device__ __forceinline__ void forces_tile(const Geo& G, const ForcesArgs& A, c
   __shared__ unsigned char s_w[AREG];
   __shared__ int s_cnt[3];
   __shared__ unsigned s_srcm;
-  __shared__ unsigned long long s_max[NTHR / 32];
+  __shared__ unsigned long long s_max[FTHR / 32];
   StepScalars* sc = A.sc;
   if (__syncthreads_or(stopped(sc))) return;
   bool sok = true;  // every speculative division of this thread accepted
@@ -377,7 +381,7 @@ __device__ __forceinline__ void forces_tile(const Geo& G, const ForcesArgs& A, c
 
   // ---- region state (all loads issued together) + wet flags (K1) ------------
   bool anywet = false;
-  for (int c = tid; c < AREG; c += NTHR) {
+  for (int c = tid; c < AREG; c += FTHR) {
     int i = i0 - 1 + c % AREGX, r = rr0 - 1 + c / AREGX;
     double d = 0.0, mx = 0.0, my = 0.0, bb = 0.0;
     unsigned char w = 0;
@@ -410,12 +414,12 @@ __device__ __forceinline__ void forces_tile(const Geo& G, const ForcesArgs& A, c
   // (the mask is fused only when bs divides 16: a power of two, so shifts)
   const int lgb = __ffs(G.bs) - 1;
   const int nbt = mask_tile ? (BX >> lgb) * (BY >> lgb) : 0;
-  const int k1w = mask_tile ? min(nbt, NTHR / 32) : 0;
+  const int k1w = mask_tile ? min(nbt, FTHR / 32) : 0;
   if (mask_tile) {
     const int bs = G.bs, lgx = 5 - lgb, nbxt = BX >> lgb;  // BX = 32 = 2^5
     const int rend = min(rr0 + BY, G.r1);
     const int lane = tid & 31, warp = tid >> 5;
-    for (int blk = warp; blk < nbt; blk += NTHR / 32) {
+    for (int blk = warp; blk < nbt; blk += FTHR / 32) {
       int bx = blk & (nbxt - 1), by = blk >> lgx;
       int bi0 = i0 + bx * bs, br0 = rr0 + by * bs;  // block origin (global col, local row)
       if (bi0 >= G.nx || br0 >= rend) continue;
@@ -464,9 +468,9 @@ __device__ __forceinline__ void forces_tile(const Geo& G, const ForcesArgs& A, c
   }
 
   // ---- region momentum -> eta, velocity ---------------------------------------
-  const int vt0 = k1w < NTHR / 32 ? 32 * k1w : 0;  // first thread of the velocity pass
+  const int vt0 = k1w < FTHR / 32 ? 32 * k1w : 0;  // first thread of the velocity pass
   if (anywet && tid >= vt0) {
-    for (int c = tid - vt0; c < AREG; c += NTHR - vt0) {  // pointwise, in place (same c)
+    for (int c = tid - vt0; c < AREG; c += FTHR - vt0) {  // pointwise, in place (same c)
       double d = s_d[c];
       double e = d + s_e[c], u = 0.0, v = 0.0;
       if (d > P.eps) {
@@ -491,7 +495,7 @@ __device__ __forceinline__ void forces_tile(const Geo& G, const ForcesArgs& A, c
   // ---- K2 forces + K3 speed on wet cells ------------------------------------
   double m = 0.0;
   const double wx = sc->wind_n[0], wy = sc->wind_n[1];
-  for (int c = tid; c < AX * AY; c += NTHR) {
+  for (int c = tid; c < AX * AY; c += FTHR) {
     int x = c % AX, y = c / AX;
     int i = i0 + x, r = rr0 + y;
     if (i >= G.nx || r < fa || r >= fb) continue;
@@ -527,14 +531,14 @@ __device__ __forceinline__ void forces_tile(const Geo& G, const ForcesArgs& A, c
       A.redo[atomicAdd(&sc->redo_n[0], 1)] = tx + (tr + REDO_ROW0) * G.tiles_x;
     } else {
       unsigned long long mb = 0;
-      for (int w = 0; w < NTHR / 32; ++w) mb = s_max[w] > mb ? s_max[w] : mb;
+      for (int w = 0; w < FTHR / 32; ++w) mb = s_max[w] > mb ? s_max[w] : mb;
       // spread over SPEED_SLOTS addresses to avoid one contended L2 atomic
       if (mb) atomicMax(&sc->speed_slots[(tx + tr * 7) & (SPEED_SLOTS - 1)], mb);
     }
   }
 }
 
-__global__ void __launch_bounds__(NTHR, SWF_FORCES_MINB) k_forces(Geo G, ForcesArgs A) {
+__global__ void __launch_bounds__(FTHR, SWF_FORCES_MINB) k_forces(Geo G, ForcesArgs A) {
   const int tx = blockIdx.x % G.tiles_x, tr = (int)(blockIdx.x / G.tiles_x) + A.tr_lo;
   forces_tile<SWF_SPECULATE != 0>(G, A, tx, tr);
 }
@@ -596,7 +600,7 @@ __global__ void k_flist(Geo G, ForcesArgs A) {
   append_ordered(A.list, &sc->list_n[0], busy, t);
 }
 
-__global__ void __launch_bounds__(NTHR, SWF_FORCES_MINB) k_forces_list(Geo G, ForcesArgs A) {
+__global__ void __launch_bounds__(FTHR, SWF_FORCES_MINB) k_forces_list(Geo G, ForcesArgs A) {
   __shared__ int s_next;
   StepScalars* sc = A.sc;
   const int n = *(volatile int*)&sc->list_n[0];
@@ -613,7 +617,7 @@ __global__ void __launch_bounds__(NTHR, SWF_FORCES_MINB) k_forces_list(Geo G, Fo
 }
 
 // the tiles with a rejected speculative division, recomputed exactly
-__global__ void __launch_bounds__(NTHR, SWF_FORCES_MINB) k_forces_redo(Geo G, ForcesArgs A) {
+__global__ void __launch_bounds__(FTHR, SWF_FORCES_MINB) k_forces_redo(Geo G, ForcesArgs A) {
   const int n = *(volatile int*)&A.sc->redo_n[0];
   for (int q = blockIdx.x; q < n; q += gridDim.x) {
     int e = A.redo[q];
@@ -1508,16 +1512,16 @@ int fused_enqueue_phase1(swf_ctx* c, double dt_cap, int part) {
     int ntile = G.tiles_x * (r_end - r_first);
     if (SWF_TILE_LISTS && fm) {
       k_flist<<<(ntile + 255) / 256, 256, 0, c->stream>>>(G, B);
-      k_forces_list<<<c->sm_count * SWF_FORCES_MINB, NTHR, 0, c->stream>>>(G, B);
+      k_forces_list<<<c->sm_count * SWF_FORCES_MINB, FTHR, 0, c->stream>>>(G, B);
     } else {
       B.tr_lo = r_first;
-      k_forces<<<ntile, NTHR, 0, c->stream>>>(G, B);
+      k_forces<<<ntile, FTHR, 0, c->stream>>>(G, B);
     }
   };
   if (part < 0) {
     int ntile = G.tiles_x * (tr_hi - A.tr_lo);
     listed(A.tr_lo, tr_hi);
-    if (ntile > 0 && SWF_SPECULATE) k_forces_redo<<<RED_CTAS, NTHR, 0, c->stream>>>(G, A);
+    if (ntile > 0 && SWF_SPECULATE) k_forces_redo<<<RED_CTAS, FTHR, 0, c->stream>>>(G, A);
   } else {
     // interior tile rows [a, b): their 1-row halo stays inside the owned rows
     int a = G.r0 > 0 ? 1 : 0;
@@ -1528,14 +1532,14 @@ int fused_enqueue_phase1(swf_ctx* c, double dt_cap, int part) {
       if (r_end <= r_first) return;
       ForcesArgs B = A;
       B.tr_lo = r_first;
-      k_forces<<<G.tiles_x * (r_end - r_first), NTHR, 0, c->stream>>>(G, B);
+      k_forces<<<G.tiles_x * (r_end - r_first), FTHR, 0, c->stream>>>(G, B);
     };
     if (part == 0) {
       listed(a, b);  // interior rows: the list (one list per step, k_begin reset it)
     } else {
       launch(lo, a);
       launch(b, tr_hi);
-      if (SWF_SPECULATE) k_forces_redo<<<RED_CTAS, NTHR, 0, c->stream>>>(G, A);
+      if (SWF_SPECULATE) k_forces_redo<<<RED_CTAS, FTHR, 0, c->stream>>>(G, A);
     }
   }
   if (part != 0) ev(c, 2);
