@@ -435,9 +435,27 @@ def b200_multi(args):
         dist.destroy_process_group()
 
 
+def relaunch_under_torchrun(args) -> int:
+    """`python bench.py --gpus N` without an external launcher: re-execute
+    this script under torch.distributed.run, one rank per GPU (the driver's
+    own launch line), and return its exit code.  With fewer visible GPUs than
+    N the ranks share devices round-robin (the same code path)."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"bench.py: relaunching under torchrun with {args.gpus} ranks", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
+    if args.gpus > 1 and "RANK" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args))
     if args.impl == "reference":
         reference_arm(args)
         return

@@ -270,15 +270,27 @@ int swf_strip_unpack(swf_ctx* ctx, int side, const double* src);
  *              (exchange done) unpack_async(side)
  *              swf_strip_forces(ctx, dt_cap, 1)   ghost-dependent tile rows
  *              swf_strip_local_speed(ctx, dev)    strip CFL speed -> device
- *              (allreduce-MAX of dev across strips, on the device)
+ *              (allreduce-MAX of dev across strips, on the device, over the
+ *               8 bytes as int64: a stopped strip publishes a marker above
+ *               every speed, and every strip's finish then stops as well)
  *              swf_strip_finish(ctx, dev, dt_cap) tau from *dev, K4..K8
  *   swf_strip_end_batch(ctx, &done, &last)        sync + commit (like swf_run)
+ *   (allreduce-MIN of done across strips)
+ *   swf_strip_settle(ctx, ok)                     commit ok = min(done) steps
+ * A strip that aborts in step k stops the others in step k + 1 (before their
+ * K4..K8), so every strip has done ok or ok + 1 steps and settle rolls the
+ * latter back by one (the other ping-pong buffer, the previous t).  A strip
+ * stopped only by that marker reports SWF_ENUMERICAL "strip stopped: ...".
  * Every call is enqueued on the context stream (swf_stream). */
 int swf_strip_begin_batch(swf_ctx* ctx);
 int swf_strip_forces(swf_ctx* ctx, double dt_cap, int part);
 int swf_strip_local_speed(swf_ctx* ctx, double* dev_out);
 int swf_strip_finish(swf_ctx* ctx, const double* dev_global_speed, double dt_cap);
 int swf_strip_end_batch(swf_ctx* ctx, int* done, swf_step_info* last);
+int swf_strip_settle(swf_ctx* ctx, int ok);
+/* steps the last batch committed on this strip (after swf_strip_end_batch,
+ * also when it returned an error) */
+int swf_strip_steps_done(const swf_ctx* ctx);
 int swf_strip_pack_async(swf_ctx* ctx, int side, double* dst);
 int swf_strip_unpack_async(swf_ctx* ctx, int side, const double* src);
 /* P2P halo (fused exchange): the base pointers of this context's six state

@@ -77,6 +77,12 @@ def declare(lib):
     _sig(lib, "swf_strip_local_speed", I, P, C.c_void_p)
     _sig(lib, "swf_strip_finish", I, P, C.c_void_p, D)
     _sig(lib, "swf_strip_end_batch", I, P, PI, PN)
+    _sig(lib, "swf_strip_settle", I, P, I)
+    _sig(lib, "swf_group_create", I, C.POINTER(P), I, C.POINTER(P))
+    _sig(lib, "swf_group_run", I, P, I, D, PI, PN)
+    _sig(lib, "swf_group_last_error", C.c_char_p, P)
+    _sig(lib, "swf_group_destroy", V, P)
+    _sig(lib, "swf_strip_steps_done", I, P)
     _sig(lib, "swf_strip_host_phase1", I, P, C.c_void_p, C.c_void_p, C.c_void_p, PD, D, PD)
     _sig(lib, "swf_strip_host_phase2", I, P, C.c_void_p, C.c_void_p, C.c_void_p, PD, D, D, PN)
     _sig(lib, "swf_strip_pack_async", I, P, I, C.c_void_p)

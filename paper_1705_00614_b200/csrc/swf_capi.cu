@@ -65,6 +65,8 @@ int check_device_error(swf_ctx* c) {
              c->h_sc->err_val[0], c->h_sc->err_val[1], c->h_sc->err_val[2]);
     return set_err(c, SWF_ENUMERICAL, buf);
   }
+  if (kind == ERR_PEER)
+    return set_err(c, SWF_ENUMERICAL, "strip stopped: another strip of the group aborted the step");
   unsigned long long ib = (key >> 24) & ((1ull << 34) - 1);
   unsigned long long low = key & ((1ull << 24) - 1);
   int bi = (int)(ib % G.nbx), bj = (int)(ib / G.nbx);
@@ -1008,15 +1010,10 @@ int swf_dev_bottom_friction(int n, const double* in, double g, double nm, double
 // ---------------------------------------------------------------------------
 extern "C" {
 
-int swf_strip_phase1(swf_ctx* c, double dt_cap, double* speed_out) {
-  if (c->state_partial)
-    return set_err(c, SWF_ECONFIG,
-                   "the device state is incomplete after a pinned host-buffer step (sparse "
-                   "momentum ingest); upload a state first");
-  cudaSetDevice(c->device);
-  int rc = reset_counters(c);
-  if (rc) return rc;
-  rc = fused_enqueue_phase1(c, dt_cap);
+// The forces of a strip step and its CFL speed; `part` as fused_enqueue_phase1
+// (-1: with k_begin, -2: the caller has enqueued k_begin and the mask).
+static int strip_phase1_body(swf_ctx* c, double dt_cap, double* speed_out, int part) {
+  int rc = fused_enqueue_phase1(c, dt_cap, part);
   if (rc) return rc;
   cudaError_t e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) return cuda_check(c, e, "strip phase 1");
@@ -1028,6 +1025,17 @@ int swf_strip_phase1(swf_ctx* c, double dt_cap, double* speed_out) {
   for (int q = 0; q < SPEED_SLOTS; ++q) mb = c->h_sc->speed_slots[q] > mb ? c->h_sc->speed_slots[q] : mb;
   if (speed_out) *speed_out = bitsd(mb);
   return SWF_OK;
+}
+
+int swf_strip_phase1(swf_ctx* c, double dt_cap, double* speed_out) {
+  if (c->state_partial)
+    return set_err(c, SWF_ECONFIG,
+                   "the device state is incomplete after a pinned host-buffer step (sparse "
+                   "momentum ingest); upload a state first");
+  cudaSetDevice(c->device);
+  int rc = reset_counters(c);
+  if (rc) return rc;
+  return strip_phase1_body(c, dt_cap, speed_out, -1);
 }
 
 int swf_strip_phase2(swf_ctx* c, double global_speed, double dt_cap, swf_step_info* info) {
@@ -1091,7 +1099,8 @@ int swf_strip_host_phase1(swf_ctx* c, double* H, double* HUx, double* HUy, const
   if (e != cudaSuccess) return cuda_check(c, e, "strip host mask");
   c->state_partial = 0;
   c->last_ingest_bytes = (long long)bytes + 16LL * (long long)(lo + (n - hi0));
-  return swf_strip_phase1(c, dt_cap, speed_out);
+  // counters reset and k_begin / k_mask enqueued above: the forces only
+  return strip_phase1_body(c, dt_cap, speed_out, -2);
 }
 
 int swf_strip_host_phase2(swf_ctx* c, double* H, double* HUx, double* HUy, double* t,
@@ -1207,6 +1216,31 @@ int swf_strip_end_batch(swf_ctx* c, int* done, swf_step_info* last) {
   return rc;
 }
 
+int swf_strip_steps_done(const swf_ctx* c) { return c && c->h_sc ? c->h_sc->steps_done : 0; }
+
+int swf_strip_settle(swf_ctx* c, int ok) {
+  cudaSetDevice(c->device);
+  const int done = c->h_sc->steps_done;
+  if (ok == done) return SWF_OK;
+  if (ok != done - 1 || ok < 0)
+    return set_err(c, SWF_ECONFIG, "strip_settle: the strips are more than one step apart");
+  // the step this strip finished beyond the others: its input buffer still
+  // holds the state after `ok` steps (every strip stopped before the next
+  // K4..K8), and k_finish kept the time before it
+  cudaError_t e = cudaMemcpy(c->h_sc, c->d_sc, sizeof(StepScalars), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_check(c, e, "strip settle");
+  const double t = c->h_sc->t_prev;
+  c->h_sc->t = t;
+  c->h_sc->steps_done = ok;
+  e = cudaMemcpy(&c->d_sc->t, &t, sizeof(double), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(&c->d_sc->steps_done, &ok, sizeof(int), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_check(c, e, "strip settle");
+  c->cur ^= 1;
+  c->h_t = t;
+  invalidate_mask(c);
+  return SWF_OK;
+}
+
 int swf_strip_pack_async(swf_ctx* c, int side, double* dst) {
   cudaSetDevice(c->device);
   double *s3[3], *r3[3];
@@ -1228,11 +1262,10 @@ int swf_strip_unpack_async(swf_ctx* c, int side, const double* src) {
   for (int q = 0; q < 3 && e == cudaSuccess && count; ++q)
     e = cudaMemcpyAsync(r3[q], src + q * count, count * sizeof(double), cudaMemcpyDeviceToDevice,
                         c->stream);
-  if (e == cudaSuccess) {
-    // the ghost rows changed outside the fused path: their tiles' dry-skip
-    // flags are no longer valid (k_forces never skips strip-boundary tiles,
-    // so nothing else to do)
-  }
+  // The ghost rows changed outside the fused path.  Their tiles' dry-skip
+  // flags need no update: k_flist always lists a strip's ghost tile rows and
+  // the tile rows next to its edges (the `edge` rule there), so no tile that
+  // reads a ghost row is ever skipped on stale flags.
   return cuda_check(c, e, "strip unpack");
 }
 
@@ -1293,6 +1326,7 @@ struct swf_group {
   std::vector<double*> gspeed;    // per strip (its device): the group maximum
   double** d_in = nullptr;        // on strip 0's device: speed[] / gspeed[] pointers
   double** d_out = nullptr;
+  StepScalars** d_sc = nullptr;   // on strip 0's device: every strip's step scalars
   std::vector<cudaEvent_t> ev_speed, ev_step;
   cudaEvent_t ev_max = nullptr;
   std::string err;
@@ -1301,9 +1335,22 @@ struct swf_group {
 namespace {
 
 // the exact maximum of the strips' speeds (non-negative doubles), written to
-// every strip's device (peer stores)
-__global__ void k_group_max(double* const* in, double* const* out, int n) {
+// every strip's device (peer stores).  It also stops the whole group once any
+// strip has aborted: a per-cell error (CFL displacement, non-finite flux) in
+// one strip's k_step of step k is seen here in step k+1 (this kernel runs
+// after every strip's phase 1 of k+1, hence after every k_step of k), and the
+// other strips get ERR_PEER, so none of them runs k_step of k+1.  Every strip
+// then holds its committed state of step k in the parity buffer the commit
+// picks (swf_group_run), and no healthy strip has overwritten it.
+__global__ void k_group_max(double* const* in, double* const* out, StepScalars* const* sc,
+                            int n) {
   if (threadIdx.x != 0) return;
+  bool stop = false;
+  for (int d = 0; d < n; ++d) stop = stop || *(volatile unsigned long long*)&sc[d]->err_key != ERR_NONE;
+  if (stop) {
+    for (int d = 0; d < n; ++d) atomicMin(&sc[d]->err_key, ERR_PEER << 58);
+    return;
+  }
   double m = 0.0;
   for (int d = 0; d < n; ++d) m = in[d][0] > m ? in[d][0] : m;
   for (int d = 0; d < n; ++d) out[d][0] = m;
@@ -1348,6 +1395,7 @@ void swf_group_destroy(swf_group* g) {
     cudaSetDevice(g->s[0]->device);
     cudaFree(g->d_in);
     cudaFree(g->d_out);
+    cudaFree(g->d_sc);
     if (g->ev_max) cudaEventDestroy(g->ev_max);
   }
   delete g;
@@ -1398,6 +1446,12 @@ int swf_group_create(swf_ctx* const* strips, int n, swf_group** out) {
     if (e == cudaSuccess) e = cudaMalloc(&g->d_out, n * sizeof(double*));
     if (e == cudaSuccess) e = cudaMemcpy(g->d_in, g->speed.data(), n * sizeof(double*), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(g->d_out, g->gspeed.data(), n * sizeof(double*), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_sc, n * sizeof(StepScalars*));
+    if (e == cudaSuccess) {
+      std::vector<StepScalars*> scs(n);
+      for (int d = 0; d < n; ++d) scs[d] = strips[d]->d_sc;
+      e = cudaMemcpy(g->d_sc, scs.data(), n * sizeof(StepScalars*), cudaMemcpyHostToDevice);
+    }
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g->ev_max, cudaEventDisableTiming);
   }
   if (e != cudaSuccess) {
@@ -1462,7 +1516,7 @@ int swf_group_run(swf_group* g, int nsteps, double dt_cap, int* done, swf_step_i
     swf_ctx* c0 = g->s[0];
     cudaSetDevice(c0->device);
     for (int d = 0; d < n; ++d) cudaStreamWaitEvent(c0->stream, g->ev_speed[d], 0);
-    k_group_max<<<1, 32, 0, c0->stream>>>(g->d_in, g->d_out, n);
+    k_group_max<<<1, 32, 0, c0->stream>>>(g->d_in, g->d_out, g->d_sc, n);
     cudaEventRecord(g->ev_max, c0->stream);
     for (int d = 0; d < n && !rc; ++d) {
       swf_ctx* c = g->s[d];
@@ -1480,6 +1534,8 @@ int swf_group_run(swf_group* g, int nsteps, double dt_cap, int* done, swf_step_i
     cudaSetDevice(c->device);
     cudaError_t e = cudaStreamSynchronize(c->stream);
     rcs[d] = e != cudaSuccess ? cuda_check(c, e, "group run") : check_device_error(c);
+    // a strip stopped only because another one aborted reports nothing itself
+    if (rcs[d] == SWF_ENUMERICAL && (c->h_sc->err_key >> 58) == ERR_PEER) rcs[d] = SWF_OK;
     ok = std::min(ok, c->h_sc->steps_done);
     if (rcs[d] && (first < 0 || (rcs[d] == SWF_ENUMERICAL && rcs[first] != SWF_ENUMERICAL))) first = d;
   }

@@ -59,6 +59,10 @@ constexpr int NPART_ALLOC = 5;  // doubles per tile in d_part (see k_reduce)
 #define SWF_STEP_MINB 3  // CTAs per SM the register budget of k_step targets
 #endif
 #ifndef SWF_FORCES_MINB
+// 9 CTAs of 128 threads per SM caps k_forces at 56 registers; ptxas then
+// spills 12-20 B per thread in k_forces_list / k_forces_redo (L1-resident).
+// Measured as the best trade-off (profiles/README.md, rounds 2t-2v: 128 x 9
+// 3.125 ms, 128 x 8 3.134, 128 x 7 3.27, 256 x 6 3.58).
 #define SWF_FORCES_MINB 9
 #endif
 
@@ -140,6 +144,10 @@ __global__ void k_tau(Geo G, const DevSrc* src, const double* ht, const double* 
   unsigned long long mb = sc->speed_bits;
   for (int q = 0; q < SPEED_SLOTS; ++q) mb = sc->speed_slots[q] > mb ? sc->speed_slots[q] : mb;
   sc->speed_bits = mb;
+  if (gspeed && dbits(*gspeed) == SPEED_STOP_BITS) {  // another strip has stopped
+    atomicMin(&sc->err_key, ERR_PEER << 58);
+    return;
+  }
   double speed = gspeed ? *gspeed : (global_speed >= 0.0 ? global_speed : bitsd(mb));
   double tau = G.dt_max;
   if (speed > 0.0) {
@@ -409,8 +417,9 @@ __device__ __forceinline__ void forces_tile(const Geo& G, const ForcesArgs& A, c
   // One warp per block: interior cells and the clamped one-cell ring
   // (corners included, block.cpp:36-56) counted with ballots; no atomics on
   // global counters — the per-tile counts go to the diagnostics partials.
-  // K1 runs on the first min(nbt, 8) warps while the others convert the
-  // region to eta/velocity (independent: K1 reads only the wet flags)
+  // K1 runs on the first min(nbt, FTHR/32) warps while the others convert
+  // the region to eta/velocity (independent: K1 reads only the wet flags;
+  // with FTHR = 128 and 16-cell blocks all 4 warps count, then convert)
   // (the mask is fused only when bs divides 16: a power of two, so shifts)
   const int lgb = __ffs(G.bs) - 1;
   const int nbt = mask_tile ? (BX >> lgb) * (BY >> lgb) : 0;
@@ -1365,6 +1374,7 @@ __global__ void k_finish(const double* red, int nred, StepScalars* sc, double ar
     sc->lag_act = (int)w[3];
     sc->flux_act = (int)w[4];
   }
+  sc->t_prev = sc->t;
   sc->t += sc->tau;  // stepper.cpp:703
   sc->steps_done += 1;
   sc->mask_valid = 1;
@@ -1461,15 +1471,19 @@ int launch_mid(swf_ctx* c, double tau) {
   return cuda_check(c, cudaGetLastError(), "k_mid");
 }
 
-// part: -1 = the whole phase (begin + every forces tile row); 0 = begin +
-// the tile rows that read no ghost row (a strip's interior, computable while
-// its halo exchange is in flight); 1 = the remaining (ghost-dependent) rows.
+// part: -1 = the whole phase (begin + every forces tile row); -2 = every
+// forces tile row, k_begin (and k_mask) already enqueued by the caller (the
+// host-buffer strip step); 0 = begin + the tile rows that read no ghost row
+// (a strip's interior, computable while its halo exchange is in flight);
+// 1 = the remaining (ghost-dependent) rows.
 int fused_enqueue_phase1(swf_ctx* c, double dt_cap, int part) {
   const Geo& G = c->geo;
   int rc;
   bool fm = mask_fused(G);
   if (part == 0 && !fm) return set_err(c, SWF_ECONFIG, "split phase 1 needs a block size dividing 16");
-  if (part <= 0) {
+  if (part == -2) {
+    part = -1;
+  } else if (part <= 0) {
     ev(c, 0);
     if ((rc = launch_begin(c, dt_cap))) return rc;
     if (!fm && (rc = launch_mask(c))) return rc;
@@ -1550,6 +1564,10 @@ int fused_enqueue_phase1(swf_ctx* c, double dt_cap) { return fused_enqueue_phase
 
 // this context's CFL speed (max over the per-CTA slots) into a device double
 __global__ void k_local_speed(const StepScalars* sc, double* out) {
+  if (stopped(sc)) {  // the stop travels through the speed allreduce
+    *out = bitsd(SPEED_STOP_BITS);
+    return;
+  }
   unsigned long long mb = sc->speed_bits;
   for (int q = 0; q < SPEED_SLOTS; ++q) mb = sc->speed_slots[q] > mb ? sc->speed_slots[q] : mb;
   *out = bitsd(mb);

@@ -26,6 +26,7 @@ constexpr int SPEED_SLOTS = 64;
 // Device-resident per-step scalars.
 struct StepScalars {
   double t;      // FlowState::t on the device
+  double t_prev; // t before the last committed step (swf_strip_settle)
   double tau;    // this step's tau
   double t_mid;  // t + 0.5*tau
   double dt_cap;
@@ -48,8 +49,14 @@ struct StepScalars {
   int list_take[2];  // work-list cursors of the persistent grids
 };
 
-enum ErrKind : unsigned long long { ERR_DT = 1, ERR_CFL = 2, ERR_FLUX = 3 };
+// ERR_PEER: stopped because another strip of a swf_group aborted (ranks
+// above every real error, so atomicMin keeps a strip's own error)
+enum ErrKind : unsigned long long { ERR_DT = 1, ERR_CFL = 2, ERR_FLUX = 3, ERR_PEER = 7 };
 constexpr unsigned long long ERR_NONE = ~0ull;
+// A strip that has stopped publishes this as its CFL speed (the bits of a NaN
+// above every non-negative double's bits): an int64 allreduce-MAX of the
+// speeds then carries the stop to every rank, whose k_tau stops too.
+constexpr unsigned long long SPEED_STOP_BITS = 0x7fffffffffffffffull;
 
 // Launch-invariant parameters of one context (passed by value to kernels).
 struct Geo {

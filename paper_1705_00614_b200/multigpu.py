@@ -240,6 +240,12 @@ class Strip:
         self._rc(self._lib.swf_strip_end_batch(self.ctx, C.byref(done), C.byref(info)))
         return done.value, info_from_c(info)
 
+    def steps_done(self) -> int:
+        return int(self._lib.swf_strip_steps_done(self.ctx))
+
+    def settle(self, ok: int):
+        self._rc(self._lib.swf_strip_settle(self.ctx, int(ok)))
+
     def pack_async(self, side: int, dev_ptr: int):
         self._rc(self._lib.swf_strip_pack_async(self.ctx, side, C.c_void_p(dev_ptr)))
 
@@ -353,12 +359,30 @@ def local_steps_async(strips: Sequence[Strip], n: int, dt_cap: float = 0.0):
             s.forces(1, dt_cap)
             s.local_speed(speeds[r:r + 1].data_ptr())
         torch.cuda.synchronize()
-        torch.max(speeds, dim=0, keepdim=True, out=(gmax, torch.empty(1, dtype=torch.int64, device="cuda")))
+        # the MAX over the int64 view of the speeds (like the NCCL path)
+        gmax.view(torch.int64).copy_(speeds.view(torch.int64).max().reshape(1))
         torch.cuda.synchronize()
         for s in strips:
             s.finish(gmax.data_ptr(), dt_cap)
         torch.cuda.synchronize()
-    return [s.end_batch() for s in strips]
+    res, errs = [], []
+    for s in strips:
+        try:
+            res.append(s.end_batch())
+            errs.append(None)
+        except Exception as e:  # noqa: BLE001 -- re-raised below
+            res.append((s.steps_done(), None))
+            errs.append(e)
+    ok = min(r[0] for r in res)
+    for s in strips:
+        s.settle(ok)
+    for e in errs:  # the first strip's own error (not a peer stop) wins
+        if e is not None and "strip stopped" not in str(e):
+            raise e
+    for e in errs:
+        if e is not None:
+            raise e
+    return res
 
 
 # ---------------------------------------------------------------------------
@@ -382,9 +406,13 @@ class RankStrip:
         torch.cuda.set_device(self.local)
         self.dev = torch.device("cuda", self.local)
         self.backend = os.environ.get("SWF_DIST_BACKEND", "nccl")
-        # rank 0 prints exactly one JSON line: keep NCCL's version banner off stdout
+        # rank 0 prints exactly one JSON line on stdout: NCCL's log goes to
+        # stderr, at INFO for the communicator set-up (rank count, transports,
+        # NVLS) unless the caller chose a level
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
-            os.environ["NCCL_DEBUG"] = "WARN"
+            os.environ["NCCL_DEBUG"] = "INFO"
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         if not dist.is_initialized():
             if self.backend == "nccl":
                 dist.init_process_group("nccl", device_id=self.dev)
@@ -584,11 +612,31 @@ class RankStrip:
                     self.strip.unpack_async(side, rbuf.data_ptr())
                 self.strip.forces(1, dt_cap)
             self.strip.local_speed(self._speed.data_ptr())
-            dist.all_reduce(self._speed, op=dist.ReduceOp.MAX)
+            # int64 MAX over the speed bits: exact for non-negative doubles,
+            # and a stopped strip's marker (swf.h) wins and stops every rank
+            dist.all_reduce(self._speed.view(torch.int64), op=dist.ReduceOp.MAX)
             self.strip.finish(self._speed.data_ptr(), dt_cap)
 
     def end_async(self):
-        return self.strip.end_batch()
+        """Synchronise the batch and commit the same number of steps on every
+        rank: a rank that aborted in step k stopped the others in step k + 1,
+        so the ranks that finished one step more roll it back
+        (swf_strip_settle).  Errors are raised after the settlement."""
+        import torch
+        import torch.distributed as dist
+        err, res = None, None
+        try:
+            res = self.strip.end_batch()
+            done = res[0]
+        except Exception as e:  # noqa: BLE001 -- re-raised below
+            err, done = e, self.strip.steps_done()
+        t = torch.tensor([done], dtype=torch.int64, device=self.xdev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        ok = int(t.item())
+        self.strip.settle(ok)
+        if err is not None:
+            raise err
+        return (ok, res[1]) if ok == res[0] else (ok, None)
 
     def gather_state(self):
         """Full-grid state on rank 0 (None elsewhere)."""

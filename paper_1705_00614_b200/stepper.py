@@ -163,6 +163,11 @@ class CsphTvdStepper:
             raise ConfigError("stepper: state does not match the terrain grid")
         for name in ("H", "HUx", "HUy"):
             a = getattr(state, name)
+            # the native entry points read and write nx*ny doubles: a wrongly
+            # sized array is a config error before any copy or native call
+            if np.size(a) != self._n:
+                raise ConfigError(f"stepper: state array {name} has {np.size(a)} cells, "
+                                  f"the terrain grid {self._n}")
             if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags["C_CONTIGUOUS"]
                     and a.size == self._n):
                 setattr(state, name, np.ascontiguousarray(a, dtype=np.float64).reshape(-1).copy())

@@ -37,6 +37,8 @@ def info_dict(i):
 
 def run_case(sc, steps, dt_cap=0.0):
     st = sc.state.copy()
+    # OpenMP workers do not change the reference's bits
+    sc.options.workers = os.cpu_count() or 1
     o = pyorc.OracleStepper(sc.terrain, sc.params, sc.control, sc.options, kind="ref")
     if sc.wind.any():
         o.set_wind(sc.wind)
@@ -56,8 +58,49 @@ CASES = {
     "lake128": (lambda: S.lake_at_rest(128), 200, 0.0),
 }
 
+# BASELINE.json configs at their stated sizes (VERDICT r1 "parity at the
+# configs' stated sizes"): digests only (the arrays are 32-96 MB each), plus
+# every step's tau.  make_golden.py --big regenerates them (several minutes).
+BIG_CASES = {
+    # C2: 2048^2 circular dam break, h = 8 m, n = 0.03, radius 256 cells, 1000 steps
+    "c2_2048_full": (lambda: S.circular_dam_break(2048, 8.0, 256, n_manning=0.03), 1000, 0.0),
+    # C3: the wettest of the bench's 8 diagonal 2048^2 crops (48.8 % wet), 200 steps
+    "c3_crop2048_k5": (lambda: S.build("C3", window=(10240, 10240, 2048, 2048)), 200, 0.0),
+    # C5 (h = 25 m, all physics): a 1024^2 crop with a wet/dry mix and the rain
+    # source over its north-east quadrant, 200 steps
+    "c5_crop1024_rain": (lambda: S.build("C5", window=(3584, 19968, 1024, 1024)), 200, 0.0),
+}
+
+
+def big():
+    pyorc.build()
+    path = os.path.join(HERE, "golden_big.json")
+    out = {"generator": "tests/golden/make_golden.py --big",
+           "reference": "/root/reference/proj (compiled by oracle/Makefile)", "cases": {}}
+    if os.path.exists(path):
+        with open(path) as f:
+            out["cases"].update(json.load(f)["cases"])
+    for name, (fac, steps, cap) in BIG_CASES.items():
+        if name in out["cases"] and "--redo" not in sys.argv:
+            continue
+        sc = fac()
+        import time
+        t0 = time.time()
+        st, infos = run_case(sc, steps, cap)
+        out["cases"][name] = {"steps": steps, "dt_cap": cap, "cells": sc.cells(), "t": st.t.hex(),
+                              "sha256": digest(st), "last_info": info_dict(infos[-1]),
+                              "taus": [i.tau.hex() for i in infos],
+                              "wet_cells_end": int((st.H > sc.params.eps_dry).sum()),
+                              "ref_seconds": round(time.time() - t0, 1)}
+        print(name, st.t, out["cases"][name]["sha256"][:16], f"{time.time() - t0:.1f} s", flush=True)
+        with open(path, "w") as f:
+            json.dump(out, f, indent=1)
+
 
 def main():
+    if "--big" in sys.argv:
+        big()
+        return
     pyorc.build()
     out = {"generator": "tests/golden/make_golden.py", "reference": "/root/reference/proj (compiled by oracle/Makefile)",
            "cases": {}, "kat": {}}

@@ -197,16 +197,28 @@ def test_host_step_pinned_write_back(gpu_cls, oracle_built):
 
 # ------------------------------------------------------------ stage API parity
 
+def _kind(oracle_built, kind):
+    """'orc' = the C restatement; 'ref' = the REAL reference compiled from
+    /root/reference (oracle/_ref/libswflood_ref.so, which travels to the GPU
+    box with the snapshot) -- compared directly, not through the restatement."""
+    if kind == "ref" and not oracle_built.available("ref"):
+        pytest.skip("the compiled reference (oracle/_ref) is not present")
+    return kind
+
+
+@pytest.mark.parametrize("kind", ["orc", "ref"])
 @pytest.mark.parametrize("skip", [True, False])
-def test_stagewise_against_oracle(gpu_cls, oracle_built, skip):
+def test_stagewise_against_oracle(gpu_cls, oracle_built, skip, kind):
     sc = S.floodplain(96, 50.0)
     sc.options.skip_dry_blocks = skip
-    a = make(oracle_built.OracleStepper, sc, kind="orc")
+    a = make(oracle_built.OracleStepper, sc, kind=_kind(oracle_built, kind))
     b = make(gpu_cls, sc)
     sa, sb = sc.state.copy(), sc.state.copy()
     names = ["fn_fx", "fn_fy", "fn_fric_x", "fn_fric_y", "fn_sigma", "fm_fx", "fm_fy",
              "fm_fric_x", "fm_fric_y", "fm_sigma", "half_H", "half_HUx", "half_HUy", "Ht",
              "HVtx", "HVty", "drx", "dry", "Fh", "Fvx", "Fvy", "sigma", "src_vx", "src_vy"]
+    if kind == "ref":  # the reference's accessors (stepper.hpp:102-119) have no half momenta
+        names = [nm for nm in names if nm not in ("half_HUx", "half_HUy")]
     for step in range(5):
         for o, s in ((a, sa), (b, sb)):
             o.begin_step(s)
@@ -265,9 +277,10 @@ def test_skip_and_block_size_equivalence(gpu_cls, bs):
     assert_state_bitwise(st, st_ref, f"B={bs}")
 
 
-def test_medium_floodplain_vs_oracle(gpu_cls, oracle_built):
+@pytest.mark.parametrize("kind", ["orc", "ref"])
+def test_medium_floodplain_vs_oracle(gpu_cls, oracle_built, kind):
     sc = S.floodplain(16384, 50.0, window=(7000, 7600, 300, 260))  # a crop of C3
-    a = make(oracle_built.OracleStepper, sc, kind="orc")
+    a = make(oracle_built.OracleStepper, sc, kind=_kind(oracle_built, kind))
     b = make(gpu_cls, sc)
     sa, sb = sc.state.copy(), sc.state.copy()
     for _ in range(8):
@@ -576,3 +589,18 @@ def test_non_finite_state_raises_like_the_reference(gpu_cls, oracle_built, what)
         assert str(eg.value) == str(eo.value), (mode, str(eg.value), str(eo.value))
         np.testing.assert_array_equal(a.H, before.H)
         np.testing.assert_array_equal(np.isnan(a.HUx), np.isnan(before.HUx))
+
+
+def test_wrong_sized_state_arrays_are_a_config_error(gpu_cls):
+    """a state array whose length is not nx*ny is rejected before
+    any copy or native call (the native entry points read and write nx*ny
+    doubles), by step, upload and download alike."""
+    from paper_1705_00614_b200 import ConfigError
+    sc = S.floodplain(32, 50.0)
+    s = make(gpu_cls, sc)
+    for f in ("H", "HUx", "HUy"):
+        st = sc.state.copy()
+        setattr(st, f, getattr(st, f)[:-5].copy())
+        for call in (s.step, s.upload, s.download):
+            with pytest.raises(ConfigError, match=f"state array {f}"):
+                call(st)
