@@ -230,6 +230,40 @@ int swf_dev_cbrt(int n, const double* x, double* y);
 /* bottom_friction, forcing.cpp:26-28: in = n x {ux,uy,H}, out = n x {fx,fy}. */
 int swf_dev_bottom_friction(int n, const double* in, double g, double n_manning,
                             double* out);
+/* assemble_forces, forcing.hpp:51-54 (forcing.cpp:58-70): the ForceField of
+ * every cell of the state (H, HUx, HUy: nx*ny host doubles).  The wind is
+ * already sampled at t (WindForcing::at, host); has_wind = wind.any().
+ * sigma/svx/svy: the SourceField (NULL sigma = empty field).  Any output may
+ * be NULL.  terrain->b and params->n_field as for swf_create. */
+int swf_dev_assemble_forces(const swf_terrain* terrain, const swf_params* params,
+                            const double* H, const double* HUx, const double* HUy,
+                            int has_wind, double wx, double wy, const double* sigma,
+                            const double* svx, const double* svy, double* fx, double* fy,
+                            double* fric_x, double* fric_y, double* sigma_eff);
+/* viscous_force (forcing.hpp:34-35, which = 0) and surface_gradient_force
+ * (forcing.hpp:46-47, which = 1) at npt cells ij = npt x {i, j}:
+ * out = npt x {fx, fy}.  SWF_ERANGE for a cell outside the grid. */
+#define SWF_POINT_VISCOUS 0
+#define SWF_POINT_SURFACE_GRADIENT 1
+int swf_dev_point_forces(const swf_terrain* terrain, const swf_params* params,
+                         const double* H, const double* HUx, const double* HUy, int which,
+                         int npt, const int* ij, double* out);
+/* coriolis_force, forcing.hpp:38: u = n x {ux, uy}, out = n x {fx, fy}. */
+int swf_dev_coriolis_force(int n, const double* u, double omega_z, double* out);
+/* wind_force, forcing.hpp:42-43, with W = wind.at(t) sampled by the caller:
+ * in = n x {ux, uy, H}, out = n x {fx, fy} (c_a, rho_air, rho_water from params). */
+int swf_dev_wind_force(int n, const double* in, double wx, double wy,
+                       const swf_params* params, double* out);
+/* compute_block_mask, block.hpp:38-39: interior/halo = nbx*nby ints with
+ * nbx = ceil(nx/B), nby = ceil(ny/B); index_q may be NULL (no sources). */
+int swf_dev_block_mask(int nx, int ny, const double* H, const uint8_t* index_q,
+                       double eps_dry, int block_size, int* interior, int* halo);
+/* source_terms (sources.hpp:40-41, resample = 0: fills sigma, vx, vy and
+ * index_q) and resample_sigma (sources.hpp:45-46, resample = 1: sigma only;
+ * vx, vy, index_q untouched and may be NULL), all nx*ny. */
+int swf_dev_source_terms(const swf_terrain* terrain, const swf_source* sources, int n_sources,
+                         double t, int resample, double* sigma, double* vx, double* vy,
+                         uint8_t* index_q);
 
 /* ---- row-strip decomposition (multi-GPU) ---- */
 /* A strip context owns global rows [j0, j1) of an nx x ny_global domain and

@@ -14,6 +14,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <functional>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -113,6 +114,10 @@ struct SourceSpec {
   double discharge_at(double t) const;
   void validate(const Terrain& terrain) const;
 };
+// sources.hpp:40-46 (the per-cell fill on the GPU)
+SourceField source_terms(const std::vector<SourceSpec>& sources, double t, const Terrain& terrain);
+void resample_sigma(const std::vector<SourceSpec>& sources, double t, const Terrain& terrain,
+                    SourceField& field);
 
 // ---- forcing / riemann free functions (evaluated on the GPU) --------------
 struct ForceField {
@@ -123,6 +128,16 @@ struct ForceField {
 };
 Vec2 bottom_friction(Vec2 u, double H, double g, double n_manning);
 Vec2 bottom_friction(Vec2 u, double H, const PhysicalParams& params);
+// forcing.hpp:34-57 (per-cell arithmetic on the GPU, swf_dev_* in swf.h)
+Vec2 viscous_force(const FlowState& state, const PhysicalParams& params, const Terrain& terrain,
+                   int i, int j);
+Vec2 coriolis_force(Vec2 u, const PhysicalParams& params);
+Vec2 wind_force(Vec2 u, double H, const WindForcing& wind, double t, const PhysicalParams& params);
+Vec2 surface_gradient_force(const FlowState& state, const Terrain& terrain,
+                            const PhysicalParams& params, int i, int j);
+ForceField assemble_forces(const FlowState& state, const Terrain& terrain,
+                           const PhysicalParams& params, const WindForcing& wind,
+                           const SourceField& src, double t);
 
 struct FaceFlux {
   double fm = 0.0, fn = 0.0, ft = 0.0;
@@ -143,6 +158,13 @@ struct BlockMask {
   }
   void block_rect(int ib, int& i0, int& j0, int& i1, int& j1) const;
 };
+// block.hpp:38-52 (the counts on the GPU; the dispatch is host control flow)
+BlockMask compute_block_mask(const FlowState& state, const SourceField& sources, double eps_dry,
+                             int block_size);
+void for_each_active_block(const BlockMask& mask, StageKind kind,
+                           const std::function<void(int)>& body,
+                           const std::function<void(int)>& skipped = {});
+std::vector<int> active_blocks(const BlockMask& mask, StageKind kind);
 double active_fraction(const BlockMask& mask);
 
 // ---- stepper (stepper.hpp) ------------------------------------------------
@@ -187,8 +209,16 @@ class CsphTvdStepper {
   CsphTvdStepper(const Terrain& terrain, PhysicalParams params, TimestepControl control,
                  StepperOptions options = {});
   ~CsphTvdStepper();
-  CsphTvdStepper(const CsphTvdStepper&) = delete;
-  CsphTvdStepper& operator=(const CsphTvdStepper&) = delete;
+  // Copyable like the reference class (stepper.hpp:76, implicitly copyable):
+  // a copy owns a new device context built from the same terrain (by
+  // pointer, as in the reference), parameters, control, options, wind and
+  // sources, so step() on a copy gives the same results as on the original.
+  // The scratch accessors of a copy (mask(), forces_n(), the spans, last_*)
+  // describe the copy's own last step: empty until it has stepped.
+  CsphTvdStepper(const CsphTvdStepper& other);
+  CsphTvdStepper& operator=(const CsphTvdStepper& other);
+  CsphTvdStepper(CsphTvdStepper&& other) noexcept;
+  CsphTvdStepper& operator=(CsphTvdStepper&& other) noexcept;
 
   void set_wind(WindForcing wind);
   void set_sources(std::vector<SourceSpec> sources);
@@ -228,6 +258,8 @@ class CsphTvdStepper {
   double last_source_volume() const;
   double last_boundary_outflow() const;
 
+  struct HalfView;  // stepper.hpp:121 (the half-step view lives on the device here)
+
   swf_ctx* native() const { return ctx_; }  // the C-ABI context (resident API; strip 0 if devices > 1)
 
  private:
@@ -238,10 +270,16 @@ class CsphTvdStepper {
   StepInfo step_group(FlowState& state, double dt_cap);
   std::span<const double> scratch(int which, std::vector<double>& buf) const;
 
+  void create();
+  void release() noexcept;
+  void swap(CsphTvdStepper& other) noexcept;
+
   const Terrain* terrain_;
   PhysicalParams params_;
   TimestepControl ctl_;
   StepperOptions opt_;
+  WindForcing wind_;                  // as last set (replayed into a copy)
+  std::vector<SourceSpec> sources_;
   swf_ctx* ctx_ = nullptr;
   std::vector<swf_ctx*> strips_;  // devices > 1: one strip context per device
   swf_group* group_ = nullptr;

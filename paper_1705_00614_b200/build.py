@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libswflood_cuda.so")
-SOURCES = ["swf_capi.cu", "swf_stage.cu", "swf_fused.cu", "swf_nest.cu"]
+SOURCES = ["swf_capi.cu", "swf_stage.cu", "swf_fused.cu", "swf_nest.cu", "swf_free.cu"]
 HEADERS = ["swf_math.cuh", "swf_internal.cuh"]
 
 # -fmad=false: no FMA contraction, so every + and * rounds exactly like the
@@ -93,13 +93,28 @@ def build_pybind(force=False, hdrs=()):
     return out
 
 
-def build(force=False, verbose=False):
-    if force or stale():
-        cmd = [nvcc()] + NVCC_FLAGS + ["-shared", "-o", OUT] + [os.path.join(CSRC, s) for s in SOURCES]
+def _compile_link(out, flags, objdir, verbose=False):
+    """One nvcc process per translation unit (in parallel), then the link."""
+    os.makedirs(objdir, exist_ok=True)
+    procs, objs = [], []
+    for src in SOURCES:
+        obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        cmd = [nvcc()] + flags + ["-c", "-o", obj, os.path.join(CSRC, src)]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), file=sys.stderr)
-        subprocess.run(cmd, check=True, cwd=CSRC)
+        procs.append((subprocess.Popen(cmd, cwd=CSRC), cmd))
+        objs.append(obj)
+    bad = [c for p, c in procs if p.wait() != 0]
+    if bad:
+        raise subprocess.CalledProcessError(1, bad[0])
+    subprocess.run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out]
+                   + objs, check=True, cwd=CSRC)
+
+
+def build(force=False, verbose=False):
+    if force or stale():
+        _compile_link(OUT, NVCC_FLAGS, os.path.join(HERE, "..", "build", "obj"), verbose)
     build_host(force)
     return OUT
 
@@ -112,9 +127,7 @@ def build_variant(name, defines):
     os.makedirs(vdir, exist_ok=True)
     out = os.path.join(vdir, f"libswf_{name}.so")
     extra = [d if d.startswith("-") else f"-D{d}" for d in defines]
-    cmd = [nvcc()] + NVCC_FLAGS + extra + ["-shared", "-o", out] + \
-        [os.path.join(CSRC, s) for s in SOURCES]
-    subprocess.run(cmd, check=True, cwd=CSRC)
+    _compile_link(out, NVCC_FLAGS + extra, os.path.join(HERE, "..", "build", "obj_" + name))
     return out
 
 

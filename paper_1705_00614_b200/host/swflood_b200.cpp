@@ -55,6 +55,75 @@ double interp_series(const std::vector<T>& s, double t, double T::*val) {
   return L.*val + a * (H.*val - L.*val);
 }
 
+// SourceSpecs as swf_source records (the hydrograph arrays live in `keep`)
+struct CSources {
+  std::vector<swf_source> v;
+  std::vector<std::vector<double>> keep;
+  explicit CSources(const std::vector<SourceSpec>& sources) {
+    keep.reserve(2 * sources.size());
+    for (const SourceSpec& s : sources) {
+      keep.emplace_back();
+      keep.emplace_back();
+      auto& ts = keep[keep.size() - 2];
+      auto& qs = keep.back();
+      for (const HydrographSample& h : s.hydrograph) {
+        ts.push_back(h.t);
+        qs.push_back(h.q);
+      }
+      v.push_back(swf_source{s.kind == SourceSpec::Kind::Rain ? SWF_SOURCE_RAIN : SWF_SOURCE_DISCHARGE,
+                             s.cells.i0, s.cells.j0, s.cells.i1, s.cells.j1, (int)ts.size(),
+                             ts.data(), qs.data(), s.rate, s.source_velocity.x,
+                             s.source_velocity.y});
+    }
+  }
+};
+
+swf_terrain to_c(const Terrain& t) {
+  return swf_terrain{t.nx, t.ny, t.h, t.x0, t.y0, t.b.data()};
+}
+
+swf_params to_c(const PhysicalParams& p) {
+  return swf_params{p.g,   p.n_manning, p.nu,        p.omega_z, p.c_a,
+                    p.rho_air, p.rho_water, p.eps_dry, p.n_field.empty() ? nullptr : p.n_field.data()};
+}
+
+void check_state(const FlowState& s, const Terrain& t, const char* what) {
+  if (s.nx != t.nx || s.ny != t.ny || s.H.size() != t.cells() || s.HUx.size() != t.cells() ||
+      s.HUy.size() != t.cells() || t.b.size() != t.cells())
+    throw ConfigError(std::string(what) + ": state does not match the terrain grid");
+}
+
+// viscous_force / surface_gradient_force at one cell: the 3x3 window around
+// (i, j) clipped at the domain edges only, so every neighbour test of the
+// 5-point stencil (i > 0, i + 1 < nx, ...) reads the same inside the window
+Vec2 point_force(const FlowState& state, const Terrain& terrain, const PhysicalParams& params,
+                 int i, int j, int which) {
+  check_state(state, terrain, which == SWF_POINT_VISCOUS ? "viscous_force" : "surface_gradient_force");
+  if (!terrain.contains(i, j)) throw std::out_of_range("cell index outside grid");
+  const int i0 = std::max(0, i - 1), i1 = std::min(terrain.nx - 1, i + 1);
+  const int j0 = std::max(0, j - 1), j1 = std::min(terrain.ny - 1, j + 1);
+  const int wx = i1 - i0 + 1, wy = j1 - j0 + 1;
+  std::vector<double> H, U, V, B;
+  for (int jj = j0; jj <= j1; ++jj)
+    for (int ii = i0; ii <= i1; ++ii) {
+      const int k = terrain.idx(ii, jj);
+      H.push_back(state.H[k]);
+      U.push_back(state.HUx[k]);
+      V.push_back(state.HUy[k]);
+      B.push_back(terrain.b[k]);
+    }
+  // the window is a whole domain only where it touches a real edge: a stencil
+  // neighbour "outside" the window is outside the grid exactly then
+  swf_terrain tw{wx, wy, terrain.h, 0.0, 0.0, B.data()};
+  swf_params pw = to_c(params);
+  pw.n_field = nullptr;
+  int ij[2] = {i - i0, j - j0};
+  double out[2];
+  if (int rc = swf_dev_point_forces(&tw, &pw, H.data(), U.data(), V.data(), which, 1, ij, out))
+    throw_status(rc, swf_last_error(nullptr));
+  return {out[0], out[1]};
+}
+
 }  // namespace
 
 // ---- value types ------------------------------------------------------------
@@ -192,6 +261,122 @@ FaceFlux hll_face_flux(double hL, double unL, double utL, double hR, double unR,
   return {out[0], out[1], out[2]};
 }
 
+Vec2 viscous_force(const FlowState& state, const PhysicalParams& params, const Terrain& terrain,
+                   int i, int j) {
+  return point_force(state, terrain, params, i, j, SWF_POINT_VISCOUS);
+}
+
+Vec2 coriolis_force(Vec2 u, const PhysicalParams& params) {
+  double in[2] = {u.x, u.y}, out[2];
+  if (int rc = swf_dev_coriolis_force(1, in, params.omega_z, out))
+    throw_status(rc, swf_last_error(nullptr));
+  return {out[0], out[1]};
+}
+
+Vec2 wind_force(Vec2 u, double H, const WindForcing& wind, double t, const PhysicalParams& params) {
+  const Vec2 w = wind.at(t);  // host: the series lookup (grid.cpp:64-75)
+  double in[3] = {u.x, u.y, H}, out[2];
+  swf_params p = to_c(params);
+  if (int rc = swf_dev_wind_force(1, in, w.x, w.y, &p, out)) throw_status(rc, swf_last_error(nullptr));
+  return {out[0], out[1]};
+}
+
+Vec2 surface_gradient_force(const FlowState& state, const Terrain& terrain,
+                            const PhysicalParams& params, int i, int j) {
+  return point_force(state, terrain, params, i, j, SWF_POINT_SURFACE_GRADIENT);
+}
+
+ForceField assemble_forces(const FlowState& state, const Terrain& terrain,
+                           const PhysicalParams& params, const WindForcing& wind,
+                           const SourceField& src, double t) {
+  check_state(state, terrain, "assemble_forces");
+  if (!params.n_field.empty() && params.n_field.size() != terrain.cells())
+    throw ConfigError("assemble_forces: Manning field size mismatch");
+  const bool present = !src.empty();
+  if (present && (src.sigma.size() != terrain.cells() || src.vx.size() != terrain.cells() ||
+                  src.vy.size() != terrain.cells()))
+    throw ConfigError("assemble_forces: source field size mismatch");
+  ForceField out;
+  out.resize(terrain.nx, terrain.ny);
+  const Vec2 w = wind.at(t);
+  swf_terrain T = to_c(terrain);
+  swf_params P = to_c(params);
+  if (int rc = swf_dev_assemble_forces(&T, &P, state.H.data(), state.HUx.data(), state.HUy.data(),
+                                       wind.any() ? 1 : 0, w.x, w.y,
+                                       present ? src.sigma.data() : nullptr,
+                                       present ? src.vx.data() : nullptr,
+                                       present ? src.vy.data() : nullptr, out.fx.data(),
+                                       out.fy.data(), out.fric_x.data(), out.fric_y.data(),
+                                       out.sigma_eff.data()))
+    throw_status(rc, swf_last_error(nullptr));
+  return out;
+}
+
+SourceField source_terms(const std::vector<SourceSpec>& sources, double t, const Terrain& terrain) {
+  for (const SourceSpec& s : sources) s.validate(terrain);  // sources.cpp:48
+  SourceField f;
+  f.resize(terrain.nx, terrain.ny);
+  CSources cs(sources);
+  swf_terrain T = to_c(terrain);
+  if (int rc = swf_dev_source_terms(&T, cs.v.data(), (int)cs.v.size(), t, 0, f.sigma.data(),
+                                    f.vx.data(), f.vy.data(), f.index_q.data()))
+    throw_status(rc, swf_last_error(nullptr));
+  return f;
+}
+
+void resample_sigma(const std::vector<SourceSpec>& sources, double t, const Terrain& terrain,
+                    SourceField& field) {
+  if (field.sigma.size() != terrain.cells()) field.sigma.assign(terrain.cells(), 0.0);
+  CSources cs(sources);
+  swf_terrain T = to_c(terrain);
+  if (int rc = swf_dev_source_terms(&T, cs.v.data(), (int)cs.v.size(), t, 1, field.sigma.data(),
+                                    nullptr, nullptr, nullptr))
+    throw_status(rc, swf_last_error(nullptr));
+}
+
+BlockMask compute_block_mask(const FlowState& state, const SourceField& sources, double eps_dry,
+                             int block_size) {
+  if (block_size < 1) throw ConfigError("block mask: block size must be >= 1");
+  if (state.H.size() != state.cells()) throw ConfigError("block mask: state size mismatch");
+  const bool has_src = !sources.empty();
+  if (has_src && sources.index_q.size() != state.cells())
+    throw ConfigError("block mask: source field size mismatch");
+  BlockMask m;
+  m.block_size = block_size;
+  m.nx = state.nx;
+  m.ny = state.ny;
+  m.nbx = (state.nx + block_size - 1) / block_size;
+  m.nby = (state.ny + block_size - 1) / block_size;
+  m.interior_wet.assign(m.total_blocks(), 0);
+  m.halo_wet.assign(m.total_blocks(), 0);
+  if (m.total_blocks() == 0) return m;
+  if (int rc = swf_dev_block_mask(state.nx, state.ny, state.H.data(),
+                                  has_src ? sources.index_q.data() : nullptr, eps_dry, block_size,
+                                  m.interior_wet.data(), m.halo_wet.data()))
+    throw_status(rc, swf_last_error(nullptr));
+  return m;
+}
+
+// block.cpp:63-79: dispatch over the mask (host control flow; the bodies are
+// the caller's)
+void for_each_active_block(const BlockMask& mask, StageKind kind,
+                           const std::function<void(int)>& body,
+                           const std::function<void(int)>& skipped) {
+  for (int ib = 0; ib < mask.total_blocks(); ++ib) {
+    if (mask.active(ib, kind))
+      body(ib);
+    else if (skipped)
+      skipped(ib);
+  }
+}
+
+std::vector<int> active_blocks(const BlockMask& mask, StageKind kind) {
+  std::vector<int> out;
+  for (int ib = 0; ib < mask.total_blocks(); ++ib)
+    if (mask.active(ib, kind)) out.push_back(ib);
+  return out;
+}
+
 void BlockMask::block_rect(int ib, int& i0, int& j0, int& i1, int& j1) const {
   i0 = (ib % nbx) * block_size;
   j0 = (ib / nbx) * block_size;
@@ -236,13 +421,17 @@ CsphTvdStepper::CsphTvdStepper(const Terrain& terrain, PhysicalParams params,
   if (opt_.workers < 1) opt_.workers = 1;
   if (!params_.n_field.empty() && params_.n_field.size() != terrain.cells())
     throw ConfigError("stepper: Manning field size mismatch");
-  swf_terrain t{terrain.nx, terrain.ny, terrain.h, terrain.x0, terrain.y0, terrain.b.data()};
-  swf_params p{params_.g,       params_.n_manning, params_.nu,        params_.omega_z,
-               params_.c_a,     params_.rho_air,   params_.rho_water, params_.eps_dry,
-               params_.n_field.empty() ? nullptr : params_.n_field.data()};
+  if (opt_.devices < 1) throw ConfigError("stepper: devices must be >= 1");
+  create();
+}
+
+// the device context(s) for the current configuration
+void CsphTvdStepper::create() {
+  const Terrain& terrain = *terrain_;
+  swf_terrain t = to_c(terrain);
+  swf_params p = to_c(params_);
   swf_control k = to_c(ctl_);
   swf_options o = to_c(opt_);
-  if (opt_.devices < 1) throw ConfigError("stepper: devices must be >= 1");
   if (opt_.devices == 1) {
     int rc = swf_create(&t, &p, &k, &o, &ctx_);
     if (rc) throw_status(rc, swf_last_error(nullptr));
@@ -284,13 +473,72 @@ CsphTvdStepper::CsphTvdStepper(const Terrain& terrain, PhysicalParams params,
   pushed_opt_ = opt_;
 }
 
-CsphTvdStepper::~CsphTvdStepper() {
+void CsphTvdStepper::release() noexcept {
   if (group_) {
     swf_group_destroy(group_);
     for (swf_ctx* s : strips_) swf_destroy(s);
-  } else {
+  } else if (ctx_) {
     swf_destroy(ctx_);
   }
+  group_ = nullptr;
+  strips_.clear();
+  ctx_ = nullptr;
+}
+
+CsphTvdStepper::~CsphTvdStepper() { release(); }
+
+CsphTvdStepper::CsphTvdStepper(const CsphTvdStepper& o)
+    : terrain_(o.terrain_), params_(o.params_), ctl_(o.ctl_), opt_(o.opt_) {
+  create();
+  try {
+    if (o.wind_.any()) set_wind(o.wind_);
+    if (!o.sources_.empty()) set_sources(o.sources_);
+  } catch (...) {
+    release();
+    throw;
+  }
+}
+
+CsphTvdStepper& CsphTvdStepper::operator=(const CsphTvdStepper& o) {
+  if (this != &o) {
+    CsphTvdStepper tmp(o);
+    swap(tmp);
+  }
+  return *this;
+}
+
+CsphTvdStepper::CsphTvdStepper(CsphTvdStepper&& o) noexcept
+    : terrain_(o.terrain_), params_(o.params_), ctl_(o.ctl_), opt_(o.opt_) {
+  swap(o);
+}
+
+CsphTvdStepper& CsphTvdStepper::operator=(CsphTvdStepper&& o) noexcept {
+  if (this != &o) {
+    release();
+    swap(o);
+  }
+  return *this;
+}
+
+void CsphTvdStepper::swap(CsphTvdStepper& o) noexcept {
+  using std::swap;
+  swap(terrain_, o.terrain_);
+  swap(params_, o.params_);
+  swap(ctl_, o.ctl_);
+  swap(opt_, o.opt_);
+  swap(wind_, o.wind_);
+  swap(sources_, o.sources_);
+  swap(ctx_, o.ctx_);
+  swap(strips_, o.strips_);
+  swap(group_, o.group_);
+  swap(group_vol_, o.group_vol_);
+  swap(pushed_ctl_, o.pushed_ctl_);
+  swap(pushed_opt_, o.pushed_opt_);
+  swap(mask_, o.mask_);
+  swap(src_, o.src_);
+  swap(f_n_, o.f_n_);
+  swap(f_mid_, o.f_mid_);
+  for (int q = 0; q < 9; ++q) swap(buf_[q], o.buf_[q]);
 }
 
 std::vector<swf_ctx*> CsphTvdStepper::contexts() const {
@@ -332,28 +580,15 @@ void CsphTvdStepper::set_wind(WindForcing wind) {
   for (swf_ctx* c : contexts())
     if (int rc = swf_set_wind(c, (int)t.size(), t.data(), x.data(), y.data()))
       throw_status(rc, swf_last_error(c));
+  wind_ = std::move(wind);
 }
 
 void CsphTvdStepper::set_sources(std::vector<SourceSpec> sources) {
   for (const SourceSpec& s : sources) s.validate(*terrain_);
-  std::vector<swf_source> v;
-  std::vector<std::vector<double>> keep;
-  for (const SourceSpec& s : sources) {
-    keep.emplace_back();
-    keep.emplace_back();
-    auto& ts = keep[keep.size() - 2];
-    auto& qs = keep.back();
-    for (const HydrographSample& h : s.hydrograph) {
-      ts.push_back(h.t);
-      qs.push_back(h.q);
-    }
-    v.push_back(swf_source{s.kind == SourceSpec::Kind::Rain ? SWF_SOURCE_RAIN : SWF_SOURCE_DISCHARGE,
-                           s.cells.i0, s.cells.j0, s.cells.i1, s.cells.j1, (int)ts.size(),
-                           ts.data(), qs.data(), s.rate, s.source_velocity.x,
-                           s.source_velocity.y});
-  }
+  CSources cs(sources);
   for (swf_ctx* c : contexts())
-    if (int rc = swf_set_sources(c, (int)v.size(), v.data())) throw_status(rc, swf_last_error(c));
+    if (int rc = swf_set_sources(c, (int)cs.v.size(), cs.v.data())) throw_status(rc, swf_last_error(c));
+  sources_ = std::move(sources);
 }
 
 StepInfo CsphTvdStepper::step(FlowState& state, double dt_cap) {
