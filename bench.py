@@ -28,6 +28,16 @@ sys.path.insert(0, ROOT)
 
 GB = 1e9
 
+# The CPU sample of C3/C5: 8 of the 64 tiles of 2048^2 cells, one from the
+# middle of each eighth of the tiles sorted by their t = 0 flux-active block
+# fraction (tools/cpu_sample_crops.py): C3 sample 0.361 vs 0.362 over all 64
+# tiles; the diagonal crops used before held 0.283 (drier, which favoured the
+# CPU).
+SAMPLE_CROPS = {
+    "C3": [(2048, 4096), (0, 4096), (2048, 0), (12288, 0), (6144, 14336), (10240, 10240),
+           (0, 14336), (4096, 0)],
+}
+
 
 def parse():
     p = argparse.ArgumentParser()
@@ -105,6 +115,33 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def fp64_roof(kernel, active_cells, kernel_s):
+    """The FP64-pipe roof beside the HBM one: the kernel's
+    FP64-pipe instructions per active cell (ncu capture, profiles/) against
+    the measured FP64 lane-op rate of this B200 (tools/fp64_peak.cu,
+    profiles/fp64_peak_r3b.json: DADD/DMUL/DFMA throughput, CUDA events)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            k = json.load(f)["kernels"][kernel]
+        with open(os.path.join(ROOT, "profiles", "fp64_peak_r3b.json")) as f:
+            pk = json.load(f)
+        ops = pk["ops"]
+        # the mix is DADD/DMUL/DSETP-heavy with DFMA from the divisions: the
+        # mean of the three measured rates
+        peak = sum(ops[o]["lane_ops_per_s"] for o in ("DADD", "DMUL", "DFMA")) / 3.0
+        lane_ops = 32.0 * k["fp64_inst_executed"]
+        per_cell = lane_ops / k["cells"] if k.get("cells") else lane_ops / active_cells
+        roof = peak / per_cell  # active cells per second
+        achieved = active_cells / kernel_s
+        return {"bound": "fp64", "unit": "active cell-updates/s",
+                "fp64_lane_ops_per_active_cell": round(per_cell, 1),
+                "peak_fp64_lane_ops_per_s": peak, "roof": round(roof, 1),
+                "achieved": round(achieved, 1), "frac": round(achieved / roof, 4),
+                "source": "profiles/fp64_peak_r3b.json (measured) + profiles/ncu_summary.json"}
+    except Exception:
+        return None
+
+
 def ncu_traffic(kernel="k_step"):
     """DRAM bytes per launch of the kernel from the committed ncu --set full
     capture summary (profiles/), with its issue and FP64-pipe utilisation
@@ -151,6 +188,10 @@ def cpu_reference(config, warmup=5, steps=30, threads=None, crop=2048):
         wins = [(k * 4096 + 2048 - c // 2, S.WEAK_ROWS // 2 - c // 2, c, c) for k in range(8)]
         scs = [S.build("C5", window=w) for w in wins]
         n_full = 32768
+    elif n_full and crop == 2048 and config in SAMPLE_CROPS:
+        c = crop
+        wins = [(i0, j0, c, c) for i0, j0 in SAMPLE_CROPS[config]]
+        scs = [S.build(config, window=w) for w in wins]
     elif n_full:
         c = min(crop, n_full // 8)
         wins = [(k * (n_full // 8) + (n_full // 16) - c // 2,) * 2 + (c, c) for k in range(8)]
@@ -173,17 +214,29 @@ def cpu_reference(config, warmup=5, steps=30, threads=None, crop=2048):
         for o in steppers:
             o.run(1)
     per_step, t_all = [], time.perf_counter()
+    crop_s = [0.0] * len(steppers)
+    act = [0.0] * len(steppers)
     for _ in range(steps):
         t0 = time.perf_counter()
-        for o in steppers:
-            o.run(1)
+        for q, o in enumerate(steppers):
+            tq = time.perf_counter()
+            _, info = o.run(1)
+            crop_s[q] += time.perf_counter() - tq
+            act[q] += info.active_fraction / steps
         per_step.append(cells / (time.perf_counter() - t0) / 1e6)
     el = time.perf_counter() - t_all
     for o in steppers:
         o.close()
     v = cells * steps / el / 1e6
-    what = (f"8 {'band' if config == 'C5W' else 'diagonal'} {scs[0].terrain.nx}x"
-            f"{scs[0].terrain.ny} crops of {config}" if n_full
+    # the sample's activity (flux-active block fraction, StepInfo, mean over
+    # the timed steps) and each crop's own rate
+    detail = {"active_fraction": round(sum(a * sc.cells() for a, sc in zip(act, scs)) / cells, 4),
+              "crops": [{"window": list(sc.window) if getattr(sc, "window", None) else None, "active_fraction": round(a, 4),
+                         "mcells_s": round(sc.cells() * steps / t / 1e6, 3) if t > 0 else None}
+                        for sc, a, t in zip(scs, act, crop_s)]}
+    kind_of = ("band" if config == "C5W" else
+               "stratified" if (crop == 2048 and config in SAMPLE_CROPS) else "diagonal")
+    what = (f"8 {kind_of} {scs[0].terrain.nx}x{scs[0].terrain.ny} crops of {config}" if n_full
             else f"{config} full grid")
     cpu = "unknown CPU"
     try:
@@ -193,10 +246,11 @@ def cpu_reference(config, warmup=5, steps=30, threads=None, crop=2048):
         pass
     built = ("the reference sources compiled by oracle/Makefile: g++ -O3 -ffp-contract=off "
              "-fopenmp, no -march" if kind == "reference" else "the C restatement (gcc -O2)")
-    sample = (f"{what} (same generator, {cells / 1e6:.1f} M cells), {warmup} warm-up + {steps} "
+    sample = (f"{what} (same generator, {cells / 1e6:.1f} M cells, flux-active fraction "
+              f"{detail['active_fraction']}), {warmup} warm-up + {steps} "
               f"timed steps from t=0 like the B200 arm, {el:.1f} s, {cores} thread(s) of "
               f"{os.cpu_count()} on {cpu}; {built}")
-    return v, cores, ("reference" if kind == "reference" else "port"), sample, per_step
+    return v, cores, ("reference" if kind == "reference" else "port"), sample, per_step, detail
 
 
 def reference_arm(args):
@@ -205,7 +259,7 @@ def reference_arm(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    v, cores, kind, sample, per_step = cpu_reference(args.config, args.warmup, args.steps)
+    v, cores, kind, sample, per_step, detail = cpu_reference(args.config, args.warmup, args.steps)
     line = {"metric": "cell-updates/sec (Mcells/s)", "value": round(v, 3), "unit": "Mcells/s",
             "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": None, "higher_is_better": True,
@@ -213,7 +267,7 @@ def reference_arm(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.config} (bounded sample on host CPU)", "grid": args.config},
             "cpu_baseline": {"value": round(v, 3), "unit": "Mcells/s", "cores": cores,
-                             "kind": kind, "sample": sample},
+                             "kind": kind, "sample": sample, **detail},
             "e2e": {"value": round(v, 3), "unit": "Mcells/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -297,12 +351,12 @@ def b200_single(args):
     cpu = None
     if not args.no_cpu_baseline:
         try:
-            v, cores, kind, sample, _ = cpu_reference(args.config, args.warmup, args.steps)
+            v, cores, kind, sample, _, detail = cpu_reference(args.config, args.warmup, args.steps)
             cpu = {"value": round(v, 3), "unit": "Mcells/s", "cores": cores, "kind": kind,
-                   "sample": sample}
+                   "sample": sample, **detail}
             # a 1-core run beside the all-threads one (a shorter
             # window: 1 warm-up + 2 timed steps of the same 8 crops)
-            v1, _, _, sample1, _ = cpu_reference(args.config, 1, 2, threads=1)
+            v1, _, _, sample1, _, _ = cpu_reference(args.config, 1, 2, threads=1)
             cpu["single_core"] = {"value": round(v1, 3), "unit": "Mcells/s", "cores": 1,
                                   "sample": sample1}
         except Exception as e:  # reported, not fatal
@@ -344,7 +398,9 @@ def b200_single(args):
                      "ncu": ({"fp64_pipe_pct": traffic["fp64_pipe_pct"],
                               "issue_active_pct": traffic["issue_active_pct"],
                               "source": traffic["source"]} if traffic else None),
-                     "binding": "FP64 issue and dependency latency, not HBM (DESIGN.md section 4)"},
+                     "binding": "FP64 issue and dependency latency, not HBM (DESIGN.md section 4)",
+                     "fp64": (fp64_roof("k_step", n_act, t_step_kernel)
+                              if args.config == "C3" else None)},
         "e2e": {"value": round(e2e_value, 3), "unit": "Mcells/s",
                 "h2d_bytes_per_step": int(h2d // E), "d2h_bytes_per_step": int(d2h // E),
                 "how": "CsphTvdStepper.step(FlowState) on pinned host buffers, every step: H and "

@@ -394,7 +394,7 @@ void swf_destroy(swf_ctx* c) {
                   c->fpx, c->fpy, c->d_src, c->d_ht, c->d_hq, c->d_sig, c->d_wt, c->d_wv,
                   c->d_interior, c->d_halo, c->d_bflag, c->d_tile_act, c->d_tile_same,
                   c->d_tile_srcm, c->d_redo_f, c->d_redo_s, c->d_list_f, c->d_list_s,
-                  c->d_part, c->d_sc};
+                  c->d_part, c->d_sc, c->d_redo_l, c->d_half[0], c->d_half[1], c->d_half[2]};
   for (void* p : ptrs) cudaFree(p);
   if (c->h_sc) cudaFreeHost(c->h_sc);
   for (auto& e : c->ev)
@@ -679,7 +679,7 @@ int swf_step_host(swf_ctx* c, double* H, double* HUx, double* HUy, double* t, do
 int swf_debug_redo_counts(const swf_ctx* c, int* counts) {
   if (!c || !counts) return SWF_ECONFIG;
   counts[0] = c->h_sc->redo_n[0];
-  counts[1] = c->h_sc->redo_n[1];
+  counts[1] = c->h_sc->redo_n[1] + c->h_sc->redo_n[2];
   return SWF_OK;
 }
 

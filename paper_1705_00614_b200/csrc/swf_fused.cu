@@ -107,8 +107,9 @@ __global__ void k_begin(Geo G, const DevSrc* src, const double* ht, const double
   sc->speed_bits = 0ull;
   sc->redo_n[0] = 0;
   sc->redo_n[1] = 0;
+  sc->redo_n[2] = 0;
   sc->list_n[0] = sc->list_n[1] = 0;
-  sc->list_take[0] = sc->list_take[1] = 0;
+  sc->list_take[0] = sc->list_take[1] = sc->list_take[2] = 0;
   for (int q = 0; q < SPEED_SLOTS; ++q) sc->speed_slots[q] = 0ull;
   sc->lag_act = 0;
   sc->flux_act = 0;
@@ -678,6 +679,12 @@ struct StepArgs {
   double* hHUy;
   double* part;  // 3 per tile
   StepScalars* sc;
+  // split step (k_lag -> k_flux): the half-step view of every cell of the
+  // flux-active tiles (and of the 2 ghost rows next to a strip's owned rows)
+  double* hd;
+  double* hu;
+  double* hv;
+  int* redo_l;  // k_lag tiles to redo exactly
 };
 
 __device__ __forceinline__ unsigned long long fused_flux_key(const Geo& G,
@@ -1327,6 +1334,699 @@ __global__ void __launch_bounds__(STHR, SWF_STEP_MINB) k_step_redo(Geo G, StepAr
   }
 }
 
+
+// ===========================================================================
+// Split step (-DSWF_SPLIT=1; measured and NOT the default): k_step's work in
+// two tile kernels, each with its own register and shared-memory budget (the
+// fused k_step runs at both limits, 80 registers x 768 threads and 3 x 76 KB
+// per SM).  On C3 it is bit-identical but slower: k_lag 5.45 + k_flux 7.26 ms
+// against k_step 11.0 ms (profiles/README.md, round 3) -- both halves still
+// sit at 24 warps per SM (k_lag's mid forces need 80 registers, k_flux 76)
+// while the hand-off adds ~110 B per active cell of HBM traffic and a load
+// phase of its own.
+//   k_lag  (K4 predictor on the tile + 1-cell halo, K5 mid forces and K6
+//          corrector on owned cells): writes the Lagrangian state (Ht, HVt)
+//          of every owned cell into the next-parity buffers -- the final
+//          update's base state -- and the half-step view (depth, u, v) of
+//          every owned cell into d_half.
+//   k_ghost_half  the half-step view of the 2 ghost rows next to a strip's
+//          owned rows (their predictor; no tile there).
+//   k_flux (K7 slopes and faces, K8 final update on owned cells): reads the
+//          half-step view on the tile + 2-cell halo and the base state.
+// A cell of a tile k_lag did not visit (not flux-active) is not active
+// (dry, no source), so its half-step view is its state: (H, 0, 0).
+// Same arithmetic, same order as step_tile: bit-identical results.
+// ===========================================================================
+#ifndef SWF_SPLIT
+#define SWF_SPLIT 0
+#endif
+#ifndef SWF_LAG_THREADS
+#define SWF_LAG_THREADS 256
+#endif
+#ifndef SWF_LAG_MINB
+#define SWF_LAG_MINB 3
+#endif
+#ifndef SWF_FLUX_THREADS
+#define SWF_FLUX_THREADS 256
+#endif
+#ifndef SWF_FLUX_MINB
+#define SWF_FLUX_MINB 3
+#endif
+constexpr int LTHR = SWF_LAG_THREADS, XTHR = SWF_FLUX_THREADS;
+static_assert(LTHR % 32 == 0 && XTHR % 32 == 0, "whole warps");
+// k_lag shared memory (doubles): 7 region planes (H->D, HUx->U, HUy->V, b->E,
+// f'x, f'y, n), then the owned cells' step-start state and lambda(H12)
+enum { L_D = 0, L_U, L_V, L_E, L_FX, L_FY, L_N, L_NUM };
+constexpr size_t lag_smem() { return (size_t)(L_NUM * AREG + 4 * BX * BY) * sizeof(double); }
+// k_flux shared memory: the 2-halo region planes, then slopes and faces
+constexpr size_t flux_smem() { return (size_t)(F_NUM * RREG + SCRATCH_A) * sizeof(double); }
+static_assert(3 * BX * BY <= 3 * NSL, "k_flux stages its results in the slope planes");
+
+template <bool SPEC>
+__device__ __forceinline__ void lag_tile(const Geo& G, const StepArgs& A, const int tile) {
+  extern __shared__ double smem[];
+  double* Q = smem;                         // L_NUM x AREG
+  double* OWN = smem + L_NUM * AREG;        // 3 x (BX*BY): H, HUx, HUy at t_n
+  double* LAM = OWN + 3 * BX * BY;          // BX*BY: lambda(H12, n) of the predictor, or -1
+  __shared__ double s_red[LTHR / 32];
+  const PhysConst& P = G.P;
+  StepScalars* sc = A.sc;
+  if (__syncthreads_or(stopped(sc))) return;
+  if (!(A.tile_act[tile] & 2)) return;  // k_flux keeps the state of an inactive tile
+  bool sok = true;
+  unsigned long long my_err = ERR_NONE;
+  const int tid = threadIdx.x;
+  const int tx = tile % G.tiles_x, ty = tile / G.tiles_x;
+  const int i0 = tx * BX;
+  const int r0 = G.r0 + ty * BY;
+  const size_t nx = G.nx;
+  const unsigned srcm = A.tile_srcm[tile];  // specs meeting the tile +- 2 cells
+  const double tau = sc->tau;
+  const double half_tau = 0.5 * tau;
+  const double wmx = sc->wind_mid[0], wmy = sc->wind_mid[1];
+  const int nsrc = G.nsrc;
+  const double* sig_n = A.sig;
+  const double* sig_m = A.sig + nsrc;
+
+  // ---- L1a: stage the region's inputs (tile + 1-cell halo) ----------------
+  for (int c = tid; c < AREG; c += LTHR) {
+    int i = i0 - 1 + c % AREGX, r = r0 - 1 + c / AREGX;
+    double h = 0.0, mx = 0.0, my = 0.0, bb = 0.0, fx = 0.0, fy = 0.0, n = G.n_manning;
+    if (i >= 0 && i < G.nx && r >= 0 && r < G.rows) {
+      size_t k = (size_t)i + (size_t)r * nx;
+      h = A.H[k];
+      mx = A.HUx[k];
+      my = A.HUy[k];
+      bb = A.b[k];
+      fx = A.fpx[k];
+      fy = A.fpy[k];
+      if (G.has_nfield) n = A.nf[k];
+    }
+    Q[L_D * AREG + c] = h;
+    Q[L_U * AREG + c] = mx;
+    Q[L_V * AREG + c] = my;
+    Q[L_E * AREG + c] = bb;
+    Q[L_FX * AREG + c] = fx;
+    Q[L_FY * AREG + c] = fy;
+    Q[L_N * AREG + c] = n;
+  }
+  __syncthreads();
+
+  // ---- L1b: K4 predictor -> half-step view (in place) ----------------------
+  for (int c = tid; c < AREG; c += LTHR) {
+    int xr = c % AREGX, yr = c / AREGX;
+    int i = i0 - 1 + xr, r = r0 - 1 + yr;
+    double Hn = Q[L_D * AREG + c], mx = Q[L_U * AREG + c], my = Q[L_V * AREG + c];
+    double bb = Q[L_E * AREG + c];
+    double d = 0.0, u = 0.0, v = 0.0;
+    const bool owned = xr >= 1 && xr < BX + 1 && yr >= 1 && yr < BY + 1;
+    const int o = (xr - 1) + (yr - 1) * BX;
+    if (owned) {
+      OWN[o] = Hn;
+      OWN[BX * BY + o] = mx;
+      OWN[2 * BX * BY + o] = my;
+    }
+    double lam = -1.0;
+    const bool in = i >= 0 && i < G.nx && r >= 0 && r < G.rows;
+    if (in) {
+      double sg = srcm ? msig(G, A.src, sig_n, srcm, i, G.jg0 + r) : 0.0;
+      bool act = Hn > P.eps || sg != 0.0;
+      d = Hn;
+      Recip Rd{0.0, 0.0};
+      if (act) {
+        bool wet = Hn > P.eps;
+        double fx = wet ? Q[L_FX * AREG + c] : 0.0, fy = wet ? Q[L_FY * AREG + c] : 0.0;
+        predict_cell(Hn, mx, my, sg, fx, fy, Q[L_N * AREG + c], half_tau, P.eps, P.g, d, mx, my,
+                     SP, &lam, &Rd);
+      }
+      if (d > P.eps) {
+        u = rdiv(mx, Rd, SP);
+        v = rdiv(my, Rd, SP);
+      }
+    }
+    Q[L_D * AREG + c] = d;
+    Q[L_E * AREG + c] = d + bb;
+    Q[L_U * AREG + c] = u;
+    Q[L_V * AREG + c] = v;
+    if (owned) {
+      LAM[o] = lam;
+      if (i < G.nx && r < G.r1) {  // the half-step view for k_flux
+        size_t k = (size_t)i + (size_t)r * nx;
+        A.hd[k] = d;
+        A.hu[k] = u;
+        A.hv[k] = v;
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- L2: K5 mid forces + K6 corrector on owned cells ---------------------
+  double srcvol = 0.0;
+  const double* QD = Q + L_D * AREG;
+  const double* QE = Q + L_E * AREG;
+  const double* QU = Q + L_U * AREG;
+  const double* QV = Q + L_V * AREG;
+  for (int c = tid; c < BX * BY; c += LTHR) {
+    int x = c % BX, y = c / BX;
+    int i = i0 + x, r = r0 + y;
+    if (i >= G.nx || r >= G.r1) continue;
+    const size_t k = (size_t)i + (size_t)r * nx;
+    double Hn = OWN[c], qxn = OWN[BX * BY + c], qyn = OWN[2 * BX * BY + c];
+    int s = (x + 1) + (y + 1) * AREGX;
+    int jg = G.jg0 + r;
+    double sgn_ = 0.0, svx = 0.0, svy = 0.0, sgm = 0.0;
+    if (srcm) {
+      sgn_ = msrc(G, A.src, sig_n, srcm, i, jg, svx, svy);
+      sgm = msig(G, A.src, sig_m, srcm, i, jg);
+    }
+    bool act = Hn > P.eps || sgn_ != 0.0;
+    double ht = Hn, qx = qxn, qy = qyn;  // base state of an inactive cell (stepper.cpp:641-651)
+    if (act) {
+      double n = Q[L_N * AREG + s];
+      double d = QD[s];  // H12
+      double fmx = 0.0, fmy = 0.0;
+      double lam = LAM[c], Hk = -1.0;
+      if (d > P.eps) {
+        auto nb = [&](bool inb, int q) { return SNbr{inb, QD, QE, QU, QV, q}; };
+        SNbr W = nb(i > 0, s - 1), E = nb(i + 1 < G.nx, s + 1);
+        SNbr S = nb(jg > 0, s - AREGX), N = nb(jg + 1 < G.ny, s + AREGX);
+        if (!(lam >= 0.0)) lam = manning_lambda(d, P.g, n);
+        Hk = d;
+        ForceOut o = cell_forces_lam(d, QU[s], QV[s], QE[s], W, E, S, N, lam, P, G.nwind > 0, wmx,
+                                     wmy, nsrc > 0 ? sgm : 0.0, svx, svy, SP);
+        fmx = o.fx - o.frx;
+        fmy = o.fy - o.fry;
+      }
+      double sv;
+      correct_cell(Hn, qxn, qyn, nsrc > 0, sgm, d, fmx, fmy, n, tau, P.eps, P.g, ht, qx, qy, sv,
+                   SP, Hk, &lam);
+      srcvol += sv;
+      double dx = tau * QU[s], dy = tau * QV[s];
+      double half_h = 0.5 * P.h;
+      if (fabs(dx) >= half_h || fabs(dy) >= half_h) {
+        int ib = i / G.bs + (jg / G.bs) * G.nbx;
+        unsigned long long local = (unsigned long long)((jg % G.bs) * G.bs + (i % G.bs));
+        unsigned long long key = (ERR_CFL << 58) | ((unsigned long long)ib << 24) | local;
+        my_err = key < my_err ? key : my_err;
+      }
+    }
+    A.Ho[k] = ht;  // the final update's base state (k_flux reads it back)
+    A.HUxo[k] = qx;
+    A.HUyo[k] = qy;
+  }
+
+  // ---- the tile's source-volume partial (deterministic) --------------------
+  double v = srcvol;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((tid & 31) == 0) s_red[tid >> 5] = v;
+  const bool any_bad = __syncthreads_or(!sok);
+  if (tid == 0) {
+    double w = 0.0;
+    for (int q = 0; q < LTHR / 32; ++q) w += s_red[q];
+    A.part[5 * (size_t)tile + 1] = w;
+  }
+  if (SPEC && any_bad) {
+    if (tid == 0) A.redo_l[atomicAdd(&sc->redo_n[2], 1)] = tile;
+  } else if (my_err != ERR_NONE) {
+    atomicMin(&sc->err_key, my_err);
+  }
+}
+
+__global__ void __launch_bounds__(LTHR, SWF_LAG_MINB) k_lag_list(Geo G, StepArgs A) {
+  __shared__ int s_next;
+  StepScalars* sc = A.sc;
+  const int n = *(volatile int*)&sc->list_n[1];
+  while (true) {
+    if (threadIdx.x == 0) s_next = atomicAdd(&sc->list_take[2], 1);
+    __syncthreads();
+    const int q = s_next;
+    __syncthreads();
+    if (q >= n) break;
+    lag_tile<SWF_SPECULATE != 0>(G, A, A.list[q]);
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(LTHR, SWF_LAG_MINB) k_lag_redo(Geo G, StepArgs A) {
+  const int n = *(volatile int*)&A.sc->redo_n[2];
+  for (int q = blockIdx.x; q < n; q += gridDim.x) {
+    lag_tile<false>(G, A, A.redo_l[q]);
+    __syncthreads();
+  }
+}
+
+// The half-step view of the ghost rows k_flux reads next to a strip's owned
+// rows (local rows [r0-2, r0) and [r1, r1+2)): one thread per cell, the
+// predictor exactly (stepper.cpp:269-308; f' is valid there, k_forces covers
+// 2 ghost rows).
+__global__ void k_ghost_half(Geo G, StepArgs A) {
+  const StepScalars* sc = A.sc;
+  if (stopped(sc)) return;
+  const PhysConst& P = G.P;
+  const int lo = G.r0 >= 2 ? 2 : G.r0;                 // ghost rows below
+  const int hi = G.rows - G.r1 >= 2 ? 2 : G.rows - G.r1;  // and above
+  const int nrow = lo + hi;
+  const size_t total = (size_t)nrow * G.nx;
+  const double half_tau = 0.5 * sc->tau;
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const int q = (int)(t / G.nx), i = (int)(t % G.nx);
+    const int r = q < lo ? G.r0 - lo + q : G.r1 + (q - lo);
+    const size_t k = (size_t)i + (size_t)r * G.nx;
+    const double Hn = A.H[k];
+    double mx = A.HUx[k], my = A.HUy[k];
+    const double sg = G.nsrc > 0 ? cell_sigma_only(A.src, A.sig, G.nsrc, i, G.jg0 + r) : 0.0;
+    const bool act = Hn > P.eps || sg != 0.0;
+    double d = Hn, u = 0.0, v = 0.0;
+    Recip Rd{0.0, 0.0};
+    if (act) {
+      const bool wet = Hn > P.eps;
+      predict_cell(Hn, mx, my, sg, wet ? A.fpx[k] : 0.0, wet ? A.fpy[k] : 0.0,
+                   G.has_nfield ? A.nf[k] : G.n_manning, half_tau, P.eps, P.g, d, mx, my,
+                   nullptr, nullptr, &Rd);
+    }
+    if (d > P.eps) {
+      u = rdiv(mx, Rd);
+      v = rdiv(my, Rd);
+    }
+    A.hd[k] = d;
+    A.hu[k] = u;
+    A.hv[k] = v;
+  }
+}
+
+template <bool SPEC>
+__device__ __forceinline__ void flux_tile(const Geo& G, const StepArgs& A, const int tile) {
+  extern __shared__ double smem[];
+  double* R = smem;                  // F_NUM x RREG
+  double* SL = smem + F_NUM * RREG;  // 3 x NSL slopes (eta, un, ut)
+  double* FB = SL + 3 * NSL;         // 4 x NFC faces (fm, fnl, fnr, ft)
+  __shared__ double s_red[2][XTHR / 32];
+  __shared__ unsigned char s_bf[MAXBF];
+  __shared__ unsigned short s_bcol[BX], s_brow[BY];
+  __shared__ unsigned char s_nact[9];  // flux-active flags of the 3 x 3 tiles around
+  const PhysConst& P = G.P;
+  StepScalars* sc = A.sc;
+  if (__syncthreads_or(stopped(sc))) return;
+  bool sok = true;
+  unsigned long long my_err = ERR_NONE;
+  const int tid = threadIdx.x;
+  const int tx = tile % G.tiles_x, ty = tile / G.tiles_x;
+  const int i0 = tx * BX;
+  const int r0 = G.r0 + ty * BY;
+  const size_t nx = G.nx;
+
+  // ---- inactive tile: keep the step-start state (skip semantics) ----------
+  if (!(A.tile_act[tile] & 2)) {
+    if (!A.tile_same[tile]) {
+      for (int c = tid; c < BX * BY; c += XTHR) {
+        int i = i0 + c % BX, r = r0 + c / BX;
+        if (i < G.nx && r < G.r1) {
+          size_t k = (size_t)i + (size_t)r * nx;
+          A.Ho[k] = A.H[k];
+          A.HUxo[k] = A.HUx[k];
+          A.HUyo[k] = A.HUy[k];
+          peer_store(G, A, i, r, A.H[k], A.HUx[k], A.HUy[k]);
+        }
+      }
+      if (tid == 0) A.tile_same[tile] = 1;
+      if (A.peer[0][0] || A.peer[1][0]) __threadfence_system();
+    }
+    if (tid < 3) A.part[5 * (size_t)tile + tid] = 0.0;
+    return;
+  }
+
+  const double tau = sc->tau;
+  const int bi_lo = i0 / G.bs, bj_lo = (G.jg0 + r0) / G.bs;
+  const int nbi = (min(i0 + BX, G.nx) - 1) / G.bs - bi_lo + 1;
+  const int nbj = (min(G.jg0 + r0 + BY, G.jg0 + G.r1) - 1) / G.bs - bj_lo + 1;
+  const bool bf_staged = nbi * nbj <= MAXBF;
+  if (bf_staged && tid < nbi * nbj)
+    s_bf[tid] = A.bflag[(bi_lo + tid % nbi) + (bj_lo + tid / nbi - G.bj0) * G.nbx];
+  if (tid >= XTHR - BX) s_bcol[tid - (XTHR - BX)] = (i0 + tid - (XTHR - BX)) / G.bs;
+  else if (tid >= XTHR - BX - BY) s_brow[tid - (XTHR - BX - BY)] = (G.jg0 + r0 + tid - (XTHR - BX - BY)) / G.bs;
+  else if (tid < 9) {
+    const int ntx = tx + tid % 3 - 1, nty = ty + tid / 3 - 1;
+    // outside the owned tile rows: ghost rows (k_ghost_half) count as visited
+    s_nact[tid] = (ntx < 0 || ntx >= G.tiles_x) ? 0
+                  : (nty < 0 || nty >= G.tiles_y) ? 1
+                  : ((A.tile_act[ntx + nty * G.tiles_x] & 2) != 0);
+  }
+  __syncthreads();
+
+  // ---- F1: the half-step view on the region (tile + 2-cell halo) ----------
+  for (int c = tid; c < RREG; c += XTHR) {
+    const int xr = c % RX, yr = c / RX;
+    const int i = i0 - 2 + xr, r = r0 - 2 + yr;
+    double d = 0.0, e = 0.0, u = 0.0, v = 0.0, sx = 0.0, sy = 0.0, bb = 0.0;
+    if (i >= 0 && i < G.nx && r >= 0 && r < G.rows) {
+      const size_t k = (size_t)i + (size_t)r * nx;
+      const int gx = xr < 2 ? 0 : (xr < BX + 2 ? 1 : 2);
+      const int gy = yr < 2 ? 0 : (yr < BY + 2 ? 1 : 2);
+      const bool ghost = r < G.r0 || r >= G.r1;
+      bb = A.b[k];
+      if (ghost || s_nact[gx + 3 * gy]) {
+        d = A.hd[k];
+        u = A.hu[k];
+        v = A.hv[k];
+      } else {
+        d = A.H[k];  // not active: the state itself, at rest
+      }
+      e = d + bb;
+      // shift = 0.5*dr, dr = tau*u12 (stepper.cpp:72-73, 373-379); 0 for an
+      // inactive cell, whose u is 0
+      sx = 0.5 * (tau * u);
+      sy = 0.5 * (tau * v);
+    }
+    R[F_D * RREG + c] = d;
+    R[F_E * RREG + c] = e;
+    R[F_U * RREG + c] = u;
+    R[F_V * RREG + c] = v;
+    R[F_SX * RREG + c] = sx;
+    R[F_SY * RREG + c] = sy;
+    R[F_B * RREG + c] = bb;
+  }
+  __syncthreads();
+    constexpr int PER = (BX * BY + XTHR - 1) / XTHR;  // owned cells per thread
+  // ---- phase 3x: x slopes of columns -1..BX (rows of the tile) -------------
+  for (int c = tid; c < (BX + 2) * BY; c += XTHR) {
+    int xx = c % (BX + 2), y = c / (BX + 2);
+    int i = i0 - 1 + xx;
+    int s = (xx + 1) + (y + 2) * RX;
+    double se = 0.0, su = 0.0, st = 0.0;
+    if (i > 0 && i + 1 < G.nx && R[F_D * RREG + s] > P.eps) {
+      Slopes q = cell_slopes(R[F_E * RREG + s - 1], R[F_U * RREG + s - 1], R[F_V * RREG + s - 1],
+                             R[F_SX * RREG + s - 1], R[F_E * RREG + s], R[F_U * RREG + s],
+                             R[F_V * RREG + s], R[F_SX * RREG + s], R[F_E * RREG + s + 1],
+                             R[F_U * RREG + s + 1], R[F_V * RREG + s + 1], R[F_SX * RREG + s + 1],
+                             P.h, SP);
+      se = q.eta;
+      su = q.un;
+      st = q.ut;
+    }
+    SL[0 * NSL + c] = se;
+    SL[1 * NSL + c] = su;
+    SL[2 * NSL + c] = st;
+  }
+  __syncthreads();
+
+  // ---- phase 4x: x faces (stepper.cpp:402-447, 496-516) ----------------------
+  double outflow = 0.0;
+  const double face_p = (1.0 * 0.5) * P.h, face_m = (-1.0 * 0.5) * P.h;
+  for (int c = tid; c < (BX + 1) * BY; c += XTHR) {
+    int fx = c % (BX + 1), y = c / (BX + 1);
+    int f = i0 + fx, r = r0 + y;
+    FaceRec rec;
+    rec.fm = rec.fnl = rec.fnr = rec.ft = 0.0;
+    if (f <= G.nx && r < G.r1) {
+      int jg = G.jg0 + r;
+      int sa = (fx + 1) + (y + 2) * RX;  // cell f-1
+      if (f == 0 || f == G.nx) {
+        bool lo = f == 0;
+        int se = lo ? sa + 1 : sa;
+        double H = R[F_D * RREG + se];
+        bool wet = H > P.eps;
+        rec = boundary_face(wet, H, R[F_U * RREG + se], R[F_V * RREG + se], lo,
+                            lo ? G.west_refl : G.east_refl, P.g);
+        outflow += lo ? -rec.fm : rec.fm;
+      } else {
+        int la = fx + y * (BX + 2), lb = la + 1;  // slope slots of cells f-1, f
+        double dA = R[F_D * RREG + sa], dB = R[F_D * RREG + sa + 1];
+        bool wetA = dA > P.eps, wetB = dB > P.eps;
+        if (wetA || wetB) {
+          double bA = R[F_B * RREG + sa], bB = R[F_B * RREG + sa + 1];
+          double bf = smax(bA, bB);
+          SideState L, Rr;
+          L.hs = L.hcell = L.un = L.ut = 0.0;
+          Rr = L;
+          if (wetA) {
+            Slopes q = {SL[la], SL[NSL + la], SL[2 * NSL + la]};
+            L = side_from_slopes(R[F_E * RREG + sa], R[F_U * RREG + sa], R[F_V * RREG + sa],
+                                 R[F_SX * RREG + sa], bA, q, face_p, bf);
+          }
+          if (wetB) {
+            Slopes q = {SL[lb], SL[NSL + lb], SL[2 * NSL + lb]};
+            Rr = side_from_slopes(R[F_E * RREG + sa + 1], R[F_U * RREG + sa + 1],
+                                  R[F_V * RREG + sa + 1], R[F_SX * RREG + sa + 1], bB, q, face_m,
+                                  bf);
+          }
+          rec = face_from_sides(wetA, wetB, L, Rr, P.g, SP);
+          if (!face_finite(rec)) {
+            unsigned long long key = fused_flux_key(G, A.bflag, 0, jg, f);
+            my_err = key < my_err ? key : my_err;
+          }
+        }
+      }
+    }
+    FB[0 * NFC + c] = rec.fm;
+    FB[1 * NFC + c] = rec.fnl;
+    FB[2 * NFC + c] = rec.fnr;
+    FB[3 * NFC + c] = rec.ft;
+  }
+  __syncthreads();
+  // face taps (nested-grid flux correction): each tile records its west
+  // faces only (fx < BX), so every face is written once; faces no active
+  // tile computes stay 0 (dry)
+  if (A.taps.n) {
+    for (int c = tid; c < (BX + 1) * BY; c += XTHR) {
+      const int fx = c % (BX + 1), y = c / (BX + 1), f = i0 + fx, jg = G.jg0 + r0 + y;
+      for (int q = 0; q < A.taps.n; ++q)
+        if (fx < BX && r0 + y < G.r1 && (f == A.taps.i0[q] || f == A.taps.i0[q] + A.taps.ni[q]) &&
+            jg >= A.taps.j0[q] && jg < A.taps.j0[q] + A.taps.nj[q])
+          A.taps.out[q][(f == A.taps.i0[q] ? 0 : A.taps.nj[q]) + (jg - A.taps.j0[q])] =
+              tau * FB[0 * NFC + c];
+    }
+  }
+  double px_m[PER], px_a[PER], px_c[PER];  // (W.fm-E.fm), (W.fnr-E.fnl), (W.ft-E.ft)
+#pragma unroll
+  for (int m = 0; m < PER; ++m) {
+    int c = tid + m * XTHR;
+    if (BX * BY % XTHR && c >= BX * BY) break;
+    int x = c % BX, y = c / BX;
+    int w = x + y * (BX + 1), e = w + 1;
+    px_m[m] = FB[0 * NFC + w] - FB[0 * NFC + e];
+    px_a[m] = FB[2 * NFC + w] - FB[1 * NFC + e];
+    px_c[m] = FB[3 * NFC + w] - FB[3 * NFC + e];
+  }
+
+  // ---- phase 3y: y slopes of rows -1..BY (columns of the tile) -------------
+  for (int c = tid; c < BX * (BY + 2); c += XTHR) {
+    int x = c % BX, yy = c / BX;
+    int r = r0 - 1 + yy, jg = G.jg0 + r;
+    int s = (x + 2) + (yy + 1) * RX;
+    double se = 0.0, su = 0.0, st = 0.0;
+    if (jg > 0 && jg + 1 < G.ny && i0 + x < G.nx && R[F_D * RREG + s] > P.eps) {
+      Slopes q = cell_slopes(R[F_E * RREG + s - RX], R[F_V * RREG + s - RX],
+                             R[F_U * RREG + s - RX], R[F_SY * RREG + s - RX], R[F_E * RREG + s],
+                             R[F_V * RREG + s], R[F_U * RREG + s], R[F_SY * RREG + s],
+                             R[F_E * RREG + s + RX], R[F_V * RREG + s + RX],
+                             R[F_U * RREG + s + RX], R[F_SY * RREG + s + RX], P.h, SP);
+      se = q.eta;
+      su = q.un;
+      st = q.ut;
+    }
+    SL[0 * NSL + c] = se;
+    SL[1 * NSL + c] = su;
+    SL[2 * NSL + c] = st;
+  }
+  __syncthreads();
+
+  // ---- phase 4y: y faces (stepper.cpp:449-494, 518-538) ----------------------
+  for (int c = tid; c < BX * (BY + 1); c += XTHR) {
+    int x = c % BX, fy = c / BX;
+    int i = i0 + x, rf = r0 + fy;  // face between local rows rf-1 and rf
+    int jf = G.jg0 + rf;           // global face index
+    FaceRec rec;
+    rec.fm = rec.fnl = rec.fnr = rec.ft = 0.0;
+    if (i < G.nx && rf <= G.r1) {
+      int sa = (x + 2) + (fy + 1) * RX;  // cell rf-1
+      if (jf == 0 || jf == G.ny) {
+        bool lo = jf == 0;
+        int se = lo ? sa + RX : sa;
+        double H = R[F_D * RREG + se];
+        bool wet = H > P.eps;
+        rec = boundary_face(wet, H, R[F_V * RREG + se], R[F_U * RREG + se], lo,
+                            lo ? G.south_refl : G.north_refl, P.g);
+        outflow += lo ? -rec.fm : rec.fm;
+      } else {
+        int la = x + fy * BX, lb = la + BX;  // slope slots of rows rf-1, rf
+        double dA = R[F_D * RREG + sa], dB = R[F_D * RREG + sa + RX];
+        bool wetA = dA > P.eps, wetB = dB > P.eps;
+        if (wetA || wetB) {
+          double bA = R[F_B * RREG + sa], bB = R[F_B * RREG + sa + RX];
+          double bf = smax(bA, bB);
+          SideState L, Rr;
+          L.hs = L.hcell = L.un = L.ut = 0.0;
+          Rr = L;
+          if (wetA) {
+            Slopes q = {SL[la], SL[NSL + la], SL[2 * NSL + la]};
+            L = side_from_slopes(R[F_E * RREG + sa], R[F_V * RREG + sa], R[F_U * RREG + sa],
+                                 R[F_SY * RREG + sa], bA, q, face_p, bf);
+          }
+          if (wetB) {
+            Slopes q = {SL[lb], SL[NSL + lb], SL[2 * NSL + lb]};
+            Rr = side_from_slopes(R[F_E * RREG + sa + RX], R[F_V * RREG + sa + RX],
+                                  R[F_U * RREG + sa + RX], R[F_SY * RREG + sa + RX], bB, q,
+                                  face_m, bf);
+          }
+          rec = face_from_sides(wetA, wetB, L, Rr, P.g, SP);
+          if (!face_finite(rec)) {
+            unsigned long long key = fused_flux_key(G, A.bflag, 1, i, jf);
+            my_err = key < my_err ? key : my_err;
+          }
+        }
+      }
+    }
+    FB[0 * NFC + c] = rec.fm;
+    FB[1 * NFC + c] = rec.fnl;
+    FB[2 * NFC + c] = rec.fnr;
+    FB[3 * NFC + c] = rec.ft;
+  }
+  __syncthreads();
+  if (A.taps.n) {
+    for (int c = tid; c < BX * (BY + 1); c += XTHR) {
+      const int x = c % BX, fy = c / BX, i = i0 + x, rf = r0 + fy, jf = G.jg0 + rf;
+      for (int q = 0; q < A.taps.n; ++q)
+        if (fy < BY && i < G.nx && rf < G.r1 &&
+            (jf == A.taps.j0[q] || jf == A.taps.j0[q] + A.taps.nj[q]) && i >= A.taps.i0[q] &&
+            i < A.taps.i0[q] + A.taps.ni[q])
+          A.taps.out[q][2 * A.taps.nj[q] + (jf == A.taps.j0[q] ? 0 : A.taps.ni[q]) +
+                        (i - A.taps.i0[q])] = tau * FB[0 * NFC + c];
+    }
+  }
+
+  // ---- phase 5: accumulate (stepper.cpp:540-566) + final (628-659) ---------
+  double deficit = 0.0;
+  const double dt_h = tau / P.h;
+#pragma unroll
+  for (int m = 0; m < PER; ++m) {
+    int c = tid + m * XTHR;
+    if (BX * BY % XTHR && c >= BX * BY) break;
+    int x = c % BX, y = c / BX;
+    int i = i0 + x, r = r0 + y;
+    if (i >= G.nx || r >= G.r1) continue;
+    int jg = G.jg0 + r;
+    int s = (x + 2) + (y + 2) * RX;
+    size_t k = (size_t)i + (size_t)r * nx;
+    const int bc = s_bcol[x], br = s_brow[y];  // i / bs, jg / bs
+    unsigned char bfl = bf_staged ? s_bf[(bc - bi_lo) + (br - bj_lo) * nbi]
+                                  : A.bflag[bc + (br - G.bj0) * G.nbx];
+    bool flux_on = !G.skip || (bfl & 2);
+    // the base state k_lag left: the Lagrangian state of an active cell, the
+    // step-start state otherwise (stepper.cpp:641-651)
+    const double Htm = A.Ho[k], Qxm = A.HUxo[k], Qym = A.HUyo[k];
+    if (!flux_on) {  // block skipped by the reference: state unchanged
+      peer_store(G, A, i, r, Htm, Qxm, Qym);
+      continue;
+    }
+    int sf = x + y * BX, nf_ = sf + BX;  // S and N face of the cell
+    double py_m = FB[0 * NFC + sf] - FB[0 * NFC + nf_];
+    double py_a = FB[2 * NFC + sf] - FB[1 * NFC + nf_];  // S.fnr - N.fnl
+    double py_c = FB[3 * NFC + sf] - FB[3 * NFC + nf_];  // S.ft - N.ft
+    double d = R[F_D * RREG + s];
+    bool wet = d > P.eps;
+    double cx = 0.0, cy = 0.0;
+    if (wet) {
+      auto nb = [&](bool in, int q) {
+        return SNbr{in, R + F_D * RREG, R + F_E * RREG, R + F_U * RREG, R + F_V * RREG, q};
+      };
+      double eta_c = R[F_E * RREG + s];
+      double gx = eta_grad_comp(nb(i > 0, s - 1), nb(i + 1 < G.nx, s + 1), eta_c, P, SP);
+      double gy = eta_grad_comp(nb(jg > 0, s - RX), nb(jg + 1 < G.ny, s + RX), eta_c, P, SP);
+      double gh = (P.g * d) * P.h;
+      cx = gh * gx;
+      cy = gh * gy;
+    }
+    double Fh = px_m[m] + py_m;
+    double Fvx = (px_a[m] + py_c) + cx;
+    double Fvy = (py_a + px_c[m]) + cy;
+    double H1, qx, qy, dfc;
+    final_cell(Htm, Qxm, Qym, Fh, Fvx, Fvy, dt_h, P.eps, H1, qx, qy, dfc);
+    deficit += dfc;
+    // staged: the base state lives in the output buffers, so a tile whose
+    // speculation failed must leave them intact for its exact redo
+    SL[c] = H1;
+    SL[BX * BY + c] = qx;
+    SL[2 * BX * BY + c] = qy;
+  }
+  const bool any_bad = __syncthreads_or(!sok);
+  if (!(SPEC && any_bad)) {
+#pragma unroll
+    for (int m = 0; m < PER; ++m) {
+      int c = tid + m * XTHR;
+      if (BX * BY % XTHR && c >= BX * BY) break;
+      int x = c % BX, y = c / BX;
+      int i = i0 + x, r = r0 + y;
+      if (i >= G.nx || r >= G.r1) continue;
+      const int bc = s_bcol[x], br = s_brow[y];
+      unsigned char bfl = bf_staged ? s_bf[(bc - bi_lo) + (br - bj_lo) * nbi]
+                                    : A.bflag[bc + (br - G.bj0) * G.nbx];
+      if (G.skip && !(bfl & 2)) continue;
+      size_t k = (size_t)i + (size_t)r * nx;
+      const double H1 = SL[c], qx = SL[BX * BY + c], qy = SL[2 * BX * BY + c];
+      A.Ho[k] = H1;
+      A.HUxo[k] = qx;
+      A.HUyo[k] = qy;
+      if (A.hH) {  // host-buffer step: write the updated cell straight into the caller's arrays
+        A.hH[k] = H1;
+        A.hHUx[k] = qx;
+        A.hHUy[k] = qy;
+      }
+      peer_store(G, A, i, r, H1, qx, qy);
+    }
+    if (tid == 0) A.tile_same[tile] = 0;
+    // the neighbour reads these rows after a stream-ordered token from us:
+    // make the peer stores visible system-wide before this kernel completes
+    if (A.peer[0][0] || A.peer[1][0]) __threadfence_system();
+  }
+
+
+  // ---- per-tile diagnostic partials (deterministic) ------------------------
+  double v2[2] = {deficit, outflow};
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    double v = v2[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((tid & 31) == 0) s_red[q][tid >> 5] = v;
+  }
+  __syncthreads();
+  if (tid < 2) {
+    double v = 0.0;
+    for (int w = 0; w < XTHR / 32; ++w) v += s_red[tid][w];
+    A.part[5 * (size_t)tile + 2 * tid] = v;  // [0] deficit, [2] outflow
+  }
+  if (SPEC && any_bad) {
+    if (tid == 0) A.redo[atomicAdd(&sc->redo_n[1], 1)] = tile;
+  } else if (my_err != ERR_NONE) {
+    atomicMin(&sc->err_key, my_err);
+  }
+}
+
+__global__ void __launch_bounds__(XTHR, SWF_FLUX_MINB) k_flux_list(Geo G, StepArgs A) {
+  __shared__ int s_next;
+  StepScalars* sc = A.sc;
+  const int n = *(volatile int*)&sc->list_n[1];
+  while (true) {
+    if (threadIdx.x == 0) s_next = atomicAdd(&sc->list_take[1], 1);
+    __syncthreads();
+    const int q = s_next;
+    __syncthreads();
+    if (q >= n) break;
+    flux_tile<SWF_SPECULATE != 0>(G, A, A.list[q]);
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(XTHR, SWF_FLUX_MINB) k_flux_redo(Geo G, StepArgs A) {
+  const int n = *(volatile int*)&A.sc->redo_n[1];
+  for (int q = blockIdx.x; q < n; q += gridDim.x) {
+    flux_tile<false>(G, A, A.redo[q]);
+    __syncthreads();
+  }
+}
+
 // k_reduce: RED_CTAS fixed-order partial sums of the per-tile partials
 // (deficit, source volume, outflow, Lagrangian blocks, flux blocks; coalesced,
 // deterministic); k_finish adds them in CTA order and commits t.
@@ -1411,6 +2111,10 @@ StepArgs step_args(swf_ctx* c) {
   A.list = c->d_list_s;
   A.part = c->d_part;
   A.sc = c->d_sc;
+  A.hd = c->d_half[0];
+  A.hu = c->d_half[1];
+  A.hv = c->d_half[2];
+  A.redo_l = c->d_redo_l;
   return A;
 }
 
@@ -1587,15 +2291,26 @@ int fused_enqueue_phase2(swf_ctx* c, double dt_cap, double global_speed, const d
   for (int q = 0; q < c->taps.n; ++q)
     cudaMemsetAsync(c->taps.out[q], 0,
                     2 * (size_t)(c->taps.ni[q] + c->taps.nj[q]) * sizeof(double), c->stream);
-  if (nt > 0 && SWF_TILE_LISTS) {
+  if (nt > 0 && SWF_TILE_LISTS && SWF_SPLIT) {
     StepArgs SA = step_args(c);
     k_slist<<<(nt + 255) / 256, 256, 0, c->stream>>>(G, SA);
-    k_step_list<<<c->sm_count * SWF_STEP_MINB, STHR, step_smem(), c->stream>>>(G, SA);
-  } else if (nt > 0) {
-    k_step<<<nt, STHR, step_smem(), c->stream>>>(G, step_args(c));
+    k_lag_list<<<c->sm_count * SWF_LAG_MINB, LTHR, lag_smem(), c->stream>>>(G, SA);
+    if (SWF_SPECULATE) k_lag_redo<<<RED_CTAS, LTHR, lag_smem(), c->stream>>>(G, SA);
+    if (G.r0 > 0 || G.r1 < G.rows)
+      k_ghost_half<<<(4 * G.nx + 127) / 128, 128, 0, c->stream>>>(G, SA);
+    k_flux_list<<<c->sm_count * SWF_FLUX_MINB, XTHR, flux_smem(), c->stream>>>(G, SA);
+    if (SWF_SPECULATE) k_flux_redo<<<RED_CTAS, XTHR, flux_smem(), c->stream>>>(G, SA);
+  } else {
+    if (nt > 0 && SWF_TILE_LISTS) {
+      StepArgs SA = step_args(c);
+      k_slist<<<(nt + 255) / 256, 256, 0, c->stream>>>(G, SA);
+      k_step_list<<<c->sm_count * SWF_STEP_MINB, STHR, step_smem(), c->stream>>>(G, SA);
+    } else if (nt > 0) {
+      k_step<<<nt, STHR, step_smem(), c->stream>>>(G, step_args(c));
+    }
+    if (nt > 0 && SWF_SPECULATE)
+      k_step_redo<<<RED_CTAS, STHR, step_smem(), c->stream>>>(G, step_args(c));
   }
-  if (nt > 0 && SWF_SPECULATE)
-    k_step_redo<<<RED_CTAS, STHR, step_smem(), c->stream>>>(G, step_args(c));
   ev(c, 4);
   double* red = c->d_part + NPART * (size_t)(nt > 0 ? nt : 1);
   k_reduce<<<RED_CTAS, NTHR, 0, c->stream>>>(c->d_part, nt, red, c->d_sc);
@@ -1795,6 +2510,24 @@ int fused_prepare(swf_ctx* c) {
   if (e == cudaSuccess && !c->d_list_s) e = cudaMalloc(&c->d_list_s, nredo * sizeof(int));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_step, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  // split step: its kernels' shared memory and the half-step view planes
+  for (auto f : {(const void*)k_lag_list, (const void*)k_lag_redo}) {
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lag_smem());
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  }
+  for (auto f : {(const void*)k_flux_list, (const void*)k_flux_redo}) {
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)flux_smem());
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  }
+  if (e == cudaSuccess && SWF_SPLIT && !c->d_redo_l) e = cudaMalloc(&c->d_redo_l, nredo * sizeof(int));
+  for (int q = 0; q < 3 && e == cudaSuccess && SWF_SPLIT; ++q) {
+    if (c->d_half[q]) continue;
+    const size_t bytes = (local_cells(c) ? local_cells(c) : 1) * sizeof(double);
+    e = cudaMalloc(&c->d_half[q], bytes);
+    if (e == cudaSuccess) e = cudaMemset(c->d_half[q], 0, bytes);
+  }
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_forces, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   return cuda_check(c, e, "kernel attributes");

@@ -44,9 +44,9 @@ struct StepScalars {
   int mask_valid;  // the tile flags of the previous step describe the current state
   int mask_fresh;  // != 0: k_mask/k_tiles just flagged the current state (host step);
                    // cleared by k_tau
-  int redo_n[2];   // tiles queued for the exact redo: [0] k_forces, [1] k_step
-  int list_n[2];   // work-list lengths: [0] k_forces, [1] k_step
-  int list_take[2];  // work-list cursors of the persistent grids
+  int redo_n[3];   // tiles queued for the exact redo: [0] k_forces, [1] k_step / k_flux, [2] k_lag
+  int list_n[2];   // work-list lengths: [0] k_forces, [1] k_step (k_lag and k_flux share it)
+  int list_take[3];  // work-list cursors of the persistent grids: [2] k_lag
 };
 
 // ERR_PEER: stopped because another strip of a swf_group aborted (ranks
@@ -129,6 +129,10 @@ struct swf_ctx {
   int* d_redo_s = nullptr;  // k_step tiles to redo exactly
   int* d_list_f = nullptr;  // k_forces work list
   int* d_list_s = nullptr;  // k_step work list
+  int* d_redo_l = nullptr;  // k_lag tiles to redo exactly (split step)
+  // split step (SWF_SPLIT): the half-step view (depth, u, v) k_lag leaves for
+  // k_flux, local cells each
+  double* d_half[3] = {nullptr, nullptr, nullptr};
   int sm_count = 148;
   swf::FaceTaps taps;  // owned by the nests that registered them
   // P2P halo: the neighbours' state buffers mapped here ([side][field][parity])

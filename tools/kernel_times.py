@@ -39,6 +39,18 @@ def main():
         out["active_tiles"] = na
     except Exception as e:  # older library builds
         out["redo_tiles"] = str(e)[:40]
+    if os.environ.get("SWF_HASH", "1") != "0":  # bitwise identity across library variants
+        import hashlib
+        import numpy as np
+        st.sync()
+        h = hashlib.sha256()
+        s = sc.state
+        st.download(s)
+        for a in (s.H, s.HUx, s.HUy):
+            a = a.cpu().numpy() if hasattr(a, "cpu") else np.asarray(a)
+            h.update(np.ascontiguousarray(a).tobytes())
+        h.update(repr(s.t).encode())
+        out["state_sha"] = h.hexdigest()[:16]
     print(json.dumps(out), flush=True)
 
 

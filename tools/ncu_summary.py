@@ -65,6 +65,41 @@ def launch_shares(path):
             "all_kernels_ms": {k: round(v, 4) for k, v in t.most_common()}}
 
 
+FP64_OPS = ("DADD", "DMUL", "DFMA", "DSETP", "DMNMX")
+
+
+def fp64_share(rep):
+    """Share of the FP64-pipe instructions (DADD, DMUL, DFMA, DSETP, DMNMX)
+    among the executed warp instructions of each kernel, from the source page
+    (per-SASS-instruction executed counts)."""
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
+    out, kern, hdr = {}, None, None
+    tot, fp = collections.Counter(), collections.Counter()
+    for r in csv.reader(io.StringIO(txt)):
+        if len(r) >= 2 and r[0] == "Kernel Name":
+            kern = short(r[1])
+            continue
+        if r and r[0] == "Address":
+            hdr = {h: j for j, h in enumerate(r)}
+            continue
+        if kern is None or hdr is None or len(r) < len(hdr):
+            continue
+        n = r[hdr["Instructions Executed"]]
+        if not n.isdigit():
+            continue
+        op = r[hdr["Source"]].strip()
+        if op.startswith("@"):
+            op = op.split(None, 1)[1] if " " in op else op
+        op = op.split(" ")[0].split(".")[0]
+        tot[kern] += int(n)
+        if op in FP64_OPS:
+            fp[kern] += int(n)
+    for k in tot:
+        out[k] = fp[k] / tot[k] if tot[k] else 0.0
+    return out
+
+
 def main():
     d, tag = sys.argv[1], sys.argv[2]
     raw = subprocess.run(["ncu", "-i", os.path.join(d, "prof.ncu-rep"), "--page", "raw", "--csv"],
@@ -81,6 +116,7 @@ def main():
             w.writerow([short(r[ix["Kernel Name"]])] + [r[ix[k]] for k in KEYS if k in ix])
     summ = {"source": f"profiles/ncu_details_{tag}.csv (ncu --set full --clock-control none, "
                       f"C3 16384^2, build {tag})", "kernels": {}}
+    share = fp64_share(os.path.join(d, "prof.ncu-rep"))
     for r in rows[2:]:
         k = short(r[ix["Kernel Name"]])
 
@@ -95,6 +131,8 @@ def main():
             "fp64_pipe_pct": g("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
             "issue_active_pct": g("smsp__issue_active.avg.pct_of_peak_sustained_active"),
             "inst_executed": g("smsp__inst_executed.sum"),
+            # FP64-pipe warp instructions per launch (source-page share x total)
+            "fp64_inst_executed": round(g("smsp__inst_executed.sum") * share.get(k, 0.0)),
         }
     lp = os.path.join(d, "launches.csv")
     if os.path.exists(lp):
