@@ -348,6 +348,28 @@ def b200_single(args):
     e2e_s = time.perf_counter() - t0
     e2e_value = N * E / e2e_s / 1e6
 
+    # ---- the same host steps with the opt-in host mirror (swf_set_host_mirror):
+    # the caller changes its pinned arrays only through step(), so the inputs
+    # are already on the device; every step still writes its result into them
+    st.set_host_mirror(True)
+    st.step(hs)  # establishes the mirror (one full upload)
+    torch.cuda.synchronize()
+    md2h = mh2d = 0
+    t0 = time.perf_counter()
+    for _ in range(E):
+        st.step(hs)
+        na, _, cpt = st.active_tiles()
+        md2h += 3 * 8 * na * cpt + 8
+        mh2d += st.last_ingest_bytes() + 8
+    mirror_s = time.perf_counter() - t0
+    st.set_host_mirror(False)
+    e2e_mirror = {"value": round(N * E / mirror_s / 1e6, 3), "unit": "Mcells/s",
+                  "h2d_bytes_per_step": int(mh2d // E), "d2h_bytes_per_step": int(md2h // E),
+                  "how": "as e2e, with the opt-in host mirror (swf_set_host_mirror, SURVEY.md 8b "
+                         "Ownership): the caller's pinned arrays change only through step(), so "
+                         "no host->device copy is needed; k_step still writes every updated "
+                         "cell into them, t read back; host-timed, synchronised"}
+
     cpu = None
     if not args.no_cpu_baseline:
         try:
@@ -411,6 +433,7 @@ def b200_single(args):
                        "writes overlapped with the arithmetic; restored on a numerical abort), "
                        "t read back; d2h counts the flux-active tiles (an upper bound); "
                        "host-timed, synchronised"},
+        "e2e_host_mirror": e2e_mirror,
         "gpu_launches": 10 * K,  # begin, flist, forces, forces_redo, tau, slist, step, step_redo, reduce, finish
         "clocks": clk,
         "cpu_baseline": cpu,

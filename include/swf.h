@@ -161,6 +161,16 @@ int swf_step_host(swf_ctx* ctx, double* H, double* HUx, double* HUy,
  * zero-copy ingest; afterwards the resident calls need swf_upload_state);
  * otherwise the three full fields. */
 int swf_last_ingest_bytes(const swf_ctx* ctx, long long* bytes);
+/* Opt-in host mirror for swf_step_host on PINNED arrays (SURVEY.md §8b,
+ * "Ownership"; off by default).  On: after a host step the device keeps
+ * the state it wrote into the caller's arrays, and the next host step with
+ * the SAME arrays and the t it returned skips every host->device copy (the
+ * first step, other arrays, another t, or any resident/upload/stage call in
+ * between make it upload the three fields in full once).  The caller
+ * promises not to change the arrays between host steps, or declares a
+ * change with swf_host_changed(ctx).  Results are identical either way. */
+int swf_set_host_mirror(swf_ctx* ctx, int on);
+int swf_host_changed(swf_ctx* ctx);
 /* Tiles of the last synchronised step whose speculative divisions were
  * rejected and that were recomputed exactly: counts[0] forces, [1] step
  * (diagnostics; see the speculative-division note in swf_fused.cu). */

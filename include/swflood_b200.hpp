@@ -260,6 +260,13 @@ class CsphTvdStepper {
 
   struct HalfView;  // stepper.hpp:121 (the half-step view lives on the device here)
 
+  // Opt-in host mirror (swf_set_host_mirror, SURVEY.md 8b "Ownership"):
+  // step() on the same FlowState, with its arrays in pinned memory, skips the
+  // host->device copies as long as the caller changes the state only through
+  // step(); host_changed() declares an edit.  Off by default.
+  void set_host_mirror(bool on);
+  void host_changed();
+
   swf_ctx* native() const { return ctx_; }  // the C-ABI context (resident API; strip 0 if devices > 1)
 
  private:

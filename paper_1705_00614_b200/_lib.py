@@ -69,6 +69,8 @@ def declare(lib):
     _sig(lib, "swf_strip_pack", I, P, I, C.c_void_p)
     _sig(lib, "swf_strip_unpack", I, P, I, C.c_void_p)
     _sig(lib, "swf_last_ingest_bytes", I, P, C.POINTER(C.c_longlong))
+    _sig(lib, "swf_set_host_mirror", I, P, I)
+    _sig(lib, "swf_host_changed", I, P)
     _sig(lib, "swf_debug_redo_counts", I, P, PI)
     _sig(lib, "swf_device_buffers", I, P, C.POINTER(C.c_void_p))
     _sig(lib, "swf_strip_set_peer", I, P, I, C.POINTER(C.c_void_p), I)

@@ -152,6 +152,12 @@ struct swf_ctx {
   // the flux-active tiles only: resident calls need a fresh upload first
   int state_partial = 0;
   double* wt_host[3] = {nullptr, nullptr, nullptr};  // write-through targets of a host step
+  // opt-in host mirror (swf_set_host_mirror): the caller's pinned arrays
+  // equal the device state after the last host step (SURVEY.md 8b Ownership)
+  int host_mirror = 0;
+  int mirror_valid = 0;
+  const double* mirror_ptr[3] = {nullptr, nullptr, nullptr};
+  double mirror_t = 0.0;
   long long last_ingest_bytes = 0;
   int batch_steps = 0;
   int last_staged = 0;  // which path produced the last diagnostics

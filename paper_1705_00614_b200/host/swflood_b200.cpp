@@ -583,6 +583,14 @@ void CsphTvdStepper::set_wind(WindForcing wind) {
   wind_ = std::move(wind);
 }
 
+void CsphTvdStepper::set_host_mirror(bool on) {
+  for (swf_ctx* c : contexts()) check(swf_set_host_mirror(c, on ? 1 : 0));
+}
+
+void CsphTvdStepper::host_changed() {
+  for (swf_ctx* c : contexts()) check(swf_host_changed(c));
+}
+
 void CsphTvdStepper::set_sources(std::vector<SourceSpec> sources) {
   for (const SourceSpec& s : sources) s.validate(*terrain_);
   CSources cs(sources);

@@ -218,6 +218,16 @@ class CsphTvdStepper:
         self._rc(self._lib.swf_last_ingest_bytes(self._ctx, C.byref(b)))
         return b.value
 
+    def set_host_mirror(self, on: bool = True) -> None:
+        """Opt-in host mirror (swf_set_host_mirror): step(state) on the same
+        pinned arrays skips the host->device copies while the caller leaves
+        them alone between steps (declare edits with host_changed())."""
+        self._rc(self._lib.swf_set_host_mirror(self._ctx, 1 if on else 0))
+
+    def host_changed(self) -> None:
+        """The caller edited the mirrored arrays: the next step uploads them."""
+        self._rc(self._lib.swf_host_changed(self._ctx))
+
     def redo_counts(self):
         """(forces, step) tiles of the last synchronised step recomputed
         exactly after a rejected speculative division."""

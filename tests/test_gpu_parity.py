@@ -453,6 +453,43 @@ def test_pinned_host_steps_follow_host_side_edits(gpu_cls, oracle_built):
     assert_state_bitwise(hs, cpu_state, "pinned steps with host-side edits")
 
 
+def test_host_mirror_steps_match_oracle(gpu_cls, oracle_built):
+    """Opt-in host mirror (swf_set_host_mirror): steady pinned host steps skip
+    every host->device copy, a declared edit (host_changed) re-uploads, and
+    the results stay bit-identical to the oracle."""
+    import torch
+    from paper_1705_00614_b200.types import FlowState
+    sc = S.floodplain(256, 50.0)
+    st = sc.state.copy()
+    pin = lambda a: torch.from_numpy(a.copy()).pin_memory().numpy()
+    hs = FlowState(st.nx, st.ny, 0.0, pin(st.H), pin(st.HUx), pin(st.HUy))
+    cpu_state = st.copy()
+    g = make(gpu_cls, sc)
+    g.set_host_mirror(True)
+    o = make(oracle_built.OracleStepper, sc)
+    ingest = []
+    for k in range(10):
+        if k == 6:  # an edit, declared
+            j, i = np.argwhere(hs.H.reshape(st.ny, st.nx) <= sc.params.eps_dry)[7]
+            for a in (hs, cpu_state):
+                a.H.reshape(st.ny, st.nx)[j, i] += 0.25
+            g.host_changed()
+        ia = g.step(hs)
+        ib = o.step(cpu_state)
+        ingest.append(g.last_ingest_bytes())
+        assert ia.tau == ib.tau, k
+    assert_state_bitwise(hs, cpu_state, "mirrored host steps")
+    full = 3 * 8 * st.nx * st.ny
+    assert ingest[0] == full and ingest[6] == full, ingest
+    assert all(ingest[k] == 0 for k in (1, 2, 3, 4, 5, 7, 8, 9)), ingest
+    # a resident call in between invalidates the mirror: the next host step re-uploads
+    g.upload(hs)
+    g.step(hs)
+    assert g.last_ingest_bytes() == full
+    o.step(cpu_state)
+    assert_state_bitwise(hs, cpu_state, "mirrored host steps after a re-upload")
+
+
 def test_speculative_division_redo_path_is_exact(gpu_cls, oracle_built):
     """Momenta in the subnormal range make the kernels' speculative divisions
     reject; those tiles are recomputed by the exact redo launches and the
