@@ -170,6 +170,11 @@ int swf_last_ingest_bytes(const swf_ctx* ctx, long long* bytes);
  * promises not to change the arrays between host steps, or declares a
  * change with swf_host_changed(ctx).  Results are identical either way. */
 int swf_set_host_mirror(swf_ctx* ctx, int on);
+/* "exact" (libswflood_cuda.so: bit-identical to the reference, -fmad=false)
+ * or "fast" (libswflood_cuda_fast.so, opt-in: FMA contraction, CUDA cbrt,
+ * reciprocal multiplications; validated to a stated tolerance with tau
+ * pinned, the wet/dry mask bit-exact -- tests/test_gpu_fast.py). */
+const char* swf_build_flavor(void);
 int swf_host_changed(swf_ctx* ctx);
 /* Tiles of the last synchronised step whose speculative divisions were
  * rejected and that were recomputed exactly: counts[0] forces, [1] step

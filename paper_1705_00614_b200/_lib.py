@@ -9,7 +9,11 @@ import os
 from . import _abi as A
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("SWF_LIB") or os.path.join(HERE, "libswflood_cuda.so")
+# SWF_FLAVOR=fast selects the opt-in FAST build (libswflood_cuda_fast.so);
+# SWF_LIB names any build explicitly (developer A/B variants)
+LIB_PATH = os.environ.get("SWF_LIB") or os.path.join(
+    HERE, "libswflood_cuda_fast.so" if os.environ.get("SWF_FLAVOR") == "fast"
+    else "libswflood_cuda.so")
 
 _lib = None
 
@@ -70,6 +74,7 @@ def declare(lib):
     _sig(lib, "swf_strip_unpack", I, P, I, C.c_void_p)
     _sig(lib, "swf_last_ingest_bytes", I, P, C.POINTER(C.c_longlong))
     _sig(lib, "swf_set_host_mirror", I, P, I)
+    _sig(lib, "swf_build_flavor", C.c_char_p)
     _sig(lib, "swf_host_changed", I, P)
     _sig(lib, "swf_debug_redo_counts", I, P, PI)
     _sig(lib, "swf_device_buffers", I, P, C.POINTER(C.c_void_p))

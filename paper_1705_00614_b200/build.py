@@ -26,10 +26,10 @@ def nvcc():
     return "nvcc"
 
 
-def stale():
-    if not os.path.exists(OUT):
+def stale(out=OUT):
+    if not os.path.exists(out):
         return True
-    t = os.path.getmtime(OUT)
+    t = os.path.getmtime(out)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
     deps.append(os.path.join(HERE, "..", "include", "swf.h"))
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
@@ -112,9 +112,17 @@ def _compile_link(out, flags, objdir, verbose=False):
                    + objs, check=True, cwd=CSRC)
 
 
+# The opt-in FAST build (include/swf.h swf_build_flavor): FMA contraction,
+# CUDA's cbrt, reciprocal multiplications -- tolerance-validated, not bit-exact.
+OUT_FAST = os.path.join(HERE, "libswflood_cuda_fast.so")
+FAST_FLAGS = [f for f in NVCC_FLAGS if f != "-fmad=false"] + ["-fmad=true", "-DSWF_FAST=1"]
+
+
 def build(force=False, verbose=False):
     if force or stale():
         _compile_link(OUT, NVCC_FLAGS, os.path.join(HERE, "..", "build", "obj"), verbose)
+    if force or stale(OUT_FAST):
+        _compile_link(OUT_FAST, FAST_FLAGS, os.path.join(HERE, "..", "build", "obj_fast"))
     build_host(force)
     return OUT
 

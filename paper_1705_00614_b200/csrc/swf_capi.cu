@@ -607,6 +607,7 @@ int swf_step(swf_ctx* c, double dt_cap, swf_step_info* info) {
 
 int swf_step_host(swf_ctx* c, double* H, double* HUx, double* HUy, double* t, double dt_cap,
                   swf_step_info* info) {
+  NvtxRange nv("swf_step_host");
   auto pinned = [](const void* p) {
     cudaPointerAttributes a;
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -722,6 +723,8 @@ int swf_step_host(swf_ctx* c, double* H, double* HUx, double* HUy, double* t, do
   return swf_download_state(c, H, HUx, HUy, t);
 }
 
+const char* swf_build_flavor(void) { return SWF_FAST ? "fast" : "exact"; }
+
 int swf_set_host_mirror(swf_ctx* c, int on) {
   if (!c) return SWF_ECONFIG;
   c->host_mirror = on ? 1 : 0;
@@ -749,6 +752,7 @@ int swf_last_ingest_bytes(const swf_ctx* c, long long* bytes) {
 }
 
 int swf_run(swf_ctx* c, int n, double dt_cap, int* done, swf_step_info* last) {
+  NvtxRange nv("swf_run");
   c->mirror_valid = 0;
   if (c->state_partial)
     return set_err(c, SWF_ECONFIG,

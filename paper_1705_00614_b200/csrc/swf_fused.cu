@@ -2181,6 +2181,7 @@ int launch_mid(swf_ctx* c, double tau) {
 // (a strip's interior, computable while its halo exchange is in flight);
 // 1 = the remaining (ghost-dependent) rows.
 int fused_enqueue_phase1(swf_ctx* c, double dt_cap, int part) {
+  NvtxRange nv("swf:forces (K1-K3)");
   const Geo& G = c->geo;
   int rc;
   bool fm = mask_fused(G);
@@ -2283,6 +2284,7 @@ int fused_local_speed(swf_ctx* c, double* dev_out) {
 }
 
 int fused_enqueue_phase2(swf_ctx* c, double dt_cap, double global_speed, const double* gspeed) {
+  NvtxRange nv("swf:step (tau, K4-K8, diagnostics)");
   const Geo& G = c->geo;
   k_tau<<<1, 1, 0, c->stream>>>(G, c->d_src, c->d_ht, c->d_hq, c->d_wt, c->d_wv, c->d_sig,
                                 c->d_sc, dt_cap, global_speed, gspeed);

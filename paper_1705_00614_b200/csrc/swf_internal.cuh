@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
 #include <string>
@@ -11,6 +12,16 @@
 #include "swf_math.cuh"
 
 namespace swf {
+
+// NVTX range over a host-side scope (SURVEY.md section 5 tracing): the
+// stage buckets of a step (forces phase, k_step phase), host steps and runs
+// show up by name in Nsight timelines.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // A source spec on the device (sources.hpp:25-36): rectangle, velocity, and
 // the per-step sigma values at t_n and t_mid (computed by the begin/tau

@@ -1,0 +1,97 @@
+"""The opt-in FAST build (libswflood_cuda_fast.so: FMA contraction, CUDA's
+cbrt, reciprocal multiplications) against the reference's algorithm (the
+oracle, pinned to the compiled reference).  It is not bit-exact by design;
+the contract north_star allows for it is a stated fp64 tolerance on H, Ux, Uy
+after N steps with the wet/dry mask bit-exact.  The time step is pinned
+through dt_cap (stepper.hpp:84-86: tau = min(dt_max, K h / speed, dt_cap)) so
+both runs advance by the same tau and the comparison measures the arithmetic,
+not a shifted trajectory.
+
+Tolerance (normwise, per field): max |fast - ref| <= RTOL * scale, with
+RTOL = 1e-12 after the stated steps, scale = max |H_ref| for the depth and
+max(max |U_ref|, sqrt(g max H_ref)) for the velocities; the mask
+(H > eps_dry) identical."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+RTOL = 1e-12
+FAST = os.path.join(ROOT, "paper_1705_00614_b200", "libswflood_cuda_fast.so")
+CASES = [("c1_dry_n002", 200), ("c1_wet_n0", 200), ("c2_256", 100), ("c3_crop", 40),
+         ("lake128", 100)]
+
+
+def test_fast_build_exists_and_exports_the_abi():
+    from paper_1705_00614_b200 import build as b
+    b.build()
+    import ctypes as C
+    lib = C.CDLL(FAST)
+    lib.swf_build_flavor.restype = C.c_char_p
+    assert lib.swf_build_flavor() == b"fast"
+    assert hasattr(lib, "swf_step_host") and hasattr(lib, "swf_run")
+
+
+def _oracle_run(case, steps, dt_cap):
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import fast_runner
+    from helpers import make
+    from oracle import pyorc
+    if not pyorc.available("orc"):
+        pyorc.build(ref=False)
+    sc = fast_runner.cases()[case]()
+    o = make(pyorc.OracleStepper, sc)
+    st = sc.state.copy()
+    o.upload(st)
+    taus = []
+    for _ in range(steps):
+        taus.append(o.run(1, dt_cap)[1].tau)
+    o.download(st)
+    return sc, st, np.array(taus)
+
+
+def _pinned_dt(case, steps):
+    """A dt_cap below every CFL tau of the reference run it caps (the
+    front's speeds depend on the step sizes, so shrink until it holds)."""
+    _, _, taus = _oracle_run(case, steps, 0.0)
+    for f in (0.9, 0.5, 0.25, 0.1, 0.05):
+        dt = float(f * taus.min())
+        sc, ref, t_ref = _oracle_run(case, steps, dt)
+        if np.all(t_ref == dt):
+            return dt, sc, ref, t_ref
+    raise AssertionError(f"{case}: no dt_cap pins tau over {steps} steps")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case,steps", CASES)
+def test_fast_build_within_tolerance_tau_pinned(case, steps, tmp_path):
+    dt, sc, ref, taus_ref = _pinned_dt(case, steps)
+    out = tmp_path / "fast.npz"
+    env = dict(os.environ, SWF_FLAVOR="fast")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "fast_runner.py"), str(out),
+                        case, str(steps), repr(dt)], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    f = np.load(out)
+    assert str(f["flavor"]) == "fast"
+    assert np.all(f["taus"] == dt) and np.all(taus_ref == dt)  # tau pinned in both runs
+    eps = sc.params.eps_dry
+    wet_f, wet_r = f["H"] > eps, ref.H > eps
+    assert np.array_equal(wet_f, wet_r), f"{int((wet_f != wet_r).sum())} mask flips"
+    w = wet_r
+    ux_r = np.where(w, ref.HUx / np.where(w, ref.H, 1.0), 0.0)
+    uy_r = np.where(w, ref.HUy / np.where(w, ref.H, 1.0), 0.0)
+    ux_f = np.where(w, f["HUx"] / np.where(w, f["H"], 1.0), 0.0)
+    uy_f = np.where(w, f["HUy"] / np.where(w, f["H"], 1.0), 0.0)
+    # velocity errors relative to the flow's own scale, or to the shallow-
+    # water wave speed sqrt(g max H) where the flow is at rest (lake at rest:
+    # the reference's velocities are round-off noise around 0)
+    c = np.sqrt(sc.params.g * ref.H.max())
+    for name, a, b in (("H", f["H"], ref.H), ("Ux", ux_f, ux_r), ("Uy", uy_f, uy_r)):
+        scale = np.abs(b).max() if name == "H" else max(np.abs(b).max(), c)
+        err = np.abs(a - b).max() / scale
+        assert err <= RTOL, f"{case} {name}: normwise relative error {err:.3e}"
