@@ -394,7 +394,8 @@ void swf_destroy(swf_ctx* c) {
                   c->fpx, c->fpy, c->d_src, c->d_ht, c->d_hq, c->d_sig, c->d_wt, c->d_wv,
                   c->d_interior, c->d_halo, c->d_bflag, c->d_tile_act, c->d_tile_same,
                   c->d_tile_srcm, c->d_redo_f, c->d_redo_s, c->d_list_f, c->d_list_s,
-                  c->d_part, c->d_sc, c->d_redo_l, c->d_half[0], c->d_half[1], c->d_half[2]};
+                  c->d_part, c->d_sc, c->d_redo_l, c->d_half[0], c->d_half[1], c->d_half[2],
+                  c->d_xdef, c->d_xsrc, c->d_xbpart, c->d_xface};
   for (void* p : ptrs) cudaFree(p);
   if (c->h_sc) cudaFreeHost(c->h_sc);
   for (auto& e : c->ev)
@@ -597,6 +598,7 @@ int swf_step(swf_ctx* c, double dt_cap, swf_step_info* info) {
     return rc;
   }
   if (!info) return SWF_OK;  // errors surface at the next synchronising call
+  if ((rc = fused_exact_volumes(c))) return rc;
   cudaError_t e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) return cuda_check(c, e, "step");
   rc = commit_batch(c, cur0, 1, nullptr);
@@ -814,6 +816,7 @@ int swf_run(swf_ctx* c, int n, double dt_cap, int* done, swf_step_info* last) {
     if ((rc = fused_enqueue_step(c, dt_cap))) return rc;
     ++enq;
   }
+  if (last && (rc = fused_exact_volumes(c))) return rc;  // the last step's volumes
   cudaError_t e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) return cuda_check(c, e, "run");
   rc = commit_batch(c, cur0, enq, done);

@@ -55,6 +55,12 @@ constexpr int STHR = SWF_STEP_THREADS;  // k_step (a multiple of 32)
 static_assert(STHR % 32 == 0, "k_step threads must be whole warps");
 constexpr int RED_CTAS = 148;
 constexpr int NPART_ALLOC = 5;  // doubles per tile in d_part (see k_reduce)
+#ifndef SWF_XDIAG_SRC  // developer A/B switches of the exact-volume term stores
+#define SWF_XDIAG_SRC 1
+#endif
+#ifndef SWF_XDIAG_DEF
+#define SWF_XDIAG_DEF 1
+#endif
 #ifndef SWF_STEP_MINB
 #define SWF_STEP_MINB 3  // CTAs per SM the register budget of k_step targets
 #endif
@@ -685,7 +691,12 @@ struct StepArgs {
   double* hu;
   double* hv;
   int* redo_l;  // k_lag tiles to redo exactly
+  // exact-diagnostics terms (full grids; null on strips), see swf_ctx
+  double* xdef;   // clamp deficit of every flux-on cell of the step
+  double* xsrc;   // Ht - Hn of every active cell of the step
+  double* xface;  // mass flux of every edge face the step computed
 };
+
 
 __device__ __forceinline__ unsigned long long fused_flux_key(const Geo& G,
                                                             const unsigned char* bflag, int dir,
@@ -804,8 +815,10 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
   __shared__ double s_red[3][STHR / 32];
   __shared__ unsigned char s_bf[MAXBF];
   __shared__ unsigned short s_bcol[BX], s_brow[BY];  // B-block column / row of each tile column / row
+  __shared__ int s_dflag;  // a clamp deficit in this tile (exact-volume terms to store)
   const PhysConst& P = G.P;  // reciprocals refined at context creation (fused_prepare)
   StepScalars* sc = A.sc;
+  if (threadIdx.x == 0) s_dflag = 0;
   if (__syncthreads_or(stopped(sc))) return;
   bool sok = true;  // every speculative division of this thread accepted
   unsigned long long my_err = ERR_NONE;  // published once the tile is known exact
@@ -872,6 +885,7 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
   static_assert(2 * RREG <= 3 * NSL, "phase-1 scratch overlaps OWN");
   static_assert(3 * NSL + 3 * BX * BY + RREG + BX * BY <= SCRATCH,
                 "phase-1 scratch overflow");
+
   for (int c = tid; c < RREG; c += STHR) {
     int i = i0 - 2 + c % RX, r = r0 - 2 + c / RX;
     double h = 0.0, mx = 0.0, my = 0.0, bb = 0.0, fx = 0.0, fy = 0.0, n = G.n_manning;
@@ -995,6 +1009,9 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
     correct_cell(Hn, qxn, qyn, nsrc > 0, sgm, d, fmx, fmy, n, tau, P.eps, P.g, ht, qx, qy, sv,
                  SP, Hk, &lam);
     srcvol += sv;
+    // Ht - Hn (stepper.cpp:353-355) for the exact volumes; nonzero only in
+    // tiles near a source spec, and every active cell of those is stored
+    if (SWF_XDIAG_SRC && srcm && A.xsrc) A.xsrc[(size_t)i + (size_t)r * nx] = sv;
     // CFL abort (stepper.cpp:378-380, 391-399): dr = tau * u12
     double dx = tau * R[F_U * RREG + s], dy = tau * R[F_V * RREG + s];
     double half_h = 0.5 * P.h;
@@ -1052,6 +1069,7 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
         rec = boundary_face(wet, H, R[F_U * RREG + se], R[F_V * RREG + se], lo,
                             lo ? G.west_refl : G.east_refl, P.g);
         outflow += lo ? -rec.fm : rec.fm;
+        if (A.xface) A.xface[(lo ? 0 : G.ny) + jg] = rec.fm;  // W/E edge faces, by row
       } else {
         int la = fx + y * (BX + 2), lb = la + 1;  // slope slots of cells f-1, f
         double dA = R[F_D * RREG + sa], dB = R[F_D * RREG + sa + 1];
@@ -1153,6 +1171,7 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
         rec = boundary_face(wet, H, R[F_V * RREG + se], R[F_U * RREG + se], lo,
                             lo ? G.south_refl : G.north_refl, P.g);
         outflow += lo ? -rec.fm : rec.fm;
+        if (A.xface) A.xface[2 * G.ny + (lo ? 0 : G.nx) + i] = rec.fm;  // S/N edge faces
       } else {
         int la = x + fy * BX, lb = la + BX;  // slope slots of rows rf-1, rf
         double dA = R[F_D * RREG + sa], dB = R[F_D * RREG + sa + RX];
@@ -1203,9 +1222,11 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
   PHASE_MARK(6);
   // ---- phase 5: accumulate (stepper.cpp:540-566) + final (628-659) ---------
   double deficit = 0.0;
+  double dfm[PER];  // the clamp deficit of each of the thread's cells (0 if not flux-on)
   const double dt_h = tau / P.h;
 #pragma unroll
   for (int m = 0; m < PER; ++m) {
+    dfm[m] = 0.0;
     int c = tid + m * STHR;
     if (BX * BY % STHR && c >= BX * BY) break;
     int x = c % BX, y = c / BX;
@@ -1249,6 +1270,7 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
     double H1, qx, qy, dfc;
     final_cell(Ht[m], Qx[m], Qy[m], Fh, Fvx, Fvy, dt_h, P.eps, H1, qx, qy, dfc);
     deficit += dfc;
+    dfm[m] = dfc;
     A.Ho[k] = H1;
     A.HUxo[k] = qx;
     A.HUyo[k] = qy;
@@ -1266,6 +1288,7 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
 
   PHASE_MARK(7);
   // ---- per-tile diagnostic partials (deterministic) ------------------------
+  if (deficit != 0.0) s_dflag = 1;  // read after the barriers below
   double v3[3] = {deficit, srcvol, outflow};
 #pragma unroll
   for (int q = 0; q < 3; ++q) {
@@ -1286,8 +1309,19 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
   const bool redo = SPEC && any_bad;
   if (redo) {
     if (tid == 0) A.redo[atomicAdd(&sc->redo_n[1], 1)] = tile;
-  } else if (my_err != ERR_NONE) {
-    atomicMin(&sc->err_key, my_err);
+  } else {
+    if (my_err != ERR_NONE) atomicMin(&sc->err_key, my_err);
+    // exact volumes: a tile with a clamp deficit stores every cell's term
+    // (the reduction reads the cells of tiles with a nonzero deficit partial)
+    if (SWF_XDIAG_DEF && s_dflag && A.xdef) {
+#pragma unroll
+      for (int m = 0; m < PER; ++m) {
+        const int c = tid + m * STHR;
+        if (BX * BY % STHR && c >= BX * BY) break;
+        const int i = i0 + c % BX, r = r0 + c / BX;
+        if (i < G.nx && r < G.r1) A.xdef[(size_t)i + (size_t)r * nx] = dfm[m];
+      }
+    }
   }
 }
 
@@ -2027,6 +2061,200 @@ __global__ void __launch_bounds__(XTHR, SWF_FLUX_MINB) k_flux_redo(Geo G, StepAr
   }
 }
 
+// ---------------------------------------------------------------------------
+// Exact StepInfo volumes (final_update, stepper.cpp:676-701): the reference
+// sums the clamp deficit and the source volume per block in row-major cell
+// order, then over the flux / Lagrangian blocks in block order, and the
+// outflow over the edge faces in a fixed order -- serial floating-point
+// sums.  k_step stores the terms that can be nonzero (every cell's deficit
+// in the rare tiles with a clamp, Ht - Hn of the active cells of tiles near a
+// source spec, the mass flux of each edge face it computes); the tile
+// partials, the source masks and the block flags of the step say which
+// blocks and cells the reference sums.  These two kernels redo the reference's sums in its order
+// on request (a synchronised step or the last step of a run).
+// ---------------------------------------------------------------------------
+constexpr int XCHUNK = 1024;  // blocks per k_xblock CTA (one nonzero count each)
+
+// Per-block partials of the step's deficit and source-volume terms, in the
+// reference's row-major cell order; blocks that cannot hold a nonzero term
+// are skipped (no clamp deficit in any tile they touch -- the tile partials
+// are sums of non-negative terms -- and no source spec near them).
+__global__ void __launch_bounds__(XCHUNK) k_xblock(Geo G, StepArgs A, const double* Hn,
+                                                   double* bpart, int* chunk_nz) {
+  const StepScalars* sc = A.sc;
+  if (stopped(sc)) return;
+  const PhysConst& P = G.P;
+  const int nbl = G.nbx * (G.bj1 - G.bj0);
+  const int lb = blockIdx.x * XCHUNK + threadIdx.x;
+  double part[2] = {0.0, 0.0};
+  if (lb < nbl) {
+    const int bi = lb % G.nbx, bj = G.bj0 + lb / G.nbx;
+    const int i0 = bi * G.bs, i1 = min(i0 + G.bs, G.nx);
+    const int j0 = bj * G.bs, j1 = min(j0 + G.bs, G.ny);
+    const unsigned char f = A.bflag[lb];
+    // the fused tiles the block touches (owned rows of this context)
+    const int tx0 = i0 / BX, tx1 = (i1 - 1) / BX;
+    const int ty0 = (j0 - G.jg0 - G.r0) / BY, ty1 = (j1 - 1 - G.jg0 - G.r0) / BY;
+    bool maydef = false, maysrc = false;
+    for (int ty = ty0; ty <= ty1; ++ty)
+      for (int tx = tx0; tx <= tx1; ++tx) {
+        const int t = tx + ty * G.tiles_x;
+        maydef |= A.part[5 * (size_t)t] != 0.0;
+        maysrc |= A.tile_srcm[t] != 0u;
+      }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      // deficit over the flux blocks, source volume over the Lagrangian ones
+      // (stepper.cpp:678-683); every term of such a block was stored this step
+      const double* val = q == 0 ? A.xdef : A.xsrc;
+      const bool blk = q == 0 ? (!G.skip || (f & 2)) : (!G.skip || (f & 1));
+      if (!val || !blk || !(q == 0 ? maydef : maysrc)) continue;
+      double acc = 0.0;
+      for (int j = j0; j < j1; ++j) {  // row-major, stepper.cpp:633-634 / 345-346
+        const size_t row = (size_t)(j - G.jg0) * G.nx;
+        const int trow = (j - G.jg0 - G.r0) / BY * G.tiles_x;
+        for (int i = i0; i < i1; ++i) {
+          // only the tiles that stored their terms this step hold any: a
+          // nonzero deficit partial, or a source spec nearby
+          const int t = trow + i / BX;
+          if (q == 0 ? A.part[5 * (size_t)t] == 0.0 : A.tile_srcm[t] == 0u) continue;
+          // the source sum runs over the active cells (cell_active,
+          // stepper.hpp:131-133): H_n > eps or a source marker at t_n
+          if (q == 1 && !(Hn[row + i] > P.eps ||
+                          cell_sigma_only(A.src, A.sig, G.nsrc, i, j) != 0.0))
+            continue;
+          acc += val[row + i];
+        }
+      }
+      part[q] = acc;
+    }
+    bpart[2 * (size_t)lb] = part[0];
+    bpart[2 * (size_t)lb + 1] = part[1];
+  }
+  const int nz = __syncthreads_count(part[0] != 0.0 || part[1] != 0.0);
+  if (threadIdx.x == 0) chunk_nz[blockIdx.x] = nz;
+}
+
+// CTA-wide ordered compaction: thread t contributes terms a (and b) in the
+// order (t, a), (t, b); the nonzero ones land in out[] in that order.
+// Returns the count (all threads).
+__device__ __forceinline__ int cta_compact2(double a, double b, double* out, int* s_warp) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int c = (a != 0.0) + (b != 0.0);
+  int incl = c;  // inclusive warp scan
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {  // scan of the warp totals
+    int v = lane < XCHUNK / 32 ? s_warp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
+    }
+    if (lane < XCHUNK / 32) s_warp[32 + lane] = v;  // inclusive totals
+  }
+  __syncthreads();
+  int pos = (warp > 0 ? s_warp[32 + warp - 1] : 0) + incl - c;
+  if (a != 0.0) out[pos++] = a;
+  if (b != 0.0) out[pos] = b;
+  const int total = s_warp[32 + XCHUNK / 32 - 1];
+  __syncthreads();
+  return total;
+}
+
+// Thread 0's serial sum of n terms in order, loads batched ahead of the
+// dependent additions.
+__device__ __forceinline__ double serial_add(double acc, const double* v, int n) {
+  int q = 0;
+  for (; q + 8 <= n; q += 8) {
+    double t[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) t[u] = v[q + u];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += t[u];
+  }
+  for (; q < n; ++q) acc += v[q];
+  return acc;
+}
+
+// One CTA: the block-order sums over the nonzero partials and the edge faces
+// in the reference's order (stepper.cpp:684-700), then the StepInfo volumes.
+// Loads, zero tests and the ordered compaction are parallel; thread 0 adds
+// the nonzero terms in order.
+__global__ void __launch_bounds__(XCHUNK) k_xserial(Geo G, StepArgs A, const double* bpart,
+                                                    const int* chunk_nz, double area, double h) {
+  StepScalars* sc = A.sc;
+  if (stopped(sc)) return;
+  __shared__ double s_c[2][XCHUNK];   // compacted terms (deficit | source, or the faces)
+  __shared__ double s_f[2 * XCHUNK];
+  __shared__ int s_warp[64];
+  __shared__ int s_list[XCHUNK];
+  __shared__ int s_n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nbl = G.nbx * (G.bj1 - G.bj0);
+  const int nch = (nbl + XCHUNK - 1) / XCHUNK;
+  double sum0 = 0.0, sum1 = 0.0, out = 0.0;  // thread 0's running sums
+  for (int cb = 0; cb < nch; cb += XCHUNK) {
+    // the nonzero chunks of this range, in order
+    if (tid == 0) s_n = 0;
+    __syncthreads();
+    const bool nz = cb + tid < nch && chunk_nz[cb + tid] != 0;
+    const unsigned bm = __ballot_sync(0xffffffffu, nz);
+    if (lane == 0) s_warp[warp] = (int)bm;
+    __syncthreads();
+    if (tid == 0) {
+      int n = 0;
+      for (int w = 0; w < XCHUNK / 32; ++w)
+        for (unsigned m = (unsigned)s_warp[w]; m; m &= m - 1) s_list[n++] = cb + 32 * w + __ffs(m) - 1;
+      s_n = n;
+    }
+    __syncthreads();
+    const int nlist = s_n;
+    for (int li = 0; li < nlist; ++li) {
+      const int lb = s_list[li] * XCHUNK + tid;
+      const double v0 = lb < nbl ? bpart[2 * (size_t)lb] : 0.0;
+      const double v1 = lb < nbl ? bpart[2 * (size_t)lb + 1] : 0.0;
+      const int n0 = cta_compact2(v0, 0.0, s_c[0], s_warp);
+      const int n1 = cta_compact2(v1, 0.0, s_c[1], s_warp);
+      if (tid == 0) {
+        sum0 = serial_add(sum0, s_c[0], n0);
+        sum1 = serial_add(sum1, s_c[1], n1);
+      }
+      __syncthreads();
+    }
+  }
+  // out -= W[j]; out += E[j] for every row, then out -= S[i]; out += N[i]
+  // (live faces only: the edge cell's block is flux-active, stepper.cpp:684-688)
+  auto live = [&](int ci, int cj) {
+    return !G.skip || (A.bflag[ci / G.bs + (cj / G.bs - G.bj0) * G.nbx] & 2);
+  };
+  for (int pass = 0; pass < 2; ++pass) {
+    const int n = pass == 0 ? G.ny : G.nx;
+    const int lo = pass == 0 ? 0 : 2 * G.ny, hi = pass == 0 ? G.ny : 2 * G.ny + G.nx;
+    for (int base = 0; base < n; base += XCHUNK) {
+      const int q = base + tid;
+      double w = 0.0, e = 0.0;
+      if (q < n) {
+        if (pass == 0 ? live(0, q) : live(q, 0)) w = A.xface[lo + q];
+        if (pass == 0 ? live(G.nx - 1, q) : live(q, G.ny - 1)) e = A.xface[hi + q];
+      }
+      const int nf = cta_compact2(-w, e, s_f, s_warp);  // out -= w is out + (-w), exactly
+      if (tid == 0) out = serial_add(out, s_f, nf);
+      __syncthreads();
+    }
+  }
+  if (tid == 0) {
+    sc->deficit = sum0 * area;           // stepper.cpp:680
+    sc->srcvol = sum1 * area;            // stepper.cpp:683
+    sc->outflow = (out * sc->tau) * h;   // stepper.cpp:701
+  }
+}
+
 // k_reduce: RED_CTAS fixed-order partial sums of the per-tile partials
 // (deficit, source volume, outflow, Lagrangian blocks, flux blocks; coalesced,
 // deterministic); k_finish adds them in CTA order and commits t.
@@ -2115,6 +2343,9 @@ StepArgs step_args(swf_ctx* c) {
   A.hu = c->d_half[1];
   A.hv = c->d_half[2];
   A.redo_l = c->d_redo_l;
+  A.xdef = c->d_xdef;
+  A.xsrc = c->geo.nsrc > 0 ? c->d_xsrc : nullptr;
+  A.xface = c->d_xface;
   return A;
 }
 
@@ -2429,6 +2660,22 @@ extern "C" int swf_debug_phase_cycles(unsigned long long* out16, int reset) {
 #endif
 int fused_reduce_ctas() { return RED_CTAS; }
 
+// The exact StepInfo volumes of the last enqueued step (full grids; the
+// strips keep the deterministic tile-order sums of k_finish).
+int fused_exact_volumes(swf_ctx* c) {
+  if (!c->d_xdef || SWF_SPLIT) return SWF_OK;
+  const Geo& G = c->geo;
+  StepArgs A = step_args(c);
+  const int nbl = G.nbx * (G.bj1 - G.bj0);
+  // the step just enqueued flipped cur: its step-start depth is the other buffer
+  const int nch = (nbl + XCHUNK - 1) / XCHUNK;
+  int* chunk_nz = (int*)(c->d_xbpart + 2 * (size_t)nbl);  // after the partials
+  if (nbl > 0)
+    k_xblock<<<nch, XCHUNK, 0, c->stream>>>(G, A, c->H[1 - c->cur], c->d_xbpart, chunk_nz);
+  k_xserial<<<1, XCHUNK, 0, c->stream>>>(G, A, c->d_xbpart, chunk_nz, c->h * c->h, c->h);
+  return cuda_check(c, cudaGetLastError(), "exact volumes");
+}
+
 // Per-tile source masks (bit s: spec s meets the tile's cells +- 2), the
 // host-side equivalent of src_mask_for, refreshed whenever the specs change.
 int fused_tile_srcm(swf_ctx* c) {
@@ -2524,6 +2771,21 @@ int fused_prepare(swf_ctx* c) {
     if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   }
   if (e == cudaSuccess && SWF_SPLIT && !c->d_redo_l) e = cudaMalloc(&c->d_redo_l, nredo * sizeof(int));
+  // exact-diagnostics captures: full grids only (a strip's sums continue
+  // its neighbours' running totals, which stay with the tile-order sums)
+  const bool full = c->geo.r0 == 0 && c->geo.r1 == c->geo.rows;
+  if (e == cudaSuccess && full && !SWF_SPLIT && !c->d_xdef) {
+    const size_t n = local_cells(c) ? local_cells(c) : 1;
+    const size_t nbl = (size_t)c->geo.nbx * (c->geo.bj1 - c->geo.bj0) + 1;
+    const size_t nf = 2 * ((size_t)c->geo.nx + c->geo.ny);
+    void** bufs[] = {(void**)&c->d_xdef, (void**)&c->d_xsrc, (void**)&c->d_xbpart,
+                     (void**)&c->d_xface};
+    const size_t sz[] = {n * 8, n * 8, 2 * nbl * 8 + (nbl / XCHUNK + 2) * 4, nf * 8};
+    for (int q = 0; q < 4 && e == cudaSuccess; ++q) {
+      e = cudaMalloc(bufs[q], sz[q]);
+      if (e == cudaSuccess) e = cudaMemset(*bufs[q], 0, sz[q]);
+    }
+  }
   for (int q = 0; q < 3 && e == cudaSuccess && SWF_SPLIT; ++q) {
     if (c->d_half[q]) continue;
     const size_t bytes = (local_cells(c) ? local_cells(c) : 1) * sizeof(double);

@@ -144,6 +144,12 @@ struct swf_ctx {
   // split step (SWF_SPLIT): the half-step view (depth, u, v) k_lag leaves for
   // k_flux, local cells each
   double* d_half[3] = {nullptr, nullptr, nullptr};
+  // exact StepInfo volumes (full grids): k_step stores the terms of the
+  // reference's volume sums; fused_exact_volumes adds them in its order
+  double* d_xdef = nullptr;    // clamp deficit per cell (flux-on cells of the step)
+  double* d_xsrc = nullptr;    // Ht - Hn per cell (active cells of the step)
+  double* d_xbpart = nullptr;  // 2 per owned block: deficit, source partials
+  double* d_xface = nullptr;   // [W ny | E ny | S nx | N nx] boundary fm
   int sm_count = 148;
   swf::FaceTaps taps;  // owned by the nests that registered them
   // P2P halo: the neighbours' state buffers mapped here ([side][field][parity])
@@ -209,6 +215,7 @@ int fused_enqueue_phase1(swf_ctx* c, double dt_cap, int part);
 int fused_local_speed(swf_ctx* c, double* dev_out);
 int fused_ingest_hu(swf_ctx* c, const double* hHUx, const double* hHUy);
 int fused_tile_srcm(swf_ctx* c);
+int fused_exact_volumes(swf_ctx* c);  // enqueue the exact reduction of the last step
 
 int launch_begin(swf_ctx* c, double dt_cap);  // sources/wind at t_n, reset counters
 int launch_mask(swf_ctx* c);                   // K1 block mask + tile flags

@@ -20,7 +20,8 @@ def cases():
         "c1_dry_n002": lambda: S.dam_break_1d(False, 0.02),
         "c1_wet_n0": lambda: S.dam_break_1d(True, 0.0),
         "c2_256": lambda: S.circular_dam_break(256, 8.0, 32, n_manning=0.03),
-        "c3_crop": lambda: S.floodplain(16384, 50.0, window=(4096, 0, 256, 256)),
+        "c3_crop": lambda: S.floodplain(16384, 50.0, window=(6144, 14336, 256, 256)),  # 30 % wet
+        "c3_rain": lambda: S.floodplain(16384, 50.0, window=(1980, 10180, 256, 256)),  # rain edge
         "lake128": lambda: S.lake_at_rest(128),
     }
 

@@ -23,7 +23,7 @@ from conftest import ROOT
 RTOL = 1e-12
 FAST = os.path.join(ROOT, "paper_1705_00614_b200", "libswflood_cuda_fast.so")
 CASES = [("c1_dry_n002", 200), ("c1_wet_n0", 200), ("c2_256", 100), ("c3_crop", 40),
-         ("lake128", 100)]
+         ("c3_rain", 40), ("lake128", 100)]
 
 
 def test_fast_build_exists_and_exports_the_abi():

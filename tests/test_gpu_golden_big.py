@@ -50,6 +50,8 @@ def test_config_size_trajectory(name, mode):
     assert (info.lagrangian_blocks, info.flux_blocks, info.total_blocks) == \
         (li["lagrangian_blocks"], li["flux_blocks"], li["total_blocks"])
     assert info.active_fraction.hex() == li["active_fraction"]
+    for k in ("clamp_deficit_volume", "source_volume", "boundary_outflow_volume"):
+        assert getattr(info, k).hex() == li[k], k  # the reference's summation order
     assert int((st.H > sc.params.eps_dry).sum()) == case["wet_cells_end"]
     s.close()
 

@@ -154,14 +154,11 @@ def test_golden_case(gpu_cls, name, mode):
     assert info.flux_blocks == li["flux_blocks"]
     assert info.total_blocks == li["total_blocks"]
     assert info.active_fraction.hex() == li["active_fraction"]
-    if mode == 1:  # the stage path sums diagnostics in the reference's block order
-        assert info.clamp_deficit_volume.hex() == li["clamp_deficit_volume"]
-        assert info.source_volume.hex() == li["source_volume"]
-        assert info.boundary_outflow_volume.hex() == li["boundary_outflow_volume"]
-    else:  # the fused path uses a deterministic tile-order reduction
-        for k in ("clamp_deficit_volume", "source_volume", "boundary_outflow_volume"):
-            ref = float.fromhex(li[k])
-            assert getattr(info, k) == pytest.approx(ref, rel=1e-12, abs=1e-9)
+    # both paths sum the diagnostics in the reference's order (the stage path
+    # per block; the fused path from the terms k_step stores, fused_exact_volumes)
+    assert info.clamp_deficit_volume.hex() == li["clamp_deficit_volume"]
+    assert info.source_volume.hex() == li["source_volume"]
+    assert info.boundary_outflow_volume.hex() == li["boundary_outflow_volume"]
 
 
 def test_flood64_arrays_and_host_step(gpu_cls):
@@ -451,6 +448,43 @@ def test_pinned_host_steps_follow_host_side_edits(gpu_cls, oracle_built):
         assert ia.tau == ib.tau, k
         assert (ia.lagrangian_blocks, ia.flux_blocks) == (ib.lagrangian_blocks, ib.flux_blocks), k
     assert_state_bitwise(hs, cpu_state, "pinned steps with host-side edits")
+
+
+@pytest.mark.parametrize("case,bs,skip", [("flood256", 16, True), ("flood256", 7, True),
+                                          ("flood256", 16, False), ("c2", 16, True),
+                                          ("c1_dry", 32, True)])
+def test_step_info_volumes_bitwise_every_step(gpu_cls, oracle_built, case, bs, skip):
+    """StepInfo's clamp deficit, source volume and boundary outflow of the
+    fused path, every step, bit for bit the reference's serial sums
+    (final_update, stepper.cpp:676-701), for block sizes that do and do not
+    align with the 32 x 16 tiles and with skipping on and off."""
+    from paper_1705_00614_b200.types import CellRect, SourceKind, SourceSpec, Vec2
+    if case == "flood256":  # + a drain strong enough to empty its cells (clamped Ht)
+        sc = S.floodplain(256, 50.0)
+        sc.sources.append(SourceSpec(SourceKind.Discharge, "drain2", CellRect(40, 127, 46, 133),
+                                     [HS(0.0, -5e4)], 0.0, Vec2(0.0, 0.0)))
+    elif case == "c2":
+        sc = S.circular_dam_break(256, 8.0, 40, n_manning=0.03)
+    else:
+        sc = S.dam_break_1d(False, 0.02)
+    sc.options.block_size = bs
+    sc.options.skip_dry_blocks = skip
+    g = make(gpu_cls, sc)
+    o = make(oracle_built.OracleStepper, sc)
+    st = sc.state.copy()
+    g.upload(st)
+    ref = sc.state.copy()
+    nonzero = [0, 0, 0]
+    for k in range(60):
+        a = g.step_resident()
+        b = o.step(ref)
+        for q, name in enumerate(("clamp_deficit_volume", "source_volume",
+                                  "boundary_outflow_volume")):
+            va, vb = getattr(a, name), getattr(b, name)
+            assert va.hex() == vb.hex(), (k, name, va, vb)
+            nonzero[q] += vb != 0.0
+    if case == "flood256":  # (the final-update clamp itself practically never fires)
+        assert nonzero[1] > 0 and nonzero[2] > 0, nonzero
 
 
 def test_host_mirror_steps_match_oracle(gpu_cls, oracle_built):
