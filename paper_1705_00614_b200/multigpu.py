@@ -91,6 +91,40 @@ def row_weights(config: str, n: int, bs: int, device: str = "cuda", dry_cost: fl
     return out
 
 
+def strip_loads(weights, bounds, bs: int) -> List[float]:
+    """Total weight per strip (weights: one value per block row)."""
+    w = np.asarray(weights, dtype=np.float64)
+    return [float(w[j0 // bs:(j1 + bs - 1) // bs].sum()) for j0, j1 in bounds]
+
+
+def rebalance_bounds(weights, bounds, bs: int, ny: int, threshold: float = 0.03):
+    """Dynamic strip rebalancing (the flood front migrates, so
+    strips balanced at t = 0 drift out of balance): new block-row cuts from
+    the current activity, or None when they would not lower the busiest
+    strip's load by more than `threshold` (relative).  Deterministic: every
+    rank derives the same answer from the same allgathered weights."""
+    new = balanced_bounds(weights, len(bounds), bs, ny)
+    if [tuple(b) for b in new] == [tuple(b) for b in bounds]:
+        return None
+    old_max, new_max = max(strip_loads(weights, bounds, bs)), max(strip_loads(weights, new, bs))
+    return new if new_max < old_max * (1.0 - threshold) else None
+
+
+def transfer_plan(old, new, ny: int, halo: int = HALO):
+    """The row moves of a re-partition: (src, dst, a, b) -- rank src sends its
+    owned global rows [a, b) to rank dst, which needs them in its new window
+    (owned rows plus ghost rows).  Every row of every new window comes from
+    exactly one owner (the old strips tile the grid)."""
+    out = []
+    for dst, (j0, j1) in enumerate(new):
+        w0, w1 = window_rows(j0, j1, ny, halo)
+        for src, (o0, o1) in enumerate(old):
+            a, b = max(w0, o0), min(w1, o1)
+            if a < b:
+                out.append((src, dst, a, b))
+    return out
+
+
 def window_rows(j0: int, j1: int, ny: int, halo: int = HALO) -> Tuple[int, int]:
     """Global rows of a strip's local window (owned + ghost rows)."""
     return max(j0 - halo, 0), min(j1 + halo, ny)
@@ -209,6 +243,17 @@ class Strip:
 
     def stream_handle(self) -> int:
         return self._lib.swf_stream(self.ctx) or 0
+
+    def mask(self):
+        """(interior, halo) block counts of the owned block rows (last step),
+        shaped (block rows, nbx)."""
+        nb = (self.nx + 15) // 16 * ((self.j1 - self.j0 + 15) // 16 + 1)
+        inn, hal = np.zeros(nb, np.int32), np.zeros(nb, np.int32)
+        a, b = C.c_int(), C.c_int()
+        self._rc(self._lib.swf_download_mask(self.ctx, inn.ctypes.data_as(A.PI),
+                                             hal.ctypes.data_as(A.PI), C.byref(a), C.byref(b)))
+        n = a.value * b.value
+        return inn[:n].reshape(b.value, a.value), hal[:n].reshape(b.value, a.value)
 
     # P2P halo (include/swf.h "P2P halo")
     def device_buffers(self):
@@ -405,7 +450,15 @@ class RankStrip:
         self.local = local % ndev
         torch.cuda.set_device(self.local)
         self.dev = torch.device("cuda", self.local)
-        self.backend = os.environ.get("SWF_DIST_BACKEND", "nccl")
+        # NCCL needs one rank per GPU; more ranks than visible GPUs (e.g.
+        # `bench.py --gpus 2` on a one-GPU box) share devices through gloo
+        # with host-staged halos -- the same strip code, said on stderr
+        self.backend = os.environ.get("SWF_DIST_BACKEND") or (
+            "nccl" if self.world <= ndev else "gloo")
+        if self.backend == "gloo" and "SWF_DIST_BACKEND" not in os.environ and self.rank == 0:
+            import sys
+            print(f"multigpu: {self.world} ranks on {ndev} visible GPU(s): gloo with host-staged "
+                  "halos (NCCL needs one rank per GPU)", file=sys.stderr, flush=True)
         # rank 0 prints exactly one JSON line on stdout: NCCL's log goes to
         # stderr, at INFO for the communicator set-up (rank count, transports,
         # NVLS) unless the caller chose a level
@@ -432,6 +485,15 @@ class RankStrip:
             self.bounds = balanced_bounds(wts, self.world, 16, self.n)
         else:
             self.bounds = strip_bounds(self.ny, self.world, 16)
+        self.config, self.n_full, self.no_skip = config, n_full, no_skip
+        self._make_strip()
+        self.strip.upload(self.sc.state.H, self.sc.state.HUx, self.sc.state.HUy, 0.0)
+
+    def _make_strip(self):
+        """The strip context of self.bounds[rank] with its window of the
+        scenario (terrain, Manning field, sources, wind)."""
+        from . import scenarios as S
+        config, n_full, no_skip = self.config, self.n_full, self.no_skip
         self.j0, self.j1 = self.bounds[self.rank]
         self.w0, self.w1 = window_rows(self.j0, self.j1, self.ny)
         if self.weak:
@@ -448,7 +510,87 @@ class RankStrip:
         self.sc = sc
         srcs = S.clip_sources(sc.global_sources, self.n, self.ny) if self.weak else sc.global_sources
         self.strip = Strip(sc, self.ny, self.j0, self.j1, srcs, sc.wind, device=self.local)
-        self.strip.upload(sc.state.H, sc.state.HUx, sc.state.HUy, 0.0)
+
+    # ---- dynamic rebalancing ----------------------------------
+    def block_row_weights(self, dry_cost: float = 0.1) -> np.ndarray:
+        """This rank's owned block rows' cost in the last step: the cells of
+        flux-active blocks (k_step runs them) plus dry_cost per other cell."""
+        inn, hal = self.strip.mask()
+        act = ((inn > 0) | (hal > 0)).sum(axis=1).astype(np.float64)
+        nbx = inn.shape[1]
+        return (act + dry_cost * (nbx - act)) * 256.0
+
+    def rebalance(self, threshold: float = 0.03) -> bool:
+        """Re-cut the strips from the current activity when that lowers the
+        busiest strip's load by more than `threshold`; outside a batch.
+        Returns whether the strips moved (every rank returns the same)."""
+        import torch.distributed as dist
+        if self.weak or self.world == 1:
+            return False
+        parts = [None] * self.world
+        dist.all_gather_object(parts, self.block_row_weights())
+        w = np.concatenate(parts)
+        new = rebalance_bounds(w, self.bounds, 16, self.ny, threshold)
+        if new is None:
+            return False
+        self.migrate(new)
+        return True
+
+    def migrate(self, new_bounds):
+        """Move to new strip bounds: the rows each rank's new window needs
+        travel from their current owners (transfer_plan, NCCL or gloo), the
+        strip context is rebuilt for the new window and the state uploaded;
+        the P2P halo, if on, is mapped again.  Same results as before the
+        move, bit for bit (the state is copied, not recomputed)."""
+        import torch
+        import torch.distributed as dist
+        new_bounds = [tuple(b) for b in new_bounds]
+        old_bounds = [tuple(b) for b in self.bounds]
+        nx = self.n
+        H, X, Y = (np.empty((self.w1 - self.w0) * nx) for _ in range(3))
+        t = self.strip.download(H, X, Y)
+        own = np.stack([a.reshape(self.w1 - self.w0, nx)[self.j0 - self.w0:self.j1 - self.w0]
+                        for a in (H, X, Y)])  # (3, owned rows, nx)
+        nw0, nw1 = window_rows(*new_bounds[self.rank], self.ny)
+        win = np.empty((3, nw1 - nw0, nx))
+        ops, recvs = [], []
+        for src, dst, a, b in transfer_plan(old_bounds, new_bounds, self.ny):
+            if src == self.rank and dst == self.rank:
+                win[:, a - nw0:b - nw0] = own[:, a - self.j0:b - self.j0]
+            elif src == self.rank:
+                buf = torch.from_numpy(np.ascontiguousarray(own[:, a - self.j0:b - self.j0]))
+                buf = buf.to(self.xdev)
+                ops.append(dist.P2POp(dist.isend, buf, dst))
+                recvs.append(buf)  # keep alive until the exchange completes
+            elif dst == self.rank:
+                buf = torch.empty((3, b - a, nx), dtype=torch.float64, device=self.xdev)
+                ops.append(dist.P2POp(dist.irecv, buf, src))
+                recvs.append((buf, a, b))
+        for w in (dist.batch_isend_irecv(ops) if ops else []):
+            w.wait()
+        for r in recvs:
+            if isinstance(r, tuple):
+                buf, a, b = r
+                win[:, a - nw0:b - nw0] = buf.cpu().numpy()
+        # a fresh context for the new window
+        for dp in getattr(self, "_ipc", []):
+            from cuda.bindings import runtime as rt
+            rt.cudaIpcCloseMemHandle(dp)
+        self._ipc = []
+        dist.barrier()  # every rank has unmapped its neighbours' buffers
+        was_p2p = getattr(self, "p2p", False)
+        self.strip.close()
+        self._abufs = None
+        if hasattr(self, "_tok"):
+            del self._tok
+        self.bounds = new_bounds
+        self._make_strip()
+        self.strip.upload(np.ascontiguousarray(win[0]).reshape(-1),
+                          np.ascontiguousarray(win[1]).reshape(-1),
+                          np.ascontiguousarray(win[2]).reshape(-1), t)
+        if was_p2p:
+            self.p2p = False
+            self.setup_p2p()
 
     def _pack(self, side, t):
         import torch
@@ -688,6 +830,14 @@ def bench_strips(args) -> Optional[dict]:
     else:
         for _ in range(args.warmup):
             step()
+    # dynamic rebalancing from the activity after the warm-up,
+    # outside the timed region; the strips keep the new cuts
+    t_rb = time.perf_counter()
+    rebalanced = rs.rebalance() if os.environ.get("SWF_REBALANCE", "1") != "0" else False
+    t_rb = time.perf_counter() - t_rb
+    if rebalanced:
+        strip, sc, bounds, j0, j1 = rs.strip, rs.sc, rs.bounds, rs.j0, rs.j1
+        p2p = getattr(rs, "p2p", False)
     K = args.steps
     strip.set_timing(K)
     stream = torch.cuda.ExternalStream(strip.stream_handle())
@@ -787,6 +937,8 @@ def bench_strips(args) -> Optional[dict]:
                                 "row strips" if rs.weak else
                                 f"{sc.name.split('-')[0]} {full_n}x{full_n} row strips"),
                    "cells": N_total, "strips": bounds, "halo_rows": HALO,
+                   "rebalanced_after_warmup": bool(rebalanced),
+                   "rebalance_s": round(t_rb, 3),
                    "parallelism": f"row strips x{world}, " + (
                        "P2P halo stored by k_step into the neighbours' ghost rows (CUDA IPC over "
                        "NVLink) + a 4-byte NCCL token per neighbour overlapped with interior "

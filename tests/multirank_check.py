@@ -19,7 +19,18 @@ def main():
     p2p = os.environ.get("SWF_HALO") == "p2p"
     if p2p:
         assert rs.setup_p2p(), "P2P halo setup failed"
-    for _ in range(steps):
+    migrate = os.environ.get("SWF_CHECK_MIGRATE") == "1"
+    for k in range(steps):
+        if migrate and k == steps // 3:
+            # dynamic rebalancing: re-cut from the current activity (any change
+            # accepted), then force a move of every interior cut by a block row
+            rs.rebalance(threshold=-1.0)
+            b = [list(x) for x in rs.bounds]
+            for q in range(1, rs.world):
+                d = 16 if q % 2 else -16
+                if b[q - 1][0] + 16 <= b[q][0] + d <= b[q][1] - 16:
+                    b[q - 1][1] = b[q][0] = b[q][0] + d
+            rs.migrate([tuple(x) for x in b])
         if p2p:
             rs.step_p2p()
         else:
@@ -38,7 +49,8 @@ def main():
         (H, X, Y), t = got
         same = all(np.array_equal(a.view(np.int64), b.view(np.int64))
                    for a, b in ((H, st.H), (X, st.HUx), (Y, st.HUy))) and t == st.t
-        print(f"multirank world={rs.world} n={n} steps={steps} p2p={p2p} bitwise_equal={same} t={t}",
+        print(f"multirank world={rs.world} n={n} steps={steps} p2p={p2p} migrate={migrate} "
+              f"bounds={rs.bounds} bitwise_equal={same} t={t}",
               flush=True)
         ok = 1 if same else 0
     flag = [ok]

@@ -21,13 +21,16 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("world,halo", [(2, "copy"), (3, "copy"), (2, "p2p"), (3, "p2p")])
-def test_torchrun_strips_bitwise(world, halo):
+@pytest.mark.parametrize("world,halo,migrate", [(2, "copy", "0"), (3, "copy", "0"), (2, "p2p", "0"),
+                                               (3, "p2p", "0"), (3, "copy", "1"), (2, "p2p", "1")])
+def test_torchrun_strips_bitwise(world, halo, migrate):
     """halo=p2p: k_step stores the boundary rows straight into the
     neighbours' ghost rows through CUDA IPC mappings (here several processes
-    on one device; across GPUs the same stores go over NVLink)."""
+    on one device; across GPUs the same stores go over NVLink).
+    migrate=1: mid-run dynamic rebalancing (RankStrip.rebalance / migrate:
+    rows move between ranks, the strips are rebuilt), still bitwise."""
     env = dict(os.environ, SWF_DIST_BACKEND="gloo", SWF_CHECK_N="512", SWF_CHECK_STEPS="15",
-               SWF_HALO=halo)
+               SWF_HALO=halo, SWF_CHECK_MIGRATE=migrate)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
            os.path.join(ROOT, "tests", "multirank_check.py")]

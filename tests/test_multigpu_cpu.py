@@ -120,3 +120,38 @@ def test_weak_scaling_sources_clipped_to_the_band():
     assert [s.name for s in out] == ["a", "b"]
     assert (out[1].cells.j0, out[1].cells.j1) == (4090, 4095)
     assert S.WEAK_ROWS == 4096
+
+
+def test_transfer_plan_covers_every_new_window_once():
+    for ny, parts in ((256, 2), (512, 3), (1024, 5)):
+        old = M.strip_bounds(ny, parts, 16)
+        rng = np.random.default_rng(parts)
+        w = rng.uniform(0.1, 5.0, ny // 16)
+        new = M.balanced_bounds(w, parts, 16, ny)
+        plan = M.transfer_plan(old, new, ny)
+        for dst, (j0, j1) in enumerate(new):
+            w0, w1 = M.window_rows(j0, j1, ny)
+            got = np.zeros(ny, int)
+            for src, d, a, b in plan:
+                if d == dst:
+                    o0, o1 = old[src]
+                    assert o0 <= a < b <= o1  # a source sends rows it owns
+                    got[a:b] += 1
+            assert (got[w0:w1] == 1).all() and got.sum() == w1 - w0
+
+
+def test_rebalance_bounds_decision():
+    ny, bs = 512, 16
+    w = np.ones(ny // bs)
+    b = M.strip_bounds(ny, 4, bs)
+    assert M.rebalance_bounds(w, b, bs, ny) is None  # already balanced
+    w2 = w.copy()
+    w2[:8] = 20.0  # the flood front moved into the first strip
+    new = M.rebalance_bounds(w2, b, bs, ny)
+    assert new is not None
+    assert max(M.strip_loads(w2, new, bs)) < max(M.strip_loads(w2, b, bs))
+    assert new[0][0] == 0 and new[-1][1] == ny and all(j0 % bs == 0 for j0, _ in new)
+    # a marginal gain below the threshold keeps the strips
+    w3 = w.copy()
+    w3[0] = 1.01
+    assert M.rebalance_bounds(w3, b, bs, ny, threshold=0.05) is None
