@@ -55,6 +55,9 @@ constexpr int STHR = SWF_STEP_THREADS;  // k_step (a multiple of 32)
 static_assert(STHR % 32 == 0, "k_step threads must be whole warps");
 constexpr int RED_CTAS = 148;
 constexpr int NPART_ALLOC = 5;  // doubles per tile in d_part (see k_reduce)
+#ifndef SWF_LAMBDA_SHARE  // k_forces hands lambda(H_n, n) of the wet cells to k_step
+#define SWF_LAMBDA_SHARE 1
+#endif
 #ifndef SWF_XDIAG_SRC  // developer A/B switches of the exact-volume term stores
 #define SWF_XDIAG_SRC 1
 #endif
@@ -331,6 +334,7 @@ struct ForcesArgs {
   const double* sig;
   double* __restrict__ fpx;
   double* __restrict__ fpy;
+  double* __restrict__ lamn;  // SWF_LAMBDA_SHARE: lambda(H_n, n) of each wet cell
   int* interior;
   int* halo;
   unsigned char* bflag;
@@ -527,8 +531,15 @@ __device__ __forceinline__ void forces_tile(const Geo& G, const ForcesArgs& A, c
     size_t k = (size_t)i + (size_t)r * nx;
     double n = G.has_nfield ? A.nf[k] : G.n_manning;
     double ux = s_u[s], uy = s_v[s];
+#if SWF_LAMBDA_SHARE
+    const double lam = manning_lambda(d, P.g, n, SP);
+    A.lamn[k] = lam;  // the predictor's lambda(H12) when H12 == H_n (no source)
+    ForceOut o = cell_forces_lam(d, ux, uy, s_e[s], W, E, S, N, lam, P, G.nwind > 0, wx, wy, sg,
+                                 svx, svy, SP, SP);
+#else
     ForceOut o = cell_forces(d, ux, uy, s_e[s], W, E, S, N, n, P, G.nwind > 0, wx, wy, sg, svx,
                              svy, SP);
+#endif
     A.fpx[k] = o.fx - o.frx;
     A.fpy[k] = o.fy - o.fry;
     m = cfl_speed(m, d, ux, uy, o.fx, o.fy, P.g, P.h, SP);
@@ -663,6 +674,7 @@ struct StepArgs {
   const double* __restrict__ nf;
   const double* __restrict__ fpx;
   const double* __restrict__ fpy;
+  const double* __restrict__ lamn;  // SWF_LAMBDA_SHARE (see ForcesArgs)
   double* __restrict__ Ho;
   double* __restrict__ HUxo;
   double* __restrict__ HUyo;
@@ -889,6 +901,7 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
   for (int c = tid; c < RREG; c += STHR) {
     int i = i0 - 2 + c % RX, r = r0 - 2 + c / RX;
     double h = 0.0, mx = 0.0, my = 0.0, bb = 0.0, fx = 0.0, fy = 0.0, n = G.n_manning;
+    double lm = -1.0;
     if (i >= 0 && i < G.nx && r >= 0 && r < G.rows) {
       size_t k = (size_t)i + (size_t)r * nx;
       h = A.H[k];
@@ -898,7 +911,9 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
       fx = A.fpx[k];  // meaningful for wet cells only (k_forces writes those)
       fy = A.fpy[k];
       if (G.has_nfield) n = A.nf[k];
+      if (SWF_LAMBDA_SHARE) lm = A.lamn[k];  // likewise
     }
+    if (SWF_LAMBDA_SHARE) R[F_SX * RREG + c] = lm;  // the shift plane is free until 1b
     R[F_D * RREG + c] = h;
     R[F_U * RREG + c] = mx;
     R[F_V * RREG + c] = my;
@@ -933,8 +948,14 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
       if (act) {
         bool wet = Hn > P.eps;
         double fx = wet ? SC[c] : 0.0, fy = wet ? SC[RREG + c] : 0.0;
+        // without a source H12 == H_n: k_forces' lambda(H_n, n) is lambda(H12, n)
+        double Hk = -1.0;
+        if (SWF_LAMBDA_SHARE && wet && sg == 0.0) {
+          lam = R[F_SX * RREG + c];
+          Hk = Hn;
+        }
         predict_cell(Hn, mx, my, sg, fx, fy, NF[c], half_tau, P.eps, P.g, d, mx, my, SP, &lam,
-                     &Rd);  // Rd = recip_of(H12) whenever H12 > eps
+                     &Rd, Hk);  // Rd = recip_of(H12) whenever H12 > eps
       }
       e = d + bb;
       if (d > P.eps) {  // implies act (an inactive cell has d = Hn <= eps)
@@ -2326,6 +2347,7 @@ StepArgs step_args(swf_ctx* c) {
   A.nf = c->nf;
   A.fpx = c->fpx;
   A.fpy = c->fpy;
+  A.lamn = c->d_lamn;
   A.Ho = c->H[nxt];
   A.HUxo = c->HUx[nxt];
   A.HUyo = c->HUy[nxt];
@@ -2435,6 +2457,7 @@ int fused_enqueue_phase1(swf_ctx* c, double dt_cap, int part) {
   A.sig = c->d_sig;
   A.fpx = c->fpx;
   A.fpy = c->fpy;
+  A.lamn = c->d_lamn;
   A.interior = c->d_interior;
   A.halo = c->d_halo;
   A.bflag = c->d_bflag;
@@ -2771,6 +2794,11 @@ int fused_prepare(swf_ctx* c) {
     if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   }
   if (e == cudaSuccess && SWF_SPLIT && !c->d_redo_l) e = cudaMalloc(&c->d_redo_l, nredo * sizeof(int));
+  if (e == cudaSuccess && SWF_LAMBDA_SHARE && !c->d_lamn) {
+    const size_t bytes = (local_cells(c) ? local_cells(c) : 1) * sizeof(double);
+    e = cudaMalloc(&c->d_lamn, bytes);
+    if (e == cudaSuccess) e = cudaMemset(c->d_lamn, 0, bytes);
+  }
   // exact-diagnostics captures: full grids only (a strip's sums continue
   // its neighbours' running totals, which stay with the tile-order sums)
   const bool full = c->geo.r0 == 0 && c->geo.r1 == c->geo.rows;

@@ -119,6 +119,7 @@ struct swf_ctx {
   int cur = 0;
   double* fpx = nullptr;  // f_n.fx - f_n.fric_x (wet cells), fused path
   double* fpy = nullptr;
+  double* d_lamn = nullptr;  // SWF_LAMBDA_SHARE builds: lambda(H_n, n) of the wet cells
   // sources / wind
   std::vector<swf::DevSrc> h_src;
   std::vector<double> h_ht, h_hq;
