@@ -287,6 +287,7 @@ def b200_single(args):
     torch.cuda.set_device(0)
     t_gen = time.perf_counter()
     sc = S.build(args.config, device="cuda")
+    torch.cuda.empty_cache()  # the generator's device tensors: back to the driver for the contexts
     if args.no_skip:
         sc.options.skip_dry_blocks = False
     gen_s = time.perf_counter() - t_gen
@@ -460,6 +461,7 @@ def b200_nested(args):
     torch.cuda.set_device(0)
     t_gen = time.perf_counter()
     ns = S.nested_floodplain(device="cuda")
+    torch.cuda.empty_cache()
     gen_s = time.perf_counter() - t_gen
     sc, fs = ns.coarse, ns.fine
     coarse = CsphTvdStepper(sc.terrain, sc.params, sc.control, sc.options)

@@ -54,7 +54,7 @@ int check_device_error(swf_ctx* c) {
   cudaError_t e = cudaMemcpy(c->h_sc, c->d_sc, sizeof(StepScalars), cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return cuda_check(c, e, "scalar readback");
   unsigned long long key = c->h_sc->err_key;
-  if (key == ERR_NONE) return SWF_OK;
+  if (key == ERR_NONE || (key >> 58) == ERR_IDLE) return SWF_OK;
   unsigned long long kind = key >> 58;
   const Geo& G = c->geo;
   if (kind == ERR_DT) {
@@ -303,7 +303,12 @@ int create_impl(const swf_terrain* T, const swf_params* P, const swf_control* K,
     e = cudaMemcpy(c->d_sc, c->h_sc, sizeof(StepScalars), cudaMemcpyHostToDevice);
   }
   for (int i = 0; i < 10 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
-  if (e == cudaSuccess && fused_prepare(c) != SWF_OK) e = cudaErrorInvalidValue;
+  if (e == cudaSuccess && fused_prepare(c) != SWF_OK) {
+    // fused_prepare recorded the CUDA error text (out of memory, ...)
+    g_err = c->err;
+    swf_destroy(c);
+    return SWF_ECUDA;
+  }
   if (e == cudaSuccess && fused_tile_srcm(c) != SWF_OK) e = cudaErrorInvalidValue;
   if (e != cudaSuccess) {
     rc = cuda_check(nullptr, e, "context allocation");
@@ -367,6 +372,10 @@ int commit_batch(swf_ctx* c, int cur_start, int enqueued, int* done) {
 
 namespace swf {
 void invalidate_graph(swf_ctx* c) { drop_graph(c); }
+int batch_reset(swf_ctx* c) { return reset_counters(c); }
+int batch_commit(swf_ctx* c, int cur_start, int enqueued, int* done) {
+  return commit_batch(c, cur_start, enqueued, done);
+}
 }  // namespace swf
 
 extern "C" {
@@ -598,7 +607,7 @@ int swf_step(swf_ctx* c, double dt_cap, swf_step_info* info) {
     return rc;
   }
   if (!info) return SWF_OK;  // errors surface at the next synchronising call
-  if ((rc = fused_exact_volumes(c))) return rc;
+  if (!c->defer_volumes && (rc = fused_exact_volumes(c))) return rc;
   cudaError_t e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) return cuda_check(c, e, "step");
   rc = commit_batch(c, cur0, 1, nullptr);

@@ -75,7 +75,6 @@ constexpr int NPART_ALLOC = 5;  // doubles per tile in d_part (see k_reduce)
 #define SWF_FORCES_MINB 9
 #endif
 
-__device__ __forceinline__ bool stopped(const StepScalars* sc) { return sc->err_key != ERR_NONE; }
 
 // Developer instrumentation (-DSWF_PHASE_TIMING): per-phase cycles of
 // k_step summed over CTAs (thread 0 of each CTA; phases end at barriers).
@@ -171,6 +170,7 @@ __global__ void k_tau(Geo G, const DevSrc* src, const double* ht, const double* 
     }
     tau = smin(tau, cfl);
   }
+  if (dt_cap < 0.0) dt_cap = sc->dt_cap_dev;  // set on the device (nested subcycling)
   if (dt_cap > 0.0) tau = smin(tau, dt_cap);
   sc->tau = tau;
   mid_scalars(G, src, ht, hq, wt, wv, sig, sc, tau);
@@ -195,6 +195,7 @@ __device__ __forceinline__ bool wet_at(const Geo& G, const double* H, const DevS
 
 __global__ void k_mask(Geo G, const double* H, const DevSrc* src, const double* sig,
                        int* interior, int* halo, unsigned char* bflag, StepScalars* sc) {
+  if (stopped(sc)) return;  // (see k_flist)
   int nbl = G.nbx * (G.bj1 - G.bj0);
   int lb = blockIdx.x * blockDim.x + threadIdx.x;
   bool lag = false, flx = false;
@@ -231,7 +232,9 @@ __global__ void k_mask(Geo G, const double* H, const DevSrc* src, const double* 
 
 // k_tiles: fused-tile flags from the B-block flags.  bit0: some overlapping
 // block is Lagrangian-active; bit1: some overlapping block is flux-active.
-__global__ void k_tiles(Geo G, const unsigned char* bflag, unsigned char* tile_act) {
+__global__ void k_tiles(Geo G, const unsigned char* bflag, unsigned char* tile_act,
+                        const StepScalars* sc) {
+  if (stopped(sc)) return;  // (see k_flist)
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= G.tiles_x * G.tiles_y) return;
   int tx = t % G.tiles_x, ty = t / G.tiles_x;
@@ -593,6 +596,9 @@ __global__ void k_flist(Geo G, ForcesArgs A) {
   const int nt = G.tiles_x * (A.lr1 - A.lr0);
   const int t = blockIdx.x * blockDim.x + threadIdx.x;  // list index: relative to row lr0
   StepScalars* sc = A.sc;
+  // a stopped context's remaining steps of a batch must not touch the tile
+  // flags or grow the list (k_begin, which resets it, did not run)
+  if (stopped(sc)) return;
   const int tx = t % G.tiles_x, tr = t / G.tiles_x + A.lr0;
   // a strip's ghost tile rows and the tile rows next to its edges are always
   // visited (their halo changes by exchange), like forces_tile's own rule
@@ -1354,6 +1360,7 @@ __global__ void __launch_bounds__(STHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A)
 // ones whose two ping-pong copies still differ; every other tile keeps its
 // state and gets zero diagnostics partials here.
 __global__ void k_slist(Geo G, StepArgs A) {
+  if (stopped(A.sc)) return;  // (see k_flist)
   const int nt = G.tiles_x * G.tiles_y;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = t < nt;  // every lane reaches the warp-wide append
@@ -2412,7 +2419,8 @@ int launch_mask(swf_ctx* c) {
                                                       c->d_sc);
   int nt = G.tiles_x * G.tiles_y;
   if (nt > 0)
-    k_tiles<<<(nt + 127) / 128, 128, 0, c->stream>>>(G, c->d_bflag, tile_act_at(c, c->cur));
+    k_tiles<<<(nt + 127) / 128, 128, 0, c->stream>>>(G, c->d_bflag, tile_act_at(c, c->cur),
+                                                     c->d_sc);
   return cuda_check(c, cudaGetLastError(), "k_mask");
 }
 

@@ -52,6 +52,7 @@ struct StepScalars {
   int fail_step;    // step index of the first failure (-1 none)
   double deficit, srcvol, outflow;  // this step's diagnostics (volumes)
   double speed_local;               // strips: local max speed (phase 1 out)
+  double dt_cap_dev;                // dt_cap of a step enqueued with dt_cap < 0 (k_tau)
   int mask_valid;  // the tile flags of the previous step describe the current state
   int mask_fresh;  // != 0: k_mask/k_tiles just flagged the current state (host step);
                    // cleared by k_tau
@@ -62,12 +63,20 @@ struct StepScalars {
 
 // ERR_PEER: stopped because another strip of a swf_group aborted (ranks
 // above every real error, so atomicMin keeps a strip's own error)
-enum ErrKind : unsigned long long { ERR_DT = 1, ERR_CFL = 2, ERR_FLUX = 3, ERR_PEER = 7 };
+// ERR_IDLE: not an error -- a nested grid's device-driven subcycling reached
+// the global time, so the remaining enqueued substeps of the batch skip
+// (ranks above ERR_PEER; check_device_error reports it as success)
+enum ErrKind : unsigned long long { ERR_DT = 1, ERR_CFL = 2, ERR_FLUX = 3, ERR_PEER = 7,
+                                    ERR_IDLE = 8 };
 constexpr unsigned long long ERR_NONE = ~0ull;
 // A strip that has stopped publishes this as its CFL speed (the bits of a NaN
 // above every non-negative double's bits): an int64 allreduce-MAX of the
 // speeds then carries the stop to every rank, whose k_tau stops too.
 constexpr unsigned long long SPEED_STOP_BITS = 0x7fffffffffffffffull;
+
+// Every step kernel returns early once the context has stopped (an error,
+// another strip's stop, or idle subcycling).
+__device__ __forceinline__ bool stopped(const StepScalars* sc) { return sc->err_key != ERR_NONE; }
 
 // Launch-invariant parameters of one context (passed by value to kernels).
 struct Geo {
@@ -179,6 +188,7 @@ struct swf_ctx {
   long long last_ingest_bytes = 0;
   int batch_steps = 0;
   int last_staged = 0;  // which path produced the last diagnostics
+  int defer_volumes = 0;  // swf_step leaves the exact volumes to its caller (nested coupling)
   // timing
   bool timing = false;
   cudaEvent_t ev[10] = {};
@@ -233,6 +243,10 @@ int check_device_error(swf_ctx* c);  // after a sync: maps err_key to status
 size_t local_cells(const swf_ctx* c);
 void invalidate_mask(swf_ctx* c);  // the state changed outside the fused path
 void invalidate_graph(swf_ctx* c); // the captured step no longer matches the context
+// a batch of enqueued steps: reset the device counters before, and after the
+// synchronisation commit the steps done (ping-pong index, error status)
+int batch_reset(swf_ctx* c);
+int batch_commit(swf_ctx* c, int cur_start, int enqueued, int* done);
 inline unsigned char* tile_act_at(swf_ctx* c, int parity) {
   return c->d_tile_act + (size_t)parity * ((size_t)c->geo.tiles_x * c->geo.tiles_y);
 }

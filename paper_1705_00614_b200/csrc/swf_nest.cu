@@ -62,6 +62,8 @@ struct swf_nest {
   double* tap_f = nullptr;      // fine faces of one substep: 2*r*(ni+nj)
   double* tap_fsum = nullptr;   // their sum over the substeps
   double* clampv = nullptr;     // per boundary face: volume added by the reflux clamp
+  double* d_sub = nullptr;      // device subcycling scalars: [alpha, smallest fine tau]
+  int last_subs = 0;            // substeps of the previous coupled step (batch size hint)
   std::string err;
 };
 
@@ -316,6 +318,67 @@ int nest_cuda(swf_nest* n, cudaError_t e, const char* what) {
   return nest_err(n, SWF_ECUDA, std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
 }
 
+// ---- device-driven subcycling (no host round trip per fine substep) --------
+// Per substep: k_sub_begin decides on the device whether the fine grid still
+// lags the global time t1 (else it marks the context idle, which makes every
+// remaining kernel of the batch skip), and sets alpha and dt_cap; then the
+// ghost band, the fused step with dt_cap read on the device, the face taps
+// and k_sub_end (the smallest fine tau).
+__global__ void k_sub_begin(StepScalars* sc, double t0, double t1, double tol, int first,
+                            double tau_g, double* alpha) {
+  if (stopped(sc)) return;
+  const double tf = sc->t;
+  if (!(t1 - tf > tol)) {  // landed on t1: the remaining substeps of the batch skip
+    sc->err_key = ERR_IDLE << 58;
+    return;
+  }
+  // the first substep is capped by the global tau itself (t1 - t0 can differ
+  // from it in the last bit), later ones by the remaining time
+  sc->dt_cap_dev = first ? tau_g : t1 - tf;
+  *alpha = (tf - t0) / (t1 - t0);
+}
+
+__global__ void k_sub_end(const StepScalars* sc, double* tau_min) {
+  if (stopped(sc)) return;
+  if (sc->tau < *tau_min) *tau_min = sc->tau;
+}
+
+__global__ void k_ghost_apply_dev(NestGeo N, const double* __restrict__ g0,
+                                  const double* __restrict__ g1, const double* alpha,
+                                  const StepScalars* sc, double* __restrict__ H,
+                                  double* __restrict__ U, double* __restrict__ V,
+                                  unsigned char* tile_prev, unsigned char* tile_same,
+                                  int tiles_x) {
+  if (stopped(sc)) return;
+  long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (q >= N.nghost) return;
+  int fi, fj;
+  ghost_cell(N, q, fi, fj);
+  long long G = N.nghost;
+  const double a = *alpha;
+  double h = lerp(g0[q], g1[q], a);
+  double u = lerp(g0[G + q], g1[G + q], a);
+  double v = lerp(g0[2 * G + q], g1[2 * G + q], a);
+  if (!(h > N.eps)) {
+    u = 0.0;
+    v = 0.0;
+  }
+  size_t k = (size_t)fi + (size_t)fj * N.nxf;
+  H[k] = h;
+  U[k] = u;
+  V[k] = v;
+  int t = fi / TBX + (fj / TBY) * tiles_x;
+  tile_prev[t] = 3;
+  tile_same[t] = 0;
+}
+
+__global__ void k_tap_add_dev(int n, const StepScalars* sc, const double* __restrict__ a,
+                              double* __restrict__ sum) {
+  if (stopped(sc)) return;
+  int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n) sum[q] = sum[q] + a[q];
+}
+
 double host_t(swf_ctx* c) {
   double t = 0.0;
   cudaMemcpy(&t, &c->d_sc->t, sizeof(double), cudaMemcpyDeviceToHost);
@@ -415,6 +478,7 @@ void swf_nest_destroy(swf_nest* n) {
   cudaFree(n->tap_f);
   cudaFree(n->tap_fsum);
   cudaFree(n->clampv);
+  cudaFree(n->d_sub);
   delete n;
 }
 
@@ -513,39 +577,99 @@ int swf_coupled_step(swf_ctx* coarse, swf_nest** nests, int nn, double dt_cap,
     int rc = swf_nest_prolong(nests[q], 0);
     if (rc) return set_err(coarse, rc, nests[q]->err);
   }
+  // the global step; its exact StepInfo volumes are reduced on the coarse
+  // stream while the fine substeps run on theirs (the terms, the step's
+  // block flags and its step-start depth stay put until the next global step)
+  coarse->defer_volumes = 1;
   int rc = swf_step(coarse, dt_cap, &I.coarse);
+  coarse->defer_volumes = 0;
   if (rc) return rc;  // global abort: both levels untouched
   double t1 = host_t(coarse);
   double tau_g = t1 - t0;
   I.tau = I.coarse.tau;
   I.fine_tau_min = INFINITY;
+  // the ghosts at t1 of every window, then (behind them on the coarse
+  // stream) the global step's exact volumes, overlapping the fine substeps,
+  // which wait for the prolongations only
+  for (int q = 0; q < nn; ++q) {
+    rc = swf_nest_prolong(nests[q], 1);
+    if (rc) return set_err(coarse, rc, nests[q]->err);
+  }
+  cudaEvent_t prolonged = nullptr;
+  cudaError_t e = cudaEventCreateWithFlags(&prolonged, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(prolonged, coarse->stream);
+  if (e != cudaSuccess) return cuda_check(coarse, e, "nest prolongation event");
+  struct EventGuard {
+    cudaEvent_t ev;
+    ~EventGuard() { cudaEventDestroy(ev); }
+  } guard{prolonged};
+  if (coarse->mode == 0 && (rc = fused_exact_volumes(coarse))) return rc;
   for (int q = 0; q < nn; ++q) {
     swf_nest* n = nests[q];
     swf_ctx* f = n->fine;
-    rc = swf_nest_prolong(n, 1);
-    if (rc) return set_err(coarse, rc, n->err);
-    double tf = t0;
     double tol = std::fmax(1e-9 * tau_g, 8.0 * 2.220446049250313e-16 * std::fabs(t1));
     int sub = 0;
     const int nft = n->tap_f ? 2 * n->d.r * (n->d.ni + n->d.nj) : 0;
     if (nft) cudaMemsetAsync(n->tap_fsum, 0, nft * sizeof(double), f->stream);
-    while (t1 - tf > tol) {
-      double alpha = (tf - t0) / (t1 - t0);
-      rc = swf_nest_apply_ghosts(n, alpha);
-      if (rc) return set_err(coarse, rc, n->err);
-      swf_step_info fi;
-      // the first substep is capped by the global tau itself (t1 - t0 can
-      // differ from it in the last bit), later ones by the remaining time
-      rc = swf_step(f, sub == 0 ? I.tau : t1 - tf, &fi);
+    // the fine substeps in device-driven batches (the prolongations of t0 and
+    // t1 were written on the coarse stream): one host synchronisation per
+    // batch, sized from the previous coupled step
+    e = cudaStreamWaitEvent(f->stream, prolonged, 0);
+    if (e != cudaSuccess) return cuda_check(coarse, e, "nest (wait for the ghosts)");
+    if (!n->d_sub && (e = cudaMalloc(&n->d_sub, 2 * sizeof(double))) != cudaSuccess)
+      return cuda_check(coarse, e, "nest subcycling scalars");
+    const double init[2] = {0.0, INFINITY};
+    cudaMemcpyAsync(n->d_sub, init, sizeof init, cudaMemcpyHostToDevice, f->stream);
+    NestGeo N = nest_geo(n);
+    const unsigned gblocks = (unsigned)((n->nghost + 255) / 256);
+    bool landed = false;
+    // batch size: the previous coupled step's substep count (capped), then
+    // one substep per batch while the fine grid still lags -- an idle
+    // substep costs about as much as the host round trip it saves
+    int batch = std::min(32, std::max(1, n->last_subs));
+    while (!landed) {
+      int cur0 = f->cur;
+      if ((rc = batch_reset(f))) return set_err(coarse, rc, swf_last_error(f));
+      for (int b = 0; b < batch; ++b) {
+        k_sub_begin<<<1, 1, 0, f->stream>>>(f->d_sc, t0, t1, tol, sub == 0 && b == 0 ? 1 : 0,
+                                            I.tau, n->d_sub);
+        if (gblocks)
+          k_ghost_apply_dev<<<gblocks, 256, 0, f->stream>>>(
+              N, n->g[0], n->g[1], n->d_sub, f->d_sc, f->H[f->cur], f->HUx[f->cur],
+              f->HUy[f->cur], tile_act_at(f, 1 - f->cur), f->d_tile_same, f->geo.tiles_x);
+        if ((rc = fused_enqueue_step(f, -1.0))) {  // dt_cap from k_sub_begin
+          f->cur = cur0;
+          return set_err(coarse, rc, std::string("nested grid: ") + swf_last_error(f));
+        }
+        if (nft)
+          k_tap_add_dev<<<(nft + 255) / 256, 256, 0, f->stream>>>(nft, f->d_sc, n->tap_f,
+                                                                  n->tap_fsum);
+        k_sub_end<<<1, 1, 0, f->stream>>>(f->d_sc, n->d_sub + 1);
+      }
+      e = cudaStreamSynchronize(f->stream);
+      if (e != cudaSuccess) return cuda_check(coarse, e, "nest substeps");
+      int done = 0;
+      rc = batch_commit(f, cur0, batch, &done);
       if (rc) return set_err(coarse, rc, std::string("nested grid: ") + swf_last_error(f));
-      if (fi.tau < I.fine_tau_min) I.fine_tau_min = fi.tau;
-      if (nft) k_tap_add<<<(nft + 255) / 256, 256, 0, f->stream>>>(nft, n->tap_f, n->tap_fsum);
-      tf = host_t(f);
-      if (++sub > 1000000)
+      sub += done;
+      // landed: marked idle, or the last substep of the batch reached t1
+      landed = (f->h_sc->err_key >> 58) == ERR_IDLE || !(t1 - f->h_sc->t > tol);
+      if (sub > 1000000)
         return set_err(coarse, SWF_ENUMERICAL, "nested grid: subcycling does not converge");
+      batch = 1;
     }
+    // the idle marker has done its job: clear it for the fine context's next calls
+    f->h_sc->err_key = ERR_NONE;
+    e = cudaMemcpyAsync(&f->d_sc->err_key, &f->h_sc->err_key, sizeof(unsigned long long),
+                        cudaMemcpyHostToDevice, f->stream);
+    if (e != cudaSuccess) return cuda_check(coarse, e, "nest idle reset");
+    n->last_subs = sub;
+    double sub_scalars[2];
+    e = cudaMemcpy(sub_scalars, n->d_sub, sizeof sub_scalars, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_check(coarse, e, "nest substep taus");
+    if (sub_scalars[1] < I.fine_tau_min) I.fine_tau_min = sub_scalars[1];
     // land exactly on the global time
-    cudaError_t e = cudaMemcpy(&f->d_sc->t, &t1, sizeof(double), cudaMemcpyHostToDevice);
+    e = cudaMemcpy(&f->d_sc->t, &t1, sizeof(double), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return cuda_check(coarse, e, "nest time sync");
     f->h_t = t1;
     I.substeps_total += sub;
@@ -558,6 +682,17 @@ int swf_coupled_step(swf_ctx* coarse, swf_nest** nests, int nn, double dt_cap,
     }
   }
   if (nn == 0) I.fine_tau_min = 0.0;
+  // the global step's volumes (fused path: reduced behind the substeps)
+  if (coarse->mode == 0) {
+    double vol[3];
+    cudaError_t ev = cudaStreamSynchronize(coarse->stream);
+    if (ev == cudaSuccess)
+      ev = cudaMemcpy(vol, &coarse->d_sc->deficit, sizeof vol, cudaMemcpyDeviceToHost);
+    if (ev != cudaSuccess) return cuda_check(coarse, ev, "coupled step volumes");
+    I.coarse.clamp_deficit_volume = vol[0];
+    I.coarse.source_volume = vol[1];
+    I.coarse.boundary_outflow_volume = vol[2];
+  }
   return SWF_OK;
 }
 

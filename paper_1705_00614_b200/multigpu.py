@@ -508,6 +508,8 @@ class RankStrip:
         if no_skip:
             sc.options.skip_dry_blocks = False
         self.sc = sc
+        import torch
+        torch.cuda.empty_cache()  # the generator's device tensors, before the strip allocates
         srcs = S.clip_sources(sc.global_sources, self.n, self.ny) if self.weak else sc.global_sources
         self.strip = Strip(sc, self.ny, self.j0, self.j1, srcs, sc.wind, device=self.local)
 

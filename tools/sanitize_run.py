@@ -46,6 +46,11 @@ def main():
     hs = FlowState(st.nx, st.ny, st.t, pin(st.H), pin(st.HUx), pin(st.HUy))
     g.step(hs)
     g.step(hs)
+    # opt-in host mirror: the upload step, then steps without ingest
+    g.set_host_mirror(True)
+    for _ in range(3):
+        g.step(hs)
+    g.set_host_mirror(False)
     # staged path
     s2 = make(sc, mode=1)
     s2.step(sc.state.copy())
