@@ -341,6 +341,35 @@ def test_cfl_abort_leaves_state_untouched(gpu_cls, oracle_built):
         assert_state_bitwise(st, before, "state changed on abort")
 
 
+def test_long_run_after_an_early_abort_stays_clean(gpu_cls, oracle_built):
+    """swf_run enqueues all its steps up front: after a CFL abort in the first
+    step, the remaining 300 steps of the run are stopped on the device.  They
+    must neither grow the work lists nor rewrite the tile flags, so the state
+    is untouched and the same context then steps another state bit for bit."""
+    from paper_1705_00614_b200 import NumericalError
+    sc = _cfl_case()
+    sc.control.dt_max = 0.1  # tau = 0.1 (the failing step of test_cfl_abort_...)
+    s = make(gpu_cls, sc)
+    st = sc.state.copy()
+    s.upload(st)
+    with pytest.raises(NumericalError, match="particle displacement"):
+        s.run(301)
+    after = sc.state.copy()
+    s.download(after)
+    assert_state_bitwise(after, sc.state, "state after the aborted run")
+    # the same context, a healthy state: bitwise against the oracle
+    good = sc.state.copy()
+    good.HUx[:] = 0.1
+    o = make(oracle_built.OracleStepper, sc, kind="orc")
+    ref = good.copy()
+    s.upload(good)
+    s.run(40, 0.01)
+    s.download(good)
+    for _ in range(40):
+        o.step(ref, 0.01)
+    assert_state_bitwise(good, ref, "steps after the aborted run")
+
+
 def test_dt_floor_abort(gpu_cls):
     from paper_1705_00614_b200 import NumericalError
     sc = S.dam_break_1d(False, 0.0, nx=64, ny=8)
