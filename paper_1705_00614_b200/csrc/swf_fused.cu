@@ -64,8 +64,14 @@ constexpr int NPART_ALLOC = 5;  // doubles per tile in d_part (see k_reduce)
 #ifndef SWF_XDIAG_DEF
 #define SWF_XDIAG_DEF 1
 #endif
+#ifndef SWF_STEP_SLIM  // k_step's slim region (see the plane enum); -DSWF_STEP_SLIM=0: the full one
+#define SWF_STEP_SLIM 1
+#endif
+#ifndef SWF_SPLIT  // the split step (k_lag + k_flux), measured and opt-in; needs SWF_STEP_SLIM=0
+#define SWF_SPLIT 0
+#endif
 #ifndef SWF_STEP_MINB
-#define SWF_STEP_MINB 3  // CTAs per SM the register budget of k_step targets
+#define SWF_STEP_MINB (SWF_STEP_SLIM ? 4 : 3)  // CTAs per SM the register budget of k_step targets
 #endif
 #ifndef SWF_FORCES_MINB
 // 9 CTAs of 128 threads per SM caps k_forces at 56 registers; ptxas then
@@ -664,13 +670,27 @@ __global__ void __launch_bounds__(FTHR, SWF_FORCES_MINB) k_forces_redo(Geo G, Fo
 // ---------------------------------------------------------------------------
 
 // shared-memory fields of the 2-cell-halo region (RX x RY), half-step view
+#if SWF_STEP_SLIM
+// slim region (the default): depth, velocities and bed only -- eta = d + b
+// and the shifts 0.5*tau*u recomputed at the point of use with the stored
+// planes' own expressions (bit-identical), the step-start state, f', n and
+// lambda read from global memory -- for 4 CTAs of 256 threads per SM (54 KB
+// of shared memory, 64 registers): k_step 11.0 -> 10.5 ms on C3 (the full
+// region, 76 KB and 80 registers, fits 3; profiles/README.md round 3)
+enum { F_D = 0, F_U, F_V, F_B, F_NUM };
+#else
 enum { F_D = 0, F_E, F_U, F_V, F_SX, F_SY, F_B, F_NUM };
+#endif
 constexpr int NSL = (BX + 2) * BY > BX * (BY + 2) ? (BX + 2) * BY : BX * (BY + 2);  // slopes
 constexpr int NFC = (BX + 1) * BY > BX * (BY + 1) ? (BX + 1) * BY : BX * (BY + 1);  // faces
 constexpr int SCRATCH_A = 3 * NSL + 4 * NFC;               // slopes + faces (phases 3-5)
 // phase 1-2 staging (see k_step), + the predictor's Manning lambda per owned cell
 constexpr int SCRATCH_B = 3 * NSL + 3 * BX * BY + RREG + BX * BY;
+#if SWF_STEP_SLIM
+constexpr int SCRATCH = SCRATCH_A;  // lambda per owned cell lives in the face planes until phase 3
+#else
 constexpr int SCRATCH = SCRATCH_A > SCRATCH_B ? SCRATCH_A : SCRATCH_B;
+#endif
 
 struct StepArgs {
   const double* __restrict__ H;
@@ -824,6 +844,29 @@ __device__ __forceinline__ FaceRec face_from_sides(bool wetA, bool wetB, const S
   return rec;
 }
 
+// region-plane accessors of step_tile: eta and the shifts stored, or (slim
+// variant) recomputed from depth, bed and velocity with the same expressions
+#if SWF_STEP_SLIM
+struct SNbrB {  // SNbr with eta = depth + b at the point of use
+  bool in;
+  const double *d, *b, *u, *v;
+  int q;
+  __device__ __forceinline__ double dep() const { return d[q]; }
+  __device__ __forceinline__ double et() const { return d[q] + b[q]; }
+  __device__ __forceinline__ double vx() const { return u[q]; }
+  __device__ __forceinline__ double vy() const { return v[q]; }
+};
+#define R_E(q) (R[F_D * RREG + (q)] + R[F_B * RREG + (q)])
+#define R_SX(q) (0.5 * (tau * R[F_U * RREG + (q)]))
+#define R_SY(q) (0.5 * (tau * R[F_V * RREG + (q)]))
+#define NB_VIEW(in, q) SNbrB{in, R + F_D * RREG, R + F_B * RREG, R + F_U * RREG, R + F_V * RREG, q}
+#else
+#define R_E(q) R[F_E * RREG + (q)]
+#define R_SX(q) R[F_SX * RREG + (q)]
+#define R_SY(q) R[F_SY * RREG + (q)]
+#define NB_VIEW(in, q) SNbr{in, R + F_D * RREG, R + F_E * RREG, R + F_U * RREG, R + F_V * RREG, q}
+#endif
+
 template <bool SPEC>
 __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const int tile) {
   extern __shared__ double smem[];
@@ -895,6 +938,67 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
   // f', n and the owned cells' step-start state meanwhile.
   // Phase 2 reads OWN and NF after phase-2 threads may already be writing the
   // x slopes (no barrier between them), so both live above the slope block.
+#if SWF_STEP_SLIM
+  // lambda(H12, n) of the owned cells as the predictor evaluated it (or -1),
+  // in the face planes, which phase 4x writes only after phase 2 is done
+  double* LAM = FB;
+  static_assert(BX * BY <= 4 * NFC, "lambda plane");
+  for (int c = tid; c < RREG; c += STHR) {
+    int i = i0 - 2 + c % RX, r = r0 - 2 + c / RX;
+    double h = 0.0, mx = 0.0, my = 0.0, bb = 0.0;
+    if (i >= 0 && i < G.nx && r >= 0 && r < G.rows) {
+      size_t k = (size_t)i + (size_t)r * nx;
+      h = A.H[k];
+      mx = A.HUx[k];
+      my = A.HUy[k];
+      bb = A.b[k];
+    }
+    R[F_D * RREG + c] = h;
+    R[F_U * RREG + c] = mx;
+    R[F_V * RREG + c] = my;
+    R[F_B * RREG + c] = bb;
+  }
+  __syncthreads();
+
+  PHASE_MARK(0);
+  // ---- phase 1b: half-step view on the region (K4 predictor, HalfView) -----
+  for (int c = tid; c < RREG; c += STHR) {
+    int xr = c % RX, yr = c / RX;
+    int i = i0 - 2 + xr, r = r0 - 2 + yr;
+    double d = 0.0, u = 0.0, v = 0.0;
+    double Hn = R[F_D * RREG + c], mx = R[F_U * RREG + c], my = R[F_V * RREG + c];
+    const bool owned = xr >= 2 && xr < BX + 2 && yr >= 2 && yr < BY + 2;
+    const int o = (xr - 2) + (yr - 2) * BX;
+    double lam = -1.0;
+    if (i >= 0 && i < G.nx && r >= 0 && r < G.rows) {
+      const size_t k = (size_t)i + (size_t)r * nx;
+      double sg = srcm ? msig(G, A.src, sig_n, srcm, i, G.jg0 + r) : 0.0;
+      bool act = Hn > P.eps || sg != 0.0;
+      d = Hn;
+      Recip Rd{0.0, 0.0};
+      if (act) {
+        bool wet = Hn > P.eps;
+        double fx = wet ? A.fpx[k] : 0.0, fy = wet ? A.fpy[k] : 0.0;
+        double Hk = -1.0;
+        if (SWF_LAMBDA_SHARE && wet && sg == 0.0) {
+          lam = A.lamn[k];
+          Hk = Hn;
+        }
+        predict_cell(Hn, mx, my, sg, fx, fy, G.has_nfield ? A.nf[k] : G.n_manning, half_tau,
+                     P.eps, P.g, d, mx, my, SP, &lam, &Rd, Hk);
+      }
+      if (d > P.eps) {
+        u = rdiv(mx, Rd, SP);
+        v = rdiv(my, Rd, SP);
+      }
+    }
+    R[F_D * RREG + c] = d;
+    R[F_U * RREG + c] = u;
+    R[F_V * RREG + c] = v;
+    if (owned) LAM[o] = lam;
+  }
+  __syncthreads();
+#else
   double* SC = SL;                      // [0,RREG) fpx  [RREG,2RREG) fpy   (phase 1 only)
   double* OWN = SL + 3 * NSL;           // 3 x (BX*BY): H, HUx, HUy at t_n of owned cells
   double* NF = OWN + 3 * BX * BY;       // RREG: Manning n of the region
@@ -985,6 +1089,7 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
   }
   __syncthreads();
 
+#endif  // SWF_STEP_SLIM
   PHASE_MARK(1);
   // ---- phase 2: K5 mid forces + K6 corrector on owned active cells ---------
   constexpr int PER = (BX * BY + STHR - 1) / STHR;  // owned cells per thread (2 at 256)
@@ -998,7 +1103,17 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
     if (BX * BY % STHR && c >= BX * BY) break;
     int x = c % BX, y = c / BX;
     int i = i0 + x, r = r0 + y;
+#if SWF_STEP_SLIM
+    double Hn = 0.0, qxn = 0.0, qyn = 0.0;
+    if (i < G.nx && r < G.r1) {
+      const size_t k0 = (size_t)i + (size_t)r * nx;
+      Hn = A.H[k0];
+      qxn = A.HUx[k0];
+      qyn = A.HUy[k0];
+    }
+#else
     double Hn = OWN[c], qxn = OWN[BX * BY + c], qyn = OWN[2 * BX * BY + c];
+#endif
     Ht[m] = Hn;
     Qx[m] = qxn;
     Qy[m] = qyn;
@@ -1012,7 +1127,11 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
     }
     bool act = Hn > P.eps || sgn_ != 0.0;
     if (!act) continue;
+#if SWF_STEP_SLIM
+    double n = G.has_nfield ? A.nf[(size_t)i + (size_t)r * nx] : G.n_manning;
+#else
     double n = NF[s];
+#endif
     double d = R[F_D * RREG + s];  // H12
     double fmx = 0.0, fmy = 0.0;
     // lambda depends on (depth, n) only: the predictor's lambda(H12) serves
@@ -1020,13 +1139,13 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
     double lam = LAM[c], Hk = -1.0;
     if (d > P.eps) {
       auto nb = [&](bool in, int q) {
-        return SNbr{in, R + F_D * RREG, R + F_E * RREG, R + F_U * RREG, R + F_V * RREG, q};
+        return NB_VIEW(in, q);
       };
-      SNbr W = nb(i > 0, s - 1), E = nb(i + 1 < G.nx, s + 1);
-      SNbr S = nb(jg > 0, s - RX), N = nb(jg + 1 < G.ny, s + RX);
+      auto W = nb(i > 0, s - 1), E = nb(i + 1 < G.nx, s + 1);
+      auto S = nb(jg > 0, s - RX), N = nb(jg + 1 < G.ny, s + RX);
       if (!(lam >= 0.0)) lam = manning_lambda(d, P.g, n);
       Hk = d;
-      ForceOut o = cell_forces_lam(d, R[F_U * RREG + s], R[F_V * RREG + s], R[F_E * RREG + s],
+      ForceOut o = cell_forces_lam(d, R[F_U * RREG + s], R[F_V * RREG + s], R_E(s),
                                    W, E, S, N, lam, P, G.nwind > 0, wmx, wmy,
                                    nsrc > 0 ? sgm : 0.0, svx, svy, SP);
       fmx = o.fx - o.frx;
@@ -1061,10 +1180,10 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
     int s = (xx + 1) + (y + 2) * RX;
     double se = 0.0, su = 0.0, st = 0.0;
     if (i > 0 && i + 1 < G.nx && R[F_D * RREG + s] > P.eps) {
-      Slopes q = cell_slopes(R[F_E * RREG + s - 1], R[F_U * RREG + s - 1], R[F_V * RREG + s - 1],
-                             R[F_SX * RREG + s - 1], R[F_E * RREG + s], R[F_U * RREG + s],
-                             R[F_V * RREG + s], R[F_SX * RREG + s], R[F_E * RREG + s + 1],
-                             R[F_U * RREG + s + 1], R[F_V * RREG + s + 1], R[F_SX * RREG + s + 1],
+      Slopes q = cell_slopes(R_E(s - 1), R[F_U * RREG + s - 1], R[F_V * RREG + s - 1],
+                             R_SX(s - 1), R_E(s), R[F_U * RREG + s],
+                             R[F_V * RREG + s], R_SX(s), R_E(s + 1),
+                             R[F_U * RREG + s + 1], R[F_V * RREG + s + 1], R_SX(s + 1),
                              P.h, SP);
       se = q.eta;
       su = q.un;
@@ -1109,13 +1228,13 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
           Rr = L;
           if (wetA) {
             Slopes q = {SL[la], SL[NSL + la], SL[2 * NSL + la]};
-            L = side_from_slopes(R[F_E * RREG + sa], R[F_U * RREG + sa], R[F_V * RREG + sa],
-                                 R[F_SX * RREG + sa], bA, q, face_p, bf);
+            L = side_from_slopes(R_E(sa), R[F_U * RREG + sa], R[F_V * RREG + sa],
+                                 R_SX(sa), bA, q, face_p, bf);
           }
           if (wetB) {
             Slopes q = {SL[lb], SL[NSL + lb], SL[2 * NSL + lb]};
-            Rr = side_from_slopes(R[F_E * RREG + sa + 1], R[F_U * RREG + sa + 1],
-                                  R[F_V * RREG + sa + 1], R[F_SX * RREG + sa + 1], bB, q, face_m,
+            Rr = side_from_slopes(R_E(sa + 1), R[F_U * RREG + sa + 1],
+                                  R[F_V * RREG + sa + 1], R_SX(sa + 1), bB, q, face_m,
                                   bf);
           }
           rec = face_from_sides(wetA, wetB, L, Rr, P.g, SP);
@@ -1165,11 +1284,11 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
     int s = (x + 2) + (yy + 1) * RX;
     double se = 0.0, su = 0.0, st = 0.0;
     if (jg > 0 && jg + 1 < G.ny && i0 + x < G.nx && R[F_D * RREG + s] > P.eps) {
-      Slopes q = cell_slopes(R[F_E * RREG + s - RX], R[F_V * RREG + s - RX],
-                             R[F_U * RREG + s - RX], R[F_SY * RREG + s - RX], R[F_E * RREG + s],
-                             R[F_V * RREG + s], R[F_U * RREG + s], R[F_SY * RREG + s],
-                             R[F_E * RREG + s + RX], R[F_V * RREG + s + RX],
-                             R[F_U * RREG + s + RX], R[F_SY * RREG + s + RX], P.h, SP);
+      Slopes q = cell_slopes(R_E(s - RX), R[F_V * RREG + s - RX],
+                             R[F_U * RREG + s - RX], R_SY(s - RX), R_E(s),
+                             R[F_V * RREG + s], R[F_U * RREG + s], R_SY(s),
+                             R_E(s + RX), R[F_V * RREG + s + RX],
+                             R[F_U * RREG + s + RX], R_SY(s + RX), P.h, SP);
       se = q.eta;
       su = q.un;
       st = q.ut;
@@ -1211,13 +1330,13 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
           Rr = L;
           if (wetA) {
             Slopes q = {SL[la], SL[NSL + la], SL[2 * NSL + la]};
-            L = side_from_slopes(R[F_E * RREG + sa], R[F_V * RREG + sa], R[F_U * RREG + sa],
-                                 R[F_SY * RREG + sa], bA, q, face_p, bf);
+            L = side_from_slopes(R_E(sa), R[F_V * RREG + sa], R[F_U * RREG + sa],
+                                 R_SY(sa), bA, q, face_p, bf);
           }
           if (wetB) {
             Slopes q = {SL[lb], SL[NSL + lb], SL[2 * NSL + lb]};
-            Rr = side_from_slopes(R[F_E * RREG + sa + RX], R[F_V * RREG + sa + RX],
-                                  R[F_U * RREG + sa + RX], R[F_SY * RREG + sa + RX], bB, q,
+            Rr = side_from_slopes(R_E(sa + RX), R[F_V * RREG + sa + RX],
+                                  R[F_U * RREG + sa + RX], R_SY(sa + RX), bB, q,
                                   face_m, bf);
           }
           rec = face_from_sides(wetA, wetB, L, Rr, P.g, SP);
@@ -1282,9 +1401,9 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
     double cx = 0.0, cy = 0.0;
     if (wet) {
       auto nb = [&](bool in, int q) {
-        return SNbr{in, R + F_D * RREG, R + F_E * RREG, R + F_U * RREG, R + F_V * RREG, q};
+        return NB_VIEW(in, q);
       };
-      double eta_c = R[F_E * RREG + s];
+      double eta_c = R_E(s);
       double gx = eta_grad_comp(nb(i > 0, s - 1), nb(i + 1 < G.nx, s + 1), eta_c, P, SP);
       double gy = eta_grad_comp(nb(jg > 0, s - RX), nb(jg + 1 < G.ny, s + RX), eta_c, P, SP);
       double gh = (P.g * d) * P.h;
@@ -1397,6 +1516,7 @@ __global__ void __launch_bounds__(STHR, SWF_STEP_MINB) k_step_redo(Geo G, StepAr
 }
 
 
+#if !SWF_STEP_SLIM  // the split kernels use the full region planes
 // ===========================================================================
 // Split step (-DSWF_SPLIT=1; measured and NOT the default): k_step's work in
 // two tile kernels, each with its own register and shared-memory budget (the
@@ -1419,9 +1539,6 @@ __global__ void __launch_bounds__(STHR, SWF_STEP_MINB) k_step_redo(Geo G, StepAr
 // (dry, no source), so its half-step view is its state: (H, 0, 0).
 // Same arithmetic, same order as step_tile: bit-identical results.
 // ===========================================================================
-#ifndef SWF_SPLIT
-#define SWF_SPLIT 0
-#endif
 #ifndef SWF_LAG_THREADS
 #define SWF_LAG_THREADS 256
 #endif
@@ -2089,6 +2206,8 @@ __global__ void __launch_bounds__(XTHR, SWF_FLUX_MINB) k_flux_redo(Geo G, StepAr
   }
 }
 
+#endif  // !SWF_STEP_SLIM
+
 // ---------------------------------------------------------------------------
 // Exact StepInfo volumes (final_update, stepper.cpp:676-701): the reference
 // sums the clamp deficit and the source volume per block in row-major cell
@@ -2555,6 +2674,7 @@ int fused_enqueue_phase2(swf_ctx* c, double dt_cap, double global_speed, const d
   for (int q = 0; q < c->taps.n; ++q)
     cudaMemsetAsync(c->taps.out[q], 0,
                     2 * (size_t)(c->taps.ni[q] + c->taps.nj[q]) * sizeof(double), c->stream);
+#if !SWF_STEP_SLIM
   if (nt > 0 && SWF_TILE_LISTS && SWF_SPLIT) {
     StepArgs SA = step_args(c);
     k_slist<<<(nt + 255) / 256, 256, 0, c->stream>>>(G, SA);
@@ -2564,7 +2684,9 @@ int fused_enqueue_phase2(swf_ctx* c, double dt_cap, double global_speed, const d
       k_ghost_half<<<(4 * G.nx + 127) / 128, 128, 0, c->stream>>>(G, SA);
     k_flux_list<<<c->sm_count * SWF_FLUX_MINB, XTHR, flux_smem(), c->stream>>>(G, SA);
     if (SWF_SPECULATE) k_flux_redo<<<RED_CTAS, XTHR, flux_smem(), c->stream>>>(G, SA);
-  } else {
+  } else
+#endif
+  {
     if (nt > 0 && SWF_TILE_LISTS) {
       StepArgs SA = step_args(c);
       k_slist<<<(nt + 255) / 256, 256, 0, c->stream>>>(G, SA);
@@ -2790,6 +2912,7 @@ int fused_prepare(swf_ctx* c) {
   if (e == cudaSuccess && !c->d_list_s) e = cudaMalloc(&c->d_list_s, nredo * sizeof(int));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_step, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+#if !SWF_STEP_SLIM
   // split step: its kernels' shared memory and the half-step view planes
   for (auto f : {(const void*)k_lag_list, (const void*)k_lag_redo}) {
     if (e == cudaSuccess)
@@ -2801,6 +2924,7 @@ int fused_prepare(swf_ctx* c) {
       e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)flux_smem());
     if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   }
+#endif
   if (e == cudaSuccess && SWF_SPLIT && !c->d_redo_l) e = cudaMalloc(&c->d_redo_l, nredo * sizeof(int));
   if (e == cudaSuccess && SWF_LAMBDA_SHARE && !c->d_lamn) {
     const size_t bytes = (local_cells(c) ? local_cells(c) : 1) * sizeof(double);
