@@ -404,7 +404,7 @@ void swf_destroy(swf_ctx* c) {
                   c->d_interior, c->d_halo, c->d_bflag, c->d_tile_act, c->d_tile_same,
                   c->d_tile_srcm, c->d_redo_f, c->d_redo_s, c->d_list_f, c->d_list_s,
                   c->d_part, c->d_sc, c->d_redo_l, c->d_half[0], c->d_half[1], c->d_half[2],
-                  c->d_xdef, c->d_xsrc, c->d_xbpart, c->d_xface, c->d_lamn};
+                  c->d_xdef, c->d_xsrc, c->d_xbpart, c->d_xface, c->d_lamn, c->d_gxy};
   for (void* p : ptrs) cudaFree(p);
   if (c->h_sc) cudaFreeHost(c->h_sc);
   for (auto& e : c->ev)

@@ -55,6 +55,9 @@ constexpr int STHR = SWF_STEP_THREADS;  // k_step (a multiple of 32)
 static_assert(STHR % 32 == 0, "k_step threads must be whole warps");
 constexpr int RED_CTAS = 148;
 constexpr int NPART_ALLOC = 5;  // doubles per tile in d_part (see k_reduce)
+#ifndef SWF_GRAD_SHARE  // k_step's mid forces hand the half-step eta gradient to its final update
+#define SWF_GRAD_SHARE 1
+#endif
 #ifndef SWF_LAMBDA_SHARE  // k_forces hands lambda(H_n, n) of the wet cells to k_step
 #define SWF_LAMBDA_SHARE 1
 #endif
@@ -701,6 +704,7 @@ struct StepArgs {
   const double* __restrict__ fpx;
   const double* __restrict__ fpy;
   const double* __restrict__ lamn;  // SWF_LAMBDA_SHARE (see ForcesArgs)
+  double* __restrict__ gxy;         // SWF_GRAD_SHARE: (gx, gy) per wet owned cell
   double* __restrict__ Ho;
   double* __restrict__ HUxo;
   double* __restrict__ HUyo;
@@ -1150,6 +1154,11 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
                                    nsrc > 0 ? sgm : 0.0, svx, svy, SP);
       fmx = o.fx - o.frx;
       fmy = o.fy - o.fry;
+      if (SWF_GRAD_SHARE) {  // the same half-step view gives phase 5's gradient
+        const size_t k2 = 2 * ((size_t)i + (size_t)r * nx);
+        A.gxy[k2] = o.gx;
+        A.gxy[k2 + 1] = o.gy;
+      }
     }
     double ht, qx, qy, sv;
     correct_cell(Hn, qxn, qyn, nsrc > 0, sgm, d, fmx, fmy, n, tau, P.eps, P.g, ht, qx, qy, sv,
@@ -1403,9 +1412,15 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
       auto nb = [&](bool in, int q) {
         return NB_VIEW(in, q);
       };
-      double eta_c = R_E(s);
-      double gx = eta_grad_comp(nb(i > 0, s - 1), nb(i + 1 < G.nx, s + 1), eta_c, P, SP);
-      double gy = eta_grad_comp(nb(jg > 0, s - RX), nb(jg + 1 < G.ny, s + RX), eta_c, P, SP);
+      double gx, gy;
+      if (SWF_GRAD_SHARE) {  // phase 2's mid forces computed it for this wet cell
+        gx = A.gxy[2 * k];
+        gy = A.gxy[2 * k + 1];
+      } else {
+        double eta_c = R_E(s);
+        gx = eta_grad_comp(nb(i > 0, s - 1), nb(i + 1 < G.nx, s + 1), eta_c, P, SP);
+        gy = eta_grad_comp(nb(jg > 0, s - RX), nb(jg + 1 < G.ny, s + RX), eta_c, P, SP);
+      }
       double gh = (P.g * d) * P.h;
       cx = gh * gx;
       cy = gh * gy;
@@ -2474,6 +2489,7 @@ StepArgs step_args(swf_ctx* c) {
   A.fpx = c->fpx;
   A.fpy = c->fpy;
   A.lamn = c->d_lamn;
+  A.gxy = c->d_gxy;
   A.Ho = c->H[nxt];
   A.HUxo = c->HUx[nxt];
   A.HUyo = c->HUy[nxt];
@@ -2926,6 +2942,11 @@ int fused_prepare(swf_ctx* c) {
   }
 #endif
   if (e == cudaSuccess && SWF_SPLIT && !c->d_redo_l) e = cudaMalloc(&c->d_redo_l, nredo * sizeof(int));
+  if (e == cudaSuccess && SWF_GRAD_SHARE && !c->d_gxy) {
+    const size_t bytes = 2 * (local_cells(c) ? local_cells(c) : 1) * sizeof(double);
+    e = cudaMalloc(&c->d_gxy, bytes);
+    if (e == cudaSuccess) e = cudaMemset(c->d_gxy, 0, bytes);
+  }
   if (e == cudaSuccess && SWF_LAMBDA_SHARE && !c->d_lamn) {
     const size_t bytes = (local_cells(c) ? local_cells(c) : 1) * sizeof(double);
     e = cudaMalloc(&c->d_lamn, bytes);

@@ -129,6 +129,7 @@ struct swf_ctx {
   double* fpx = nullptr;  // f_n.fx - f_n.fric_x (wet cells), fused path
   double* fpy = nullptr;
   double* d_lamn = nullptr;  // SWF_LAMBDA_SHARE builds: lambda(H_n, n) of the wet cells
+  double* d_gxy = nullptr;   // SWF_GRAD_SHARE builds: k_step's half-step eta gradients
   // sources / wind
   std::vector<swf::DevSrc> h_src;
   std::vector<double> h_ht, h_hq;
