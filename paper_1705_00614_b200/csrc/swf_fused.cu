@@ -55,6 +55,15 @@ constexpr int STHR = SWF_STEP_THREADS;  // k_step (a multiple of 32)
 static_assert(STHR % 32 == 0, "k_step threads must be whole warps");
 constexpr int RED_CTAS = 148;
 constexpr int NPART_ALLOC = 5;  // doubles per tile in d_part (see k_reduce)
+#ifndef SWF_PHASE_UNROLL  // unroll factor of k_step's region / slope / face loops (1: rolled)
+#define SWF_PHASE_UNROLL 1
+#endif
+#define SWF_PRAGMA_(x) _Pragma(#x)
+#define SWF_UNROLL_(n) SWF_PRAGMA_(unroll n)
+#define SWF_PHASE_LOOP SWF_UNROLL_(SWF_PHASE_UNROLL)
+#ifndef SWF_P2_ROLLED  // k_step phase 2 as a rolled loop, the Lagrangian state parked in the output buffers
+#define SWF_P2_ROLLED 1
+#endif
 #ifndef SWF_GRAD_SHARE  // k_step's mid forces hand the half-step eta gradient to its final update
 #define SWF_GRAD_SHARE 1
 #endif
@@ -947,6 +956,7 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
   // in the face planes, which phase 4x writes only after phase 2 is done
   double* LAM = FB;
   static_assert(BX * BY <= 4 * NFC, "lambda plane");
+  SWF_PHASE_LOOP
   for (int c = tid; c < RREG; c += STHR) {
     int i = i0 - 2 + c % RX, r = r0 - 2 + c / RX;
     double h = 0.0, mx = 0.0, my = 0.0, bb = 0.0;
@@ -966,6 +976,7 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
 
   PHASE_MARK(0);
   // ---- phase 1b: half-step view on the region (K4 predictor, HalfView) -----
+  SWF_PHASE_LOOP
   for (int c = tid; c < RREG; c += STHR) {
     int xr = c % RX, yr = c / RX;
     int i = i0 - 2 + xr, r = r0 - 2 + yr;
@@ -1099,9 +1110,31 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
   constexpr int PER = (BX * BY + STHR - 1) / STHR;  // owned cells per thread (2 at 256)
   // (Ht, Qx, Qy) end up as the final update's base state: the Lagrangian
   // state for active cells, the step-start state otherwise (stepper.cpp:641-651)
+#if SWF_P2_ROLLED
+  // one copy of the phase's code: the base state goes to the output buffers
+  // (phase 5 reads it back and overwrites it; an exact redo re-parks it)
+#define PARK(m, h, qx_, qy_)                                   \
+  do {                                                         \
+    if (i < G.nx && r < G.r1) {                                \
+      const size_t kp = (size_t)i + (size_t)r * nx;            \
+      A.Ho[kp] = (h);                                          \
+      A.HUxo[kp] = (qx_);                                      \
+      A.HUyo[kp] = (qy_);                                      \
+    }                                                          \
+  } while (0)
+  double srcvol = 0.0;
+#pragma unroll 1
+#else
+#define PARK(m, h, qx_, qy_) \
+  do {                       \
+    Ht[m] = (h);             \
+    Qx[m] = (qx_);           \
+    Qy[m] = (qy_);           \
+  } while (0)
   double Ht[PER], Qx[PER], Qy[PER];
   double srcvol = 0.0;
 #pragma unroll
+#endif
   for (int m = 0; m < PER; ++m) {
     int c = tid + m * STHR;
     if (BX * BY % STHR && c >= BX * BY) break;
@@ -1118,9 +1151,6 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
 #else
     double Hn = OWN[c], qxn = OWN[BX * BY + c], qyn = OWN[2 * BX * BY + c];
 #endif
-    Ht[m] = Hn;
-    Qx[m] = qxn;
-    Qy[m] = qyn;
     if (i >= G.nx || r >= G.r1) continue;
     int s = (x + 2) + (y + 2) * RX;
     int jg = G.jg0 + r;
@@ -1130,7 +1160,10 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
       sgm = msig(G, A.src, sig_m, srcm, i, jg);
     }
     bool act = Hn > P.eps || sgn_ != 0.0;
-    if (!act) continue;
+    if (!act) {
+      PARK(m, Hn, qxn, qyn);  // the step-start state is the base
+      continue;
+    }
 #if SWF_STEP_SLIM
     double n = G.has_nfield ? A.nf[(size_t)i + (size_t)r * nx] : G.n_manning;
 #else
@@ -1176,13 +1209,13 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
       unsigned long long key = (ERR_CFL << 58) | ((unsigned long long)ib << 24) | local;
       my_err = key < my_err ? key : my_err;
     }
-    Ht[m] = ht;
-    Qx[m] = qx;
-    Qy[m] = qy;
+    PARK(m, ht, qx, qy);
   }
+#undef PARK
 
   PHASE_MARK(2);
   // ---- phase 3x: x slopes of columns -1..BX (rows of the tile) -------------
+  SWF_PHASE_LOOP
   for (int c = tid; c < (BX + 2) * BY; c += STHR) {
     int xx = c % (BX + 2), y = c / (BX + 2);
     int i = i0 - 1 + xx;
@@ -1208,6 +1241,7 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
   // ---- phase 4x: x faces (stepper.cpp:402-447, 496-516) ----------------------
   double outflow = 0.0;
   const double face_p = (1.0 * 0.5) * P.h, face_m = (-1.0 * 0.5) * P.h;
+  SWF_PHASE_LOOP
   for (int c = tid; c < (BX + 1) * BY; c += STHR) {
     int fx = c % (BX + 1), y = c / (BX + 1);
     int f = i0 + fx, r = r0 + y;
@@ -1287,6 +1321,7 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
 
   PHASE_MARK(4);
   // ---- phase 3y: y slopes of rows -1..BY (columns of the tile) -------------
+  SWF_PHASE_LOOP
   for (int c = tid; c < BX * (BY + 2); c += STHR) {
     int x = c % BX, yy = c / BX;
     int r = r0 - 1 + yy, jg = G.jg0 + r;
@@ -1310,6 +1345,7 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
 
   PHASE_MARK(5);
   // ---- phase 4y: y faces (stepper.cpp:449-494, 518-538) ----------------------
+  SWF_PHASE_LOOP
   for (int c = tid; c < BX * (BY + 1); c += STHR) {
     int x = c % BX, fy = c / BX;
     int i = i0 + x, rf = r0 + fy;  // face between local rows rf-1 and rf
@@ -1394,11 +1430,16 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
     unsigned char bfl = bf_staged ? s_bf[(bc - bi_lo) + (br - bj_lo) * nbi]
                                   : A.bflag[bc + (br - G.bj0) * G.nbx];
     bool flux_on = !G.skip || (bfl & 2);
+#if SWF_P2_ROLLED
+    const double Htm = A.Ho[k], Qxm = A.HUxo[k], Qym = A.HUyo[k];  // parked in phase 2
+#else
+    const double Htm = Ht[m], Qxm = Qx[m], Qym = Qy[m];
+#endif
     if (!flux_on) {  // block skipped by the reference: state unchanged
-      A.Ho[k] = Ht[m];  // no active cell in such a block: (Ht, Qx, Qy) = step-start state
-      A.HUxo[k] = Qx[m];
-      A.HUyo[k] = Qy[m];
-      peer_store(G, A, i, r, Ht[m], Qx[m], Qy[m]);
+      A.Ho[k] = Htm;  // no active cell in such a block: (Ht, Qx, Qy) = step-start state
+      A.HUxo[k] = Qxm;
+      A.HUyo[k] = Qym;
+      peer_store(G, A, i, r, Htm, Qxm, Qym);
       continue;
     }
     int sf = x + y * BX, nf_ = sf + BX;  // S and N face of the cell
@@ -1429,7 +1470,7 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
     double Fvx = (px_a[m] + py_c) + cx;
     double Fvy = (py_a + px_c[m]) + cy;
     double H1, qx, qy, dfc;
-    final_cell(Ht[m], Qx[m], Qy[m], Fh, Fvx, Fvy, dt_h, P.eps, H1, qx, qy, dfc);
+    final_cell(Htm, Qxm, Qym, Fh, Fvx, Fvy, dt_h, P.eps, H1, qx, qy, dfc);
     deficit += dfc;
     dfm[m] = dfc;
     A.Ho[k] = H1;
