@@ -1214,202 +1214,163 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
 #undef PARK
 
   PHASE_MARK(2);
-  // ---- phase 3x: x slopes of columns -1..BX (rows of the tile) -------------
-  SWF_PHASE_LOOP
-  for (int c = tid; c < (BX + 2) * BY; c += STHR) {
-    int xx = c % (BX + 2), y = c / (BX + 2);
-    int i = i0 - 1 + xx;
-    int s = (xx + 1) + (y + 2) * RX;
-    double se = 0.0, su = 0.0, st = 0.0;
-    if (i > 0 && i + 1 < G.nx && R[F_D * RREG + s] > P.eps) {
-      Slopes q = cell_slopes(R_E(s - 1), R[F_U * RREG + s - 1], R[F_V * RREG + s - 1],
-                             R_SX(s - 1), R_E(s), R[F_U * RREG + s],
-                             R[F_V * RREG + s], R_SX(s), R_E(s + 1),
-                             R[F_U * RREG + s + 1], R[F_V * RREG + s + 1], R_SX(s + 1),
-                             P.h, SP);
-      se = q.eta;
-      su = q.un;
-      st = q.ut;
-    }
-    SL[0 * NSL + c] = se;
-    SL[1 * NSL + c] = su;
-    SL[2 * NSL + c] = st;
-  }
-  __syncthreads();
-
-  PHASE_MARK(3);
-  // ---- phase 4x: x faces (stepper.cpp:402-447, 496-516) ----------------------
+  // ---- phases 3 and 4, x then y: one copy of the slope and face code -------
+  // (the two directions differ only in their index maps and in which
+  // velocity is normal; a rolled loop keeps k_step's code -- and its
+  // instruction-cache footprint -- to one copy)
   double outflow = 0.0;
   const double face_p = (1.0 * 0.5) * P.h, face_m = (-1.0 * 0.5) * P.h;
-  SWF_PHASE_LOOP
-  for (int c = tid; c < (BX + 1) * BY; c += STHR) {
-    int fx = c % (BX + 1), y = c / (BX + 1);
-    int f = i0 + fx, r = r0 + y;
-    FaceRec rec;
-    rec.fm = rec.fnl = rec.fnr = rec.ft = 0.0;
-    if (f <= G.nx && r < G.r1) {
-      int jg = G.jg0 + r;
-      int sa = (fx + 1) + (y + 2) * RX;  // cell f-1
-      if (f == 0 || f == G.nx) {
-        bool lo = f == 0;
-        int se = lo ? sa + 1 : sa;
-        double H = R[F_D * RREG + se];
-        bool wet = H > P.eps;
-        rec = boundary_face(wet, H, R[F_U * RREG + se], R[F_V * RREG + se], lo,
-                            lo ? G.west_refl : G.east_refl, P.g);
-        outflow += lo ? -rec.fm : rec.fm;
-        if (A.xface) A.xface[(lo ? 0 : G.ny) + jg] = rec.fm;  // W/E edge faces, by row
-      } else {
-        int la = fx + y * (BX + 2), lb = la + 1;  // slope slots of cells f-1, f
-        double dA = R[F_D * RREG + sa], dB = R[F_D * RREG + sa + 1];
-        bool wetA = dA > P.eps, wetB = dB > P.eps;
-        if (wetA || wetB) {
-          double bA = R[F_B * RREG + sa], bB = R[F_B * RREG + sa + 1];
-          double bf = smax(bA, bB);
-          SideState L, Rr;
-          L.hs = L.hcell = L.un = L.ut = 0.0;
-          Rr = L;
-          if (wetA) {
-            Slopes q = {SL[la], SL[NSL + la], SL[2 * NSL + la]};
-            L = side_from_slopes(R_E(sa), R[F_U * RREG + sa], R[F_V * RREG + sa],
-                                 R_SX(sa), bA, q, face_p, bf);
-          }
-          if (wetB) {
-            Slopes q = {SL[lb], SL[NSL + lb], SL[2 * NSL + lb]};
-            Rr = side_from_slopes(R_E(sa + 1), R[F_U * RREG + sa + 1],
-                                  R[F_V * RREG + sa + 1], R_SX(sa + 1), bB, q, face_m,
-                                  bf);
-          }
-          rec = face_from_sides(wetA, wetB, L, Rr, P.g, SP);
-          if (!face_finite(rec)) {
-            unsigned long long key = fused_flux_key(G, A.bflag, 0, jg, f);
-            my_err = key < my_err ? key : my_err;
-          }
-        }
-      }
-    }
-    FB[0 * NFC + c] = rec.fm;
-    FB[1 * NFC + c] = rec.fnl;
-    FB[2 * NFC + c] = rec.fnr;
-    FB[3 * NFC + c] = rec.ft;
-  }
-  __syncthreads();
-  // face taps (nested-grid flux correction): each tile records its west
-  // faces only (fx < BX), so every face is written once; faces no active
-  // tile computes stay 0 (dry)
-  if (A.taps.n) {
-    for (int c = tid; c < (BX + 1) * BY; c += STHR) {
-      const int fx = c % (BX + 1), y = c / (BX + 1), f = i0 + fx, jg = G.jg0 + r0 + y;
-      for (int q = 0; q < A.taps.n; ++q)
-        if (fx < BX && r0 + y < G.r1 && (f == A.taps.i0[q] || f == A.taps.i0[q] + A.taps.ni[q]) &&
-            jg >= A.taps.j0[q] && jg < A.taps.j0[q] + A.taps.nj[q])
-          A.taps.out[q][(f == A.taps.i0[q] ? 0 : A.taps.nj[q]) + (jg - A.taps.j0[q])] =
-              tau * FB[0 * NFC + c];
-    }
-  }
   double px_m[PER], px_a[PER], px_c[PER];  // (W.fm-E.fm), (W.fnr-E.fnl), (W.ft-E.ft)
-#pragma unroll
-  for (int m = 0; m < PER; ++m) {
-    int c = tid + m * STHR;
-    if (BX * BY % STHR && c >= BX * BY) break;
-    int x = c % BX, y = c / BX;
-    int w = x + y * (BX + 1), e = w + 1;
-    px_m[m] = FB[0 * NFC + w] - FB[0 * NFC + e];
-    px_a[m] = FB[2 * NFC + w] - FB[1 * NFC + e];
-    px_c[m] = FB[3 * NFC + w] - FB[3 * NFC + e];
-  }
-
-  PHASE_MARK(4);
-  // ---- phase 3y: y slopes of rows -1..BY (columns of the tile) -------------
-  SWF_PHASE_LOOP
-  for (int c = tid; c < BX * (BY + 2); c += STHR) {
-    int x = c % BX, yy = c / BX;
-    int r = r0 - 1 + yy, jg = G.jg0 + r;
-    int s = (x + 2) + (yy + 1) * RX;
-    double se = 0.0, su = 0.0, st = 0.0;
-    if (jg > 0 && jg + 1 < G.ny && i0 + x < G.nx && R[F_D * RREG + s] > P.eps) {
-      Slopes q = cell_slopes(R_E(s - RX), R[F_V * RREG + s - RX],
-                             R[F_U * RREG + s - RX], R_SY(s - RX), R_E(s),
-                             R[F_V * RREG + s], R[F_U * RREG + s], R_SY(s),
-                             R_E(s + RX), R[F_V * RREG + s + RX],
-                             R[F_U * RREG + s + RX], R_SY(s + RX), P.h, SP);
-      se = q.eta;
-      su = q.un;
-      st = q.ut;
-    }
-    SL[0 * NSL + c] = se;
-    SL[1 * NSL + c] = su;
-    SL[2 * NSL + c] = st;
-  }
-  __syncthreads();
-
-  PHASE_MARK(5);
-  // ---- phase 4y: y faces (stepper.cpp:449-494, 518-538) ----------------------
-  SWF_PHASE_LOOP
-  for (int c = tid; c < BX * (BY + 1); c += STHR) {
-    int x = c % BX, fy = c / BX;
-    int i = i0 + x, rf = r0 + fy;  // face between local rows rf-1 and rf
-    int jf = G.jg0 + rf;           // global face index
-    FaceRec rec;
-    rec.fm = rec.fnl = rec.fnr = rec.ft = 0.0;
-    if (i < G.nx && rf <= G.r1) {
-      int sa = (x + 2) + (fy + 1) * RX;  // cell rf-1
-      if (jf == 0 || jf == G.ny) {
-        bool lo = jf == 0;
-        int se = lo ? sa + RX : sa;
-        double H = R[F_D * RREG + se];
-        bool wet = H > P.eps;
-        rec = boundary_face(wet, H, R[F_V * RREG + se], R[F_U * RREG + se], lo,
-                            lo ? G.south_refl : G.north_refl, P.g);
-        outflow += lo ? -rec.fm : rec.fm;
-        if (A.xface) A.xface[2 * G.ny + (lo ? 0 : G.nx) + i] = rec.fm;  // S/N edge faces
+#pragma unroll 1
+  for (int dir = 0; dir < 2; ++dir) {
+    const double* UN = R + (dir == 0 ? F_U : F_V) * RREG;  // normal velocity
+    const double* UT = R + (dir == 0 ? F_V : F_U) * RREG;  // tangential
+    const int ds = dir == 0 ? 1 : RX;                        // the next cell along the normal
+    // shift along the normal: 0.5*dr (stepper.cpp:72-73)
+    auto SH = [&](int q) { return dir == 0 ? R_SX(q) : R_SY(q); };
+    // slopes of the cells -1..B of every line of the tile
+    const int nsl = dir == 0 ? (BX + 2) * BY : BX * (BY + 2);
+    SWF_PHASE_LOOP
+    for (int c = tid; c < nsl; c += STHR) {
+      int s;
+      bool inside;
+      if (dir == 0) {
+        const int xx = c % (BX + 2), y = c / (BX + 2), i = i0 - 1 + xx;
+        s = (xx + 1) + (y + 2) * RX;
+        inside = i > 0 && i + 1 < G.nx;
       } else {
-        int la = x + fy * BX, lb = la + BX;  // slope slots of rows rf-1, rf
-        double dA = R[F_D * RREG + sa], dB = R[F_D * RREG + sa + RX];
-        bool wetA = dA > P.eps, wetB = dB > P.eps;
-        if (wetA || wetB) {
-          double bA = R[F_B * RREG + sa], bB = R[F_B * RREG + sa + RX];
-          double bf = smax(bA, bB);
-          SideState L, Rr;
-          L.hs = L.hcell = L.un = L.ut = 0.0;
-          Rr = L;
-          if (wetA) {
-            Slopes q = {SL[la], SL[NSL + la], SL[2 * NSL + la]};
-            L = side_from_slopes(R_E(sa), R[F_V * RREG + sa], R[F_U * RREG + sa],
-                                 R_SY(sa), bA, q, face_p, bf);
-          }
-          if (wetB) {
-            Slopes q = {SL[lb], SL[NSL + lb], SL[2 * NSL + lb]};
-            Rr = side_from_slopes(R_E(sa + RX), R[F_V * RREG + sa + RX],
-                                  R[F_U * RREG + sa + RX], R_SY(sa + RX), bB, q,
-                                  face_m, bf);
-          }
-          rec = face_from_sides(wetA, wetB, L, Rr, P.g, SP);
-          if (!face_finite(rec)) {
-            unsigned long long key = fused_flux_key(G, A.bflag, 1, i, jf);
-            my_err = key < my_err ? key : my_err;
+        const int x = c % BX, yy = c / BX, jg = G.jg0 + r0 - 1 + yy;
+        s = (x + 2) + (yy + 1) * RX;
+        inside = jg > 0 && jg + 1 < G.ny && i0 + x < G.nx;
+      }
+      double se = 0.0, su = 0.0, st = 0.0;
+      if (inside && R[F_D * RREG + s] > P.eps) {
+        Slopes q = cell_slopes(R_E(s - ds), UN[s - ds], UT[s - ds], SH(s - ds), R_E(s), UN[s],
+                               UT[s], SH(s), R_E(s + ds), UN[s + ds], UT[s + ds], SH(s + ds),
+                               P.h, SP);
+        se = q.eta;
+        su = q.un;
+        st = q.ut;
+      }
+      SL[0 * NSL + c] = se;
+      SL[1 * NSL + c] = su;
+      SL[2 * NSL + c] = st;
+    }
+    __syncthreads();
+
+    // faces (stepper.cpp:402-494, 496-538)
+    const int nfc = dir == 0 ? (BX + 1) * BY : BX * (BY + 1);
+    SWF_PHASE_LOOP
+    for (int c = tid; c < nfc; c += STHR) {
+      // f: the face index along the normal (global), line: the cell line
+      // across it (global row of an x face, column of a y face)
+      int f, line, sa, la, lb;
+      bool valid, edge_lo, edge_hi;
+      if (dir == 0) {
+        const int fx = c % (BX + 1), y = c / (BX + 1), r = r0 + y;
+        f = i0 + fx;
+        line = G.jg0 + r;
+        valid = f <= G.nx && r < G.r1;
+        edge_lo = f == 0;
+        edge_hi = f == G.nx;
+        sa = (fx + 1) + (y + 2) * RX;  // cell f-1
+        la = fx + y * (BX + 2);        // slope slots of cells f-1, f
+        lb = la + 1;
+      } else {
+        const int x = c % BX, fy = c / BX, rf = r0 + fy;
+        f = G.jg0 + rf;
+        line = i0 + x;
+        valid = line < G.nx && rf <= G.r1;
+        edge_lo = f == 0;
+        edge_hi = f == G.ny;
+        sa = (x + 2) + (fy + 1) * RX;  // cell rf-1
+        la = x + fy * BX;              // slope slots of rows rf-1, rf
+        lb = la + BX;
+      }
+      FaceRec rec;
+      rec.fm = rec.fnl = rec.fnr = rec.ft = 0.0;
+      if (valid) {
+        if (edge_lo || edge_hi) {
+          const bool lo = edge_lo;
+          const int se = lo ? sa + ds : sa;
+          const double H = R[F_D * RREG + se];
+          const bool refl = dir == 0 ? (lo ? G.west_refl : G.east_refl)
+                                     : (lo ? G.south_refl : G.north_refl);
+          rec = boundary_face(H > P.eps, H, UN[se], UT[se], lo, refl, P.g);
+          outflow += lo ? -rec.fm : rec.fm;
+          if (A.xface)  // the edge faces in the exact-volume order (W, E by row; S, N by column)
+            A.xface[(dir == 0 ? 0 : 2 * G.ny) + (lo ? 0 : (dir == 0 ? G.ny : G.nx)) + line] =
+                rec.fm;
+        } else {
+          const int sb = sa + ds;
+          double dA = R[F_D * RREG + sa], dB = R[F_D * RREG + sb];
+          bool wetA = dA > P.eps, wetB = dB > P.eps;
+          if (wetA || wetB) {
+            double bA = R[F_B * RREG + sa], bB = R[F_B * RREG + sb];
+            double bf = smax(bA, bB);
+            SideState L, Rr;
+            L.hs = L.hcell = L.un = L.ut = 0.0;
+            Rr = L;
+            if (wetA) {
+              Slopes q = {SL[la], SL[NSL + la], SL[2 * NSL + la]};
+              L = side_from_slopes(R_E(sa), UN[sa], UT[sa], SH(sa), bA, q, face_p, bf);
+            }
+            if (wetB) {
+              Slopes q = {SL[lb], SL[NSL + lb], SL[2 * NSL + lb]};
+              Rr = side_from_slopes(R_E(sb), UN[sb], UT[sb], SH(sb), bB, q, face_m, bf);
+            }
+            rec = face_from_sides(wetA, wetB, L, Rr, P.g, SP);
+            if (!face_finite(rec)) {
+              unsigned long long key = fused_flux_key(G, A.bflag, dir, line, f);
+              my_err = key < my_err ? key : my_err;
+            }
           }
         }
       }
+      FB[0 * NFC + c] = rec.fm;
+      FB[1 * NFC + c] = rec.fnl;
+      FB[2 * NFC + c] = rec.fnr;
+      FB[3 * NFC + c] = rec.ft;
     }
-    FB[0 * NFC + c] = rec.fm;
-    FB[1 * NFC + c] = rec.fnl;
-    FB[2 * NFC + c] = rec.fnr;
-    FB[3 * NFC + c] = rec.ft;
-  }
-  __syncthreads();
-  if (A.taps.n) {
-    for (int c = tid; c < BX * (BY + 1); c += STHR) {
-      const int x = c % BX, fy = c / BX, i = i0 + x, rf = r0 + fy, jf = G.jg0 + rf;
-      for (int q = 0; q < A.taps.n; ++q)
-        if (fy < BY && i < G.nx && rf < G.r1 &&
-            (jf == A.taps.j0[q] || jf == A.taps.j0[q] + A.taps.nj[q]) && i >= A.taps.i0[q] &&
-            i < A.taps.i0[q] + A.taps.ni[q])
-          A.taps.out[q][2 * A.taps.nj[q] + (jf == A.taps.j0[q] ? 0 : A.taps.ni[q]) +
-                        (i - A.taps.i0[q])] = tau * FB[0 * NFC + c];
+    __syncthreads();
+    // face taps (nested-grid flux correction): each tile records its west /
+    // south faces only, so every face is written once; faces no active tile
+    // computes stay 0 (dry)
+    if (A.taps.n) {
+      for (int c = tid; c < nfc; c += STHR) {
+        if (dir == 0) {
+          const int fx = c % (BX + 1), y = c / (BX + 1), f = i0 + fx, jg = G.jg0 + r0 + y;
+          for (int q = 0; q < A.taps.n; ++q)
+            if (fx < BX && r0 + y < G.r1 &&
+                (f == A.taps.i0[q] || f == A.taps.i0[q] + A.taps.ni[q]) &&
+                jg >= A.taps.j0[q] && jg < A.taps.j0[q] + A.taps.nj[q])
+              A.taps.out[q][(f == A.taps.i0[q] ? 0 : A.taps.nj[q]) + (jg - A.taps.j0[q])] =
+                  tau * FB[0 * NFC + c];
+        } else {
+          const int x = c % BX, fy = c / BX, i = i0 + x, rf = r0 + fy, jf = G.jg0 + rf;
+          for (int q = 0; q < A.taps.n; ++q)
+            if (fy < BY && i < G.nx && rf < G.r1 &&
+                (jf == A.taps.j0[q] || jf == A.taps.j0[q] + A.taps.nj[q]) &&
+                i >= A.taps.i0[q] && i < A.taps.i0[q] + A.taps.ni[q])
+              A.taps.out[q][2 * A.taps.nj[q] + (jf == A.taps.j0[q] ? 0 : A.taps.ni[q]) +
+                            (i - A.taps.i0[q])] = tau * FB[0 * NFC + c];
+        }
+      }
+    }
+    if (dir == 0) {  // the x faces' contributions, before the y faces take the planes
+#pragma unroll
+      for (int m = 0; m < PER; ++m) {
+        int c = tid + m * STHR;
+        if (BX * BY % STHR && c >= BX * BY) break;
+        int x = c % BX, y = c / BX;
+        int w = x + y * (BX + 1), e = w + 1;
+        px_m[m] = FB[0 * NFC + w] - FB[0 * NFC + e];
+        px_a[m] = FB[2 * NFC + w] - FB[1 * NFC + e];
+        px_c[m] = FB[3 * NFC + w] - FB[3 * NFC + e];
+      }
+      // (the y slopes write only SL; FB is rewritten after the next barrier)
     }
   }
-
   PHASE_MARK(6);
   // ---- phase 5: accumulate (stepper.cpp:540-566) + final (628-659) ---------
   double deficit = 0.0;
