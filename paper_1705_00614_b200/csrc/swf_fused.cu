@@ -956,32 +956,25 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
   // in the face planes, which phase 4x writes only after phase 2 is done
   double* LAM = FB;
   static_assert(BX * BY <= 4 * NFC, "lambda plane");
-  SWF_PHASE_LOOP
-  for (int c = tid; c < RREG; c += STHR) {
-    int i = i0 - 2 + c % RX, r = r0 - 2 + c / RX;
-    double h = 0.0, mx = 0.0, my = 0.0, bb = 0.0;
-    if (i >= 0 && i < G.nx && r >= 0 && r < G.rows) {
-      size_t k = (size_t)i + (size_t)r * nx;
-      h = A.H[k];
-      mx = A.HUx[k];
-      my = A.HUy[k];
-      bb = A.b[k];
-    }
-    R[F_D * RREG + c] = h;
-    R[F_U * RREG + c] = mx;
-    R[F_V * RREG + c] = my;
-    R[F_B * RREG + c] = bb;
-  }
-  __syncthreads();
 
   PHASE_MARK(0);
-  // ---- phase 1b: half-step view on the region (K4 predictor, HalfView) -----
+  // ---- phase 1: region inputs and the half-step view (K4 predictor, HalfView)
+  // (each thread loads its cells' inputs here: the predictor of a cell needs
+  // that cell only, so loads and predictor share one pass and no barrier)
   SWF_PHASE_LOOP
   for (int c = tid; c < RREG; c += STHR) {
     int xr = c % RX, yr = c / RX;
     int i = i0 - 2 + xr, r = r0 - 2 + yr;
     double d = 0.0, u = 0.0, v = 0.0;
-    double Hn = R[F_D * RREG + c], mx = R[F_U * RREG + c], my = R[F_V * RREG + c];
+    double Hn = 0.0, mx = 0.0, my = 0.0, bb = 0.0;
+    if (i >= 0 && i < G.nx && r >= 0 && r < G.rows) {
+      size_t k = (size_t)i + (size_t)r * nx;
+      Hn = A.H[k];
+      mx = A.HUx[k];
+      my = A.HUy[k];
+      bb = A.b[k];
+    }
+    R[F_B * RREG + c] = bb;
     const bool owned = xr >= 2 && xr < BX + 2 && yr >= 2 && yr < BY + 2;
     const int o = (xr - 2) + (yr - 2) * BX;
     double lam = -1.0;
