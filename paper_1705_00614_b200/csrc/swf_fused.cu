@@ -61,6 +61,12 @@ constexpr int NPART_ALLOC = 5;  // doubles per tile in d_part (see k_reduce)
 #define SWF_PRAGMA_(x) _Pragma(#x)
 #define SWF_UNROLL_(n) SWF_PRAGMA_(unroll n)
 #define SWF_PHASE_LOOP SWF_UNROLL_(SWF_PHASE_UNROLL)
+#ifndef SWF_EPI_ONEBAR  // k_step epilogue: the partials' barrier is the acceptance barrier
+#define SWF_EPI_ONEBAR 1
+#endif
+#ifndef SWF_OWN_FB  // slim k_step: the owned cells' step-start state kept in the face planes for phase 2
+#define SWF_OWN_FB 1
+#endif
 #ifndef SWF_P2_ROLLED  // k_step phase 2 as a rolled loop, the Lagrangian state parked in the output buffers
 #define SWF_P2_ROLLED 1
 #endif
@@ -955,7 +961,7 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
   // lambda(H12, n) of the owned cells as the predictor evaluated it (or -1),
   // in the face planes, which phase 4x writes only after phase 2 is done
   double* LAM = FB;
-  static_assert(BX * BY <= 4 * NFC, "lambda plane");
+  static_assert(4 * BX * BY <= 4 * NFC, "lambda plane + the owned step-start state (SWF_OWN_FB)");
 
   PHASE_MARK(0);
   // ---- phase 1: region inputs and the half-step view (K4 predictor, HalfView)
@@ -977,6 +983,11 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
     R[F_B * RREG + c] = bb;
     const bool owned = xr >= 2 && xr < BX + 2 && yr >= 2 && yr < BY + 2;
     const int o = (xr - 2) + (yr - 2) * BX;
+    if (SWF_OWN_FB && owned) {  // the step-start state, for phase 2 (FB is free until 4x)
+      FB[BX * BY + o] = Hn;
+      FB[2 * BX * BY + o] = mx;
+      FB[3 * BX * BY + o] = my;
+    }
     double lam = -1.0;
     if (i >= 0 && i < G.nx && r >= 0 && r < G.rows) {
       const size_t k = (size_t)i + (size_t)r * nx;
@@ -1135,7 +1146,11 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
     int i = i0 + x, r = r0 + y;
 #if SWF_STEP_SLIM
     double Hn = 0.0, qxn = 0.0, qyn = 0.0;
-    if (i < G.nx && r < G.r1) {
+    if (SWF_OWN_FB) {
+      Hn = FB[BX * BY + c];
+      qxn = FB[2 * BX * BY + c];
+      qyn = FB[3 * BX * BY + c];
+    } else if (i < G.nx && r < G.r1) {
       const size_t k0 = (size_t)i + (size_t)r * nx;
       Hn = A.H[k0];
       qxn = A.HUx[k0];
@@ -1453,15 +1468,24 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     if ((tid & 31) == 0) s_red[q][tid >> 5] = v;
   }
+#if !SWF_EPI_ONEBAR
   __syncthreads();
   if (tid < 3) {
     double v = 0.0;
     for (int w = 0; w < STHR / 32; ++w) v += s_red[tid][w];
     A.part[5 * (size_t)tile + tid] = v;
   }
+#endif
   // a tile with a rejected speculative division is redone exactly (its
   // outputs and partials are overwritten there); otherwise publish errors
   const bool any_bad = __syncthreads_or(!sok);
+#if SWF_EPI_ONEBAR
+  if (tid < 3) {  // (the barrier above also orders the s_red writes)
+    double v = 0.0;
+    for (int w = 0; w < STHR / 32; ++w) v += s_red[tid][w];
+    A.part[5 * (size_t)tile + tid] = v;
+  }
+#endif
   const bool redo = SPEC && any_bad;
   if (redo) {
     if (tid == 0) A.redo[atomicAdd(&sc->redo_n[1], 1)] = tile;
