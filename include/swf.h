@@ -161,6 +161,9 @@ int swf_step_host(swf_ctx* ctx, double* H, double* HUx, double* HUy,
  * zero-copy ingest; afterwards the resident calls need swf_upload_state);
  * otherwise the three full fields. */
 int swf_last_ingest_bytes(const swf_ctx* ctx, long long* bytes);
+/* Host bytes the last synchronised pinned host-buffer step wrote back (the
+ * updated cells of its flux-on blocks, counted on the device). */
+int swf_last_writeback_bytes(swf_ctx* ctx, long long* bytes);
 /* Opt-in host mirror for swf_step_host on PINNED arrays (SURVEY.md §8b,
  * "Ownership"; off by default).  On: after a host step the device keeps
  * the state it wrote into the caller's arrays, and the next host step with

@@ -73,6 +73,7 @@ def declare(lib):
     _sig(lib, "swf_strip_pack", I, P, I, C.c_void_p)
     _sig(lib, "swf_strip_unpack", I, P, I, C.c_void_p)
     _sig(lib, "swf_last_ingest_bytes", I, P, C.POINTER(C.c_longlong))
+    _sig(lib, "swf_last_writeback_bytes", I, P, C.POINTER(C.c_longlong))
     _sig(lib, "swf_set_host_mirror", I, P, I)
     _sig(lib, "swf_build_flavor", C.c_char_p)
     _sig(lib, "swf_host_changed", I, P)

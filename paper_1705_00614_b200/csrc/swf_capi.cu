@@ -736,6 +736,12 @@ int swf_step_host(swf_ctx* c, double* H, double* HUx, double* HUy, double* t, do
 
 const char* swf_build_flavor(void) { return SWF_FAST ? "fast" : "exact"; }
 
+int swf_last_writeback_bytes(swf_ctx* c, long long* bytes) {
+  if (!c || !bytes) return SWF_ECONFIG;
+  *bytes = 8LL * (long long)c->h_sc->host_writes;
+  return SWF_OK;
+}
+
 int swf_set_host_mirror(swf_ctx* c, int on) {
   if (!c) return SWF_ECONFIG;
   c->host_mirror = on ? 1 : 0;

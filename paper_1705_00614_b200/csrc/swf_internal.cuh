@@ -53,6 +53,7 @@ struct StepScalars {
   double deficit, srcvol, outflow;  // this step's diagnostics (volumes)
   double speed_local;               // strips: local max speed (phase 1 out)
   double dt_cap_dev;                // dt_cap of a step enqueued with dt_cap < 0 (k_tau)
+  unsigned long long host_writes;   // doubles a host-buffer step wrote back (changed values only)
   int mask_valid;  // the tile flags of the previous step describe the current state
   int mask_fresh;  // != 0: k_mask/k_tiles just flagged the current state (host step);
                    // cleared by k_tau

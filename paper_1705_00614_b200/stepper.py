@@ -218,6 +218,12 @@ class CsphTvdStepper:
         self._rc(self._lib.swf_last_ingest_bytes(self._ctx, C.byref(b)))
         return b.value
 
+    def last_writeback_bytes(self) -> int:
+        """Host bytes the last step(state) on pinned arrays wrote back."""
+        b = C.c_longlong()
+        self._rc(self._lib.swf_last_writeback_bytes(self._ctx, C.byref(b)))
+        return b.value
+
     def set_host_mirror(self, on: bool = True) -> None:
         """Opt-in host mirror (swf_set_host_mirror): step(state) on the same
         pinned arrays skips the host->device copies while the caller leaves
