@@ -61,6 +61,9 @@ constexpr int NPART_ALLOC = 5;  // doubles per tile in d_part (see k_reduce)
 #define SWF_PRAGMA_(x) _Pragma(#x)
 #define SWF_UNROLL_(n) SWF_PRAGMA_(unroll n)
 #define SWF_PHASE_LOOP SWF_UNROLL_(SWF_PHASE_UNROLL)
+#ifndef SWF_TMA  // slim k_step: the region's H, HUx, HUy, b tiles by TMA (cp.async.bulk.tensor)
+#define SWF_TMA 1
+#endif
 #ifndef SWF_EPI_ONEBAR  // k_step epilogue: the partials' barrier is the acceptance barrier
 #define SWF_EPI_ONEBAR 1
 #endif
@@ -864,6 +867,52 @@ __device__ __forceinline__ FaceRec face_from_sides(bool wetA, bool wetB, const S
   return rec;
 }
 
+// ---- TMA: the region tiles of k_step (Blackwell tensor-memory copies) -------
+// One thread arms an mbarrier with the byte count and issues four 2D tensor
+// copies (H, HUx, HUy, b; box = RX x RY doubles, out-of-bounds cells zero-
+// filled exactly like the per-thread loads' domain check); every thread
+// waits on the barrier's phase.  No registers hold the region in flight.
+struct TmaArgs {
+  CUtensorMap m[4];  // H, HUx, HUy of the step-start buffer, b
+  int on;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void tma_region_loads(const TmaArgs& T, double* R, uint64_t* bar,
+                                                 int c0, int c1) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // after the threads' last smem use
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(4 * RREG * (int)sizeof(double))
+               : "memory");
+  const int planes[4] = {F_D, F_U, F_V, F_B};
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(R + planes[q] * RREG)),
+        "l"(reinterpret_cast<uint64_t>(&T.m[q])), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+        "selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+}
+
 // region-plane accessors of step_tile: eta and the shifts stored, or (slim
 // variant) recomputed from depth, bed and velocity with the same expressions
 #if SWF_STEP_SLIM
@@ -888,8 +937,9 @@ struct SNbrB {  // SNbr with eta = depth + b at the point of use
 #endif
 
 template <bool SPEC>
-__device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const int tile) {
-  extern __shared__ double smem[];
+__device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const int tile,
+                                          const TmaArgs& T, uint64_t* mbar, uint32_t& tphase) {
+  extern __shared__ __align__(128) double smem[];
   double* R = smem;                       // F_NUM x RREG
   double* SL = smem + F_NUM * RREG;       // 3 x NSL slopes (eta, un, ut)
   double* FB = SL + 3 * NSL;              // 4 x NFC faces (fm, fnl, fnr, ft)
@@ -964,6 +1014,12 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
   double* LAM = FB;
   static_assert(4 * BX * BY <= 4 * NFC, "lambda plane + the owned step-start state (SWF_OWN_FB)");
 
+  const bool tma = SWF_TMA && T.on;
+  if (tma) {  // the region's inputs by TMA into the D, U, V, B planes
+    if (tid == 0) tma_region_loads(T, R, mbar, i0 - 2, r0 - 2);
+    mbar_wait(mbar, tphase);
+    tphase ^= 1u;
+  }
   PHASE_MARK(0);
   // ---- phase 1: region inputs and the half-step view (K4 predictor, HalfView)
   // (each thread loads its cells' inputs here: the predictor of a cell needs
@@ -973,15 +1029,22 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
     int xr = c % RX, yr = c / RX;
     int i = i0 - 2 + xr, r = r0 - 2 + yr;
     double d = 0.0, u = 0.0, v = 0.0;
-    double Hn = 0.0, mx = 0.0, my = 0.0, bb = 0.0;
-    if (i >= 0 && i < G.nx && r >= 0 && r < G.rows) {
-      size_t k = (size_t)i + (size_t)r * nx;
-      Hn = A.H[k];
-      mx = A.HUx[k];
-      my = A.HUy[k];
-      bb = A.b[k];
+    double Hn = 0.0, mx = 0.0, my = 0.0;
+    if (tma) {  // (zero outside the local grid, like the loads below)
+      Hn = R[F_D * RREG + c];
+      mx = R[F_U * RREG + c];
+      my = R[F_V * RREG + c];
+    } else {
+      double bb = 0.0;
+      if (i >= 0 && i < G.nx && r >= 0 && r < G.rows) {
+        size_t k = (size_t)i + (size_t)r * nx;
+        Hn = A.H[k];
+        mx = A.HUx[k];
+        my = A.HUy[k];
+        bb = A.b[k];
+      }
+      R[F_B * RREG + c] = bb;
     }
-    R[F_B * RREG + c] = bb;
     const bool owned = xr >= 2 && xr < BX + 2 && yr >= 2 && yr < BY + 2;
     const int o = (xr - 2) + (yr - 2) * BX;
     if (SWF_OWN_FB && owned) {  // the step-start state, for phase 2 (FB is free until 4x)
@@ -1515,8 +1578,17 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
   }
 }
 
-__global__ void __launch_bounds__(STHR, SWF_STEP_MINB) k_step(Geo G, StepArgs A) {
-  step_tile<SWF_SPECULATE != 0>(G, A, blockIdx.x);
+__device__ __forceinline__ void step_kernel_init(const TmaArgs& T, uint64_t* mbar) {
+  if (SWF_TMA && T.on && threadIdx.x == 0) mbar_init(mbar);
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(STHR, SWF_STEP_MINB)
+    k_step(Geo G, StepArgs A, const __grid_constant__ TmaArgs T) {
+  __shared__ __align__(8) uint64_t s_mbar;
+  uint32_t tphase = 0;
+  step_kernel_init(T, &s_mbar);
+  step_tile<SWF_SPECULATE != 0>(G, A, blockIdx.x, T, &s_mbar, tphase);
 }
 
 // k_slist: the tiles k_step must visit -- flux-active ones, and inactive
@@ -1536,8 +1608,12 @@ __global__ void k_slist(Geo G, StepArgs A) {
   }
 }
 
-__global__ void __launch_bounds__(STHR, SWF_STEP_MINB) k_step_list(Geo G, StepArgs A) {
+__global__ void __launch_bounds__(STHR, SWF_STEP_MINB)
+    k_step_list(Geo G, StepArgs A, const __grid_constant__ TmaArgs T) {
   __shared__ int s_next;
+  __shared__ __align__(8) uint64_t s_mbar;
+  uint32_t tphase = 0;
+  step_kernel_init(T, &s_mbar);
   StepScalars* sc = A.sc;
   const int n = *(volatile int*)&sc->list_n[1];
   while (true) {
@@ -1546,15 +1622,19 @@ __global__ void __launch_bounds__(STHR, SWF_STEP_MINB) k_step_list(Geo G, StepAr
     const int q = s_next;
     __syncthreads();
     if (q >= n) break;
-    step_tile<SWF_SPECULATE != 0>(G, A, A.list[q]);
+    step_tile<SWF_SPECULATE != 0>(G, A, A.list[q], T, &s_mbar, tphase);
     __syncthreads();
   }
 }
 
-__global__ void __launch_bounds__(STHR, SWF_STEP_MINB) k_step_redo(Geo G, StepArgs A) {
+__global__ void __launch_bounds__(STHR, SWF_STEP_MINB)
+    k_step_redo(Geo G, StepArgs A, const __grid_constant__ TmaArgs T) {
+  __shared__ __align__(8) uint64_t s_mbar;
+  uint32_t tphase = 0;
+  step_kernel_init(T, &s_mbar);
   const int n = *(volatile int*)&A.sc->redo_n[1];
   for (int q = blockIdx.x; q < n; q += gridDim.x) {
-    step_tile<false>(G, A, A.redo[q]);
+    step_tile<false>(G, A, A.redo[q], T, &s_mbar, tphase);
     __syncthreads();
   }
 }
@@ -2542,6 +2622,15 @@ StepArgs step_args(swf_ctx* c) {
   return A;
 }
 
+// The TMA descriptors of this step: the step-start buffer (cur) and b.
+TmaArgs tma_args(const swf_ctx* c) {
+  TmaArgs T;
+  T.on = (SWF_TMA && SWF_STEP_SLIM && c->tma_ok) ? 1 : 0;
+  for (int q = 0; q < 3; ++q) T.m[q] = c->tma_state[c->cur][q];
+  T.m[3] = c->tma_b;
+  return T;
+}
+
 constexpr size_t step_smem() {
   return (size_t)(F_NUM * RREG + SCRATCH) * sizeof(double);
 }
@@ -2735,12 +2824,13 @@ int fused_enqueue_phase2(swf_ctx* c, double dt_cap, double global_speed, const d
     if (nt > 0 && SWF_TILE_LISTS) {
       StepArgs SA = step_args(c);
       k_slist<<<(nt + 255) / 256, 256, 0, c->stream>>>(G, SA);
-      k_step_list<<<c->sm_count * SWF_STEP_MINB, STHR, step_smem(), c->stream>>>(G, SA);
+      k_step_list<<<c->sm_count * SWF_STEP_MINB, STHR, step_smem(), c->stream>>>(G, SA,
+                                                                                 tma_args(c));
     } else if (nt > 0) {
-      k_step<<<nt, STHR, step_smem(), c->stream>>>(G, step_args(c));
+      k_step<<<nt, STHR, step_smem(), c->stream>>>(G, step_args(c), tma_args(c));
     }
     if (nt > 0 && SWF_SPECULATE)
-      k_step_redo<<<RED_CTAS, STHR, step_smem(), c->stream>>>(G, step_args(c));
+      k_step_redo<<<RED_CTAS, STHR, step_smem(), c->stream>>>(G, step_args(c), tma_args(c));
   }
   ev(c, 4);
   double* red = c->d_part + NPART * (size_t)(nt > 0 ? nt : 1);
@@ -2980,6 +3070,39 @@ int fused_prepare(swf_ctx* c) {
     const size_t bytes = (local_cells(c) ? local_cells(c) : 1) * sizeof(double);
     e = cudaMalloc(&c->d_lamn, bytes);
     if (e == cudaSuccess) e = cudaMemset(c->d_lamn, 0, bytes);
+  }
+  // TMA descriptors of k_step's region loads (2D tiles RX x RY of doubles):
+  // the row stride must be a multiple of 16 bytes (even nx); else the
+  // per-thread loads stay
+  c->tma_ok = 0;
+  if (e == cudaSuccess && SWF_TMA && SWF_STEP_SLIM && c->geo.nx % 2 == 0) {
+    using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess && fn) {
+      auto encode = reinterpret_cast<EncodeFn>(fn);
+      const cuuint64_t dims[2] = {(cuuint64_t)c->geo.nx, (cuuint64_t)c->geo.rows};
+      const cuuint64_t strides[1] = {(cuuint64_t)c->geo.nx * sizeof(double)};
+      const cuuint32_t box[2] = {(cuuint32_t)RX, (cuuint32_t)RY};
+      const cuuint32_t estr[2] = {1, 1};
+      auto mk = [&](CUtensorMap* m, const double* ptr) {
+        return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)ptr, dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+      };
+      bool ok = mk(&c->tma_b, c->b);
+      for (int p = 0; p < 2 && ok; ++p)
+        ok = mk(&c->tma_state[p][0], c->H[p]) && mk(&c->tma_state[p][1], c->HUx[p]) &&
+             mk(&c->tma_state[p][2], c->HUy[p]);
+      c->tma_ok = ok ? 1 : 0;
+    }
+    cudaGetLastError();
   }
   // exact-diagnostics captures: full grids only (a strip's sums continue
   // its neighbours' running totals, which stay with the tile-order sums)

@@ -1,6 +1,7 @@
 // swf_internal.cuh — device context of libswflood_cuda.so (not part of the ABI).
 #pragma once
 
+#include <cuda.h>  // CUtensorMap (TMA descriptors; encoded through the runtime's driver entry point)
 #include <cuda_runtime.h>
 #include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
@@ -131,6 +132,11 @@ struct swf_ctx {
   double* fpy = nullptr;
   double* d_lamn = nullptr;  // SWF_LAMBDA_SHARE builds: lambda(H_n, n) of the wet cells
   double* d_gxy = nullptr;   // SWF_GRAD_SHARE builds: k_step's half-step eta gradients
+  // TMA descriptors of k_step's region loads: [parity][H, HUx, HUy] and b
+  // (2D, box = the tile + 2-cell halo; tma_ok = 0: per-thread loads instead)
+  CUtensorMap tma_state[2][3];
+  CUtensorMap tma_b;
+  int tma_ok = 0;
   // sources / wind
   std::vector<swf::DevSrc> h_src;
   std::vector<double> h_ht, h_hq;
