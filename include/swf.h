@@ -183,6 +183,10 @@ int swf_host_changed(swf_ctx* ctx);
  * rejected and that were recomputed exactly: counts[0] forces, [1] step
  * (diagnostics; see the speculative-division note in swf_fused.cu). */
 int swf_debug_redo_counts(const swf_ctx* ctx, int* counts);
+/* How k_step stages its tile regions: 1 = TMA tensor copies
+ * (cp.async.bulk.tensor; needs an even nx), 0 = per-thread loads.  Results
+ * are identical either way (diagnostics). */
+int swf_debug_region_loads(const swf_ctx* ctx);
 /* One step on the device-resident state; info may be NULL (then no host
  * synchronisation happens and errors surface at the next synchronising
  * call). */

@@ -78,6 +78,7 @@ def declare(lib):
     _sig(lib, "swf_build_flavor", C.c_char_p)
     _sig(lib, "swf_host_changed", I, P)
     _sig(lib, "swf_debug_redo_counts", I, P, PI)
+    _sig(lib, "swf_debug_region_loads", I, P)
     _sig(lib, "swf_device_buffers", I, P, C.POINTER(C.c_void_p))
     _sig(lib, "swf_strip_set_peer", I, P, I, C.POINTER(C.c_void_p), I)
     _sig(lib, "swf_strip_begin_batch", I, P)

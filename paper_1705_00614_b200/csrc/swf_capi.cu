@@ -762,6 +762,11 @@ int swf_debug_redo_counts(const swf_ctx* c, int* counts) {
   return SWF_OK;
 }
 
+int swf_debug_region_loads(const swf_ctx* c) {
+  if (!c) return SWF_ECONFIG;
+  return c->tma_ok ? 1 : 0;
+}
+
 int swf_last_ingest_bytes(const swf_ctx* c, long long* bytes) {
   if (!c || !bytes) return SWF_ECONFIG;
   *bytes = c->last_ingest_bytes;

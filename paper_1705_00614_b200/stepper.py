@@ -241,6 +241,14 @@ class CsphTvdStepper:
         self._rc(self._lib.swf_debug_redo_counts(self._ctx, a))
         return a[0], a[1]
 
+    def region_loads(self) -> str:
+        """How k_step stages its tile regions: "tma" (tensor copies, even nx)
+        or "threads" (per-thread loads)."""
+        r = self._lib.swf_debug_region_loads(self._ctx)
+        if r < 0:
+            self._rc(r)
+        return "tma" if r == 1 else "threads"
+
     def active_tiles(self):
         """(updated tiles, all tiles, cells per tile) of the last fused step."""
         a, b, c = C.c_int(), C.c_int(), C.c_int()

@@ -621,6 +621,26 @@ def test_odd_sizes_vs_oracle(gpu_cls, oracle_built, nx, ny, bs):
     assert_state_bitwise(hs, st, f"{nx}x{ny} pinned")
 
 
+@pytest.mark.parametrize("nx,ny", [(96, 70), (97, 70)])
+def test_region_loads_tma_and_per_thread_vs_oracle(gpu_cls, oracle_built, nx, ny):
+    """k_step stages its tile regions with TMA tensor copies when the row
+    stride allows (even nx; out-of-range cells zero-filled by the copy
+    engine) and with per-thread loads otherwise: both bitwise vs the oracle
+    on a window whose tiles straddle every domain edge."""
+    sc = S.floodplain(192, 50.0, window=(40, 60, nx, ny))
+    st = sc.state.copy()
+    g = make(gpu_cls, sc)
+    assert g.region_loads() == ("tma" if nx % 2 == 0 else "threads")
+    o = make(oracle_built.OracleStepper, sc)
+    a = st.copy()
+    g.upload(a)
+    for _ in range(12):
+        g.step_resident()
+        o.step(st)
+    g.download(a)
+    assert_state_bitwise(a, st, f"{nx}x{ny} ({g.region_loads()})")
+
+
 @pytest.mark.parametrize("n,win", [(40960, (0, 20000, 40960, 40)), (8192, (4000, 0, 5, 8192))])
 def test_extreme_aspect_ratios_vs_oracle(gpu_cls, oracle_built, n, win):
     """Ragged extremes: a 40960-wide, 40-row band (long rows, one partial tile
