@@ -291,10 +291,16 @@ __device__ __forceinline__ unsigned src_mask_for(const Geo& G, const DevSrc* src
   return m;
 }
 
+#ifndef SWF_SRC_ROLLED  // keep the source lookup loops rolled (rare path, compact code)
+#define SWF_SRC_ROLLED 1
+#endif
 __device__ __forceinline__ double msrc(const Geo& G, const DevSrc* src, const double* sig,
                                        unsigned mask, int i, int jg, double& vx, double& vy) {
   double s = 0.0;
   if (!mask) return s;
+#if SWF_SRC_ROLLED
+#pragma unroll 1
+#endif
   for (int m = 0; m < G.nsrc; ++m) {
     if (G.nsrc <= 32 && !((mask >> m) & 1u)) continue;
     const DevSrc& d = src[m];
