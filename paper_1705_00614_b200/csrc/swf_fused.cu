@@ -805,6 +805,23 @@ struct Slopes {
   double eta, un, ut;
 };
 
+// minmod without branches: for operands of one sign (both > 0 or both < 0)
+// the one of smaller magnitude is std::min / std::max of stepper.cpp:23-27
+// (equal magnitudes: the same bits); anything else -- mixed signs, zeros,
+// NaN -- is 0 as there.
+#ifndef SWF_MINMOD_BF
+#define SWF_MINMOD_BF 1
+#endif
+__device__ __forceinline__ double minmod_sel(double a, double b) {
+#if SWF_MINMOD_BF
+  const bool take = (a > 0.0 && b > 0.0) || (a < 0.0 && b < 0.0);
+  const double m = fabs(a) < fabs(b) ? a : b;
+  return take ? m : 0.0;
+#else
+  return minmod(a, b);
+#endif
+}
+
 __device__ __forceinline__ Slopes cell_slopes(double em, double um, double tm, double sm, double ec,
                                               double uc, double tc, double sc_, double ep, double up,
                                               double tp, double sp, double h, bool* ok = nullptr) {
@@ -815,9 +832,9 @@ __device__ __forceinline__ Slopes cell_slopes(double em, double um, double tm, d
   double d_out = sc_ - p_out;
   Slopes s;
   Recip Ri = recip_of(d_in), Ro = recip_of(d_out);
-  s.eta = minmod(rdiv(ep - ec, Ri, ok), rdiv(ec - em, Ro, ok));
-  s.un = minmod(rdiv(up - uc, Ri, ok), rdiv(uc - um, Ro, ok));
-  s.ut = minmod(rdiv(tp - tc, Ri, ok), rdiv(tc - tm, Ro, ok));
+  s.eta = minmod_sel(rdiv(ep - ec, Ri, ok), rdiv(ec - em, Ro, ok));
+  s.un = minmod_sel(rdiv(up - uc, Ri, ok), rdiv(uc - um, Ro, ok));
+  s.ut = minmod_sel(rdiv(tp - tc, Ri, ok), rdiv(tc - tm, Ro, ok));
   return s;
 }
 
