@@ -198,6 +198,10 @@ int create_impl(const swf_terrain* T, const swf_params* P, const swf_control* K,
   if (!T || !P || !K || !O) return set_err(nullptr, SWF_ECONFIG, "null argument");
   if (T->ny >= 1 && (j0 < 0 || j1 > T->ny || j0 >= j1))
     return set_err(nullptr, SWF_ECONFIG, "strip rows out of range");
+  // a neighbour's SWF_HALO ghost rows are this strip's owned boundary rows
+  if (T->ny >= 1 && (j0 > 0 || j1 < T->ny) && j1 - j0 < SWF_HALO)
+    return set_err(nullptr, SWF_ECONFIG,
+                   "strip: a strip with a neighbour must own at least 3 rows (the halo depth)");
   // host arrays cover the local window: global rows [j0 - glo, j1 + ghi)
   int glo = j0 > 0 ? SWF_HALO : 0, ghi = j1 < T->ny ? SWF_HALO : 0;
   if (j0 - glo < 0) glo = j0;

@@ -442,9 +442,24 @@ void CsphTvdStepper::create() {
     int ndev = 0;
     int rc = swf_device_count(&ndev);
     if (rc || ndev < 1) throw_status(rc ? rc : SWF_ECUDA, swf_last_error(nullptr));
+    // block-row cuts, then every strip at least SWF_HALO rows (a neighbour's
+    // ghost rows come from one strip's owned rows; multigpu.min_rows_cuts)
+    std::vector<int> cut(D + 1);
+    for (int d = 0; d <= D; ++d) cut[d] = (int)((long long)d * nby / D);
+    auto rows = [&](int d) {
+      return std::min(terrain.ny, cut[d + 1] * bs) - std::min(terrain.ny, cut[d] * bs);
+    };
+    if (D > 1) {
+      for (int d = D - 1; d > 0; --d)
+        while (rows(d) < SWF_HALO && cut[d] - 1 > cut[d - 1]) --cut[d];
+      for (int d = 0; d + 1 < D; ++d)
+        while (rows(d) < SWF_HALO && cut[d + 1] + 1 < cut[d + 2]) ++cut[d + 1];
+      for (int d = 0; d < D; ++d)
+        if (rows(d) < SWF_HALO) throw ConfigError("stepper: too many devices for the grid rows");
+    }
     for (int d = 0; d < D; ++d) {
-      int j0 = std::min(terrain.ny, (int)((long long)d * nby / D) * bs);
-      int j1 = std::min(terrain.ny, (int)((long long)(d + 1) * nby / D) * bs);
+      int j0 = std::min(terrain.ny, cut[d] * bs);
+      int j1 = std::min(terrain.ny, cut[d + 1] * bs);
       int w0 = std::max(0, j0 - SWF_HALO);
       swf_terrain tw = t;
       tw.b = terrain.b.data() + (size_t)w0 * terrain.nx;

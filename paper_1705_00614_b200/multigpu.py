@@ -34,18 +34,41 @@ from . import _abi as A
 HALO = 3
 
 
+def min_rows_cuts(cuts, bs: int, ny: int, halo: int = HALO) -> List[int]:
+    """Block-row cuts adjusted so that every strip of a multi-strip split owns
+    at least `halo` rows: a neighbour's ghost rows must all come from one
+    strip's owned rows (swf_create_strip rejects smaller strips).  Later strips
+    grow first (the last block row may be partial), then earlier ones;
+    ValueError if the grid is too small for that many strips."""
+    cuts = list(cuts)
+    parts = len(cuts) - 1
+    if parts <= 1:
+        return cuts
+    rows = lambda p: min(cuts[p + 1] * bs, ny) - min(cuts[p] * bs, ny)
+    for p in range(parts - 1, 0, -1):
+        while rows(p) < halo and cuts[p] - 1 > cuts[p - 1]:
+            cuts[p] -= 1
+    for p in range(parts - 1):
+        while rows(p) < halo and cuts[p + 1] + 1 < cuts[p + 2]:
+            cuts[p + 1] += 1
+    if any(rows(p) < halo for p in range(parts)):
+        raise ValueError(f"cannot split {ny} rows into {parts} strips of at least {halo} rows "
+                         f"at block size {bs}")
+    return cuts
+
+
 def strip_bounds(ny: int, parts: int, bs: int) -> List[Tuple[int, int]]:
-    """Owned global rows [j0, j1) per strip: balanced whole block rows."""
+    """Owned global rows [j0, j1) per strip: balanced whole block rows, every
+    strip at least HALO rows (min_rows_cuts)."""
     nbr = (ny + bs - 1) // bs
     if parts < 1 or parts > nbr:
         raise ValueError(f"cannot split {nbr} block rows into {parts} strips")
     base, rem = divmod(nbr, parts)
-    out, b0 = [], 0
+    cuts = [0]
     for p in range(parts):
-        b1 = b0 + base + (1 if p < rem else 0)
-        out.append((b0 * bs, min(b1 * bs, ny)))
-        b0 = b1
-    return out
+        cuts.append(cuts[-1] + base + (1 if p < rem else 0))
+    cuts = min_rows_cuts(cuts, bs, ny)
+    return [(cuts[p] * bs, min(cuts[p + 1] * bs, ny)) for p in range(parts)]
 
 
 def balanced_bounds(weights, parts: int, bs: int, ny: int) -> List[Tuple[int, int]]:
@@ -70,6 +93,7 @@ def balanced_bounds(weights, parts: int, bs: int, ny: int) -> List[Tuple[int, in
         b = min(b, nbr - (parts - p))
         cuts.append(b)
     cuts.append(nbr)
+    cuts = min_rows_cuts(cuts, bs, ny)
     return [(cuts[p] * bs, min(cuts[p + 1] * bs, ny)) for p in range(parts)]
 
 

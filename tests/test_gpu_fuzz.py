@@ -51,3 +51,52 @@ def test_random_scenarios_vs_reference(oracle_built, seed):
     k, msg = run_pair(o, drv, so, sg, 20)
     assert_state_bitwise(sg, so, f"seed {seed} ({['pageable', 'resident', 'pinned'][how]}, "
                                  f"{k} steps{', ' + msg if msg else ''})")
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_random_scenarios_row_strips_vs_single_grid(seed):
+    """The same random scenarios split into 2-4 row strips (virtual ranks on
+    this GPU; synchronous protocol, or the asynchronous one where the block
+    size divides 16): the assembled owned rows bitwise equal to the single
+    grid (itself bitwise to the reference above)."""
+    from paper_1705_00614_b200 import CsphTvdStepper, NumericalError
+    from paper_1705_00614_b200 import multigpu as M
+    from fuzz_scenarios import window
+    from helpers import assert_bitwise
+    sc = random_scenario(seed)
+    ny, nx, bs = sc.terrain.ny, sc.terrain.nx, sc.options.block_size
+    parts = 2 + seed % 3
+    try:
+        bounds = M.strip_bounds(ny, parts, bs)
+    except ValueError:
+        pytest.skip("grid too small for that many strips of >= 3 rows")
+    one = make(CsphTvdStepper, sc)
+    st = sc.state.copy()
+    one.upload(st)
+    try:
+        done, _ = one.run(15)
+    except NumericalError:
+        pytest.skip("the scenario aborts (covered against the reference above)")
+    one.download(st)
+    strips = []
+    for j0, j1 in bounds:
+        w0, w1 = M.window_rows(j0, j1, ny)
+        ws = window(sc, w0, w1)
+        s = M.Strip(ws, ny, j0, j1, ws.global_sources, ws.wind)
+        s.upload(ws.state.H, ws.state.HUx, ws.state.HUy, 0.0)
+        strips.append((s, ws, w0))
+    if seed % 2 and 16 % bs == 0:
+        res = M.local_steps_async([s for s, _, _ in strips], 15)
+        assert all(d == 15 for d, _ in res)
+    else:
+        for _ in range(15):
+            M.local_step([s for s, _, _ in strips])
+    out = {f: np.empty(nx * ny) for f in ("H", "HUx", "HUy")}
+    for (s, ws, w0), (j0, j1) in zip(strips, bounds):
+        a = {f: np.empty(ws.terrain.nx * ws.terrain.ny) for f in out}
+        assert s.download(a["H"], a["HUx"], a["HUy"]) == st.t
+        r0 = (j0 - w0) * nx
+        for f in out:
+            out[f][j0 * nx:j1 * nx] = a[f][r0:r0 + (j1 - j0) * nx]
+    for f in out:
+        assert_bitwise(out[f], getattr(st, f), f"seed {seed} {parts} strips {f}")

@@ -155,3 +155,37 @@ def test_rebalance_bounds_decision():
     w3 = w.copy()
     w3[0] = 1.01
     assert M.rebalance_bounds(w3, b, bs, ny, threshold=0.05) is None
+
+
+def test_strip_bounds_every_strip_owns_a_full_halo():
+    """Every strip of a multi-strip split owns >= HALO rows (a neighbour's
+    ghost rows all come from one strip; swf_create_strip rejects smaller
+    strips), block-aligned cuts tile the grid, for the even and the
+    activity-balanced split alike; impossible splits raise ValueError."""
+    import random
+    from paper_1705_00614_b200 import multigpu as M
+    rnd = random.Random(1705)
+    seen = 0
+    for _ in range(5000):
+        ny = rnd.randint(1, 300)
+        bs = rnd.choice([1, 2, 3, 4, 7, 8, 16, 32])
+        parts = rnd.randint(1, 9)
+        nbr = (ny + bs - 1) // bs
+        for kind in ("even", "balanced"):
+            try:
+                if kind == "even":
+                    b = M.strip_bounds(ny, parts, bs)
+                else:
+                    w = [rnd.random() ** 4 for _ in range(nbr)]
+                    b = M.balanced_bounds(w, parts, bs, ny)
+            except ValueError:
+                assert parts > 1
+                continue
+            seen += 1
+            assert len(b) == parts and b[0][0] == 0 and b[-1][1] == ny
+            for (a0, a1), (c0, c1) in zip(b, b[1:]):
+                assert a1 == c0 and c0 % bs == 0
+            if parts > 1:
+                assert all(j1 - j0 >= M.HALO for j0, j1 in b), (ny, bs, parts, b)
+    assert seen > 5000
+    assert M.strip_bounds(33, 2, 16) == [(0, 16), (16, 33)]
