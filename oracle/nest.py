@@ -40,6 +40,12 @@ class Window:
         return self.r * self.nj + 2 * self.ghost
 
 
+
+# substeps of one fine grid per coupled step before the coupling gives up
+# (the device path's limit, csrc/swf_nest.cu); tests may lower it to check a
+# non-converging case without a million Python substeps
+MAX_SUBSTEPS = 1000000
+
 def ghost_cells(w: Window):
     """(fi, fj) of the ghost band in the device's enumeration order: ghost
     bottom rows, ghost top rows, then (left gw, right gw) columns per middle row."""
@@ -261,7 +267,7 @@ def coupled_step(coarse_stepper, coarse_state: FlowState, coarse_b, nests: List[
                 tfs = tfs + fi.tau * face_taps(n.fine, n.w.nxf, n.w.nyf, frect)
             tf = n.state.t
             sub += 1
-            if sub > 1000000:
+            if sub > MAX_SUBSTEPS:
                 raise NumericalError("nested grid: subcycling does not converge")
         n.state.t = t1
         subs.append(sub)

@@ -142,3 +142,52 @@ def test_coupled_mass_ledger_on_gpu():
     st = _down(coarse, ns.coarse.state)
     m1 = st.H.sum() * area
     assert abs((m1 - m0) - ledger) <= 1e-11 * m0, (m1 - m0, ledger)
+
+
+# Seeds 1, 7, 32 and 33 draw nests whose fine CFL step collapses (a film on a
+# steep fine-resolution bank; up to the 10^6-substep limit, e.g. seed 1,
+# which the non-convergence branch below checks against the oracle): 2-5
+# minutes each, run in the recorded sweep (profiles/fuzz_nest_r3zz.txt, all
+# 40 seeds passed) and left out of the routine suite.
+SLOW_NEST_SEEDS = {1, 7, 32, 33}
+
+
+@pytest.mark.parametrize("seed", [s for s in range(40) if s not in SLOW_NEST_SEEDS])
+def test_random_nests_match_oracle(oracle_built, seed):
+    """Seeded random nests: coarse size, cell size, refinement ratio 2-4,
+    window size and place (edges near or far), generator seed, one- or
+    two-way coupling; coupled steps bitwise against the oracle nest."""
+    from paper_1705_00614_b200.nesting import coupled_step
+    rng = np.random.default_rng(4000 + seed)
+    n = int(rng.integers(32, 81))
+    h = float(rng.choice([25.0, 50.0]))
+    r = int(rng.integers(2, 5))
+    ni, nj = int(rng.integers(3, n // 3)), int(rng.integers(3, n // 3))
+    # (the window keeps a 2-coarse-cell margin from the domain edges)
+    i0, j0 = int(rng.integers(2, n - ni - 1)), int(rng.integers(2, n - nj - 1))
+    two_way = bool(rng.random() < 0.7)
+    ns = S.nested_floodplain(n, h, (i0, j0, ni, nj), r, 2, seed=int(rng.integers(1, 10**6)))
+    coarse, nest = _gpu(ns, two_way=two_way)
+    cs, cstate, onest = _oracle(oracle_built, ns, two_way=two_way)
+    from paper_1705_00614_b200 import NumericalError
+    for k in range(4):
+        try:
+            gi = coupled_step(coarse, [nest])
+        except NumericalError as e:
+            # a fine grid whose CFL step collapses (a film racing down a steep
+            # fine-resolution bank): the device gives up after 10^6 substeps;
+            # the oracle must not land within a few thousand either
+            assert "subcycling does not converge" in str(e)
+            lim = N.MAX_SUBSTEPS
+            N.MAX_SUBSTEPS = 3000
+            try:
+                with pytest.raises(NumericalError, match="does not converge"):
+                    N.coupled_step(cs, cstate, ns.coarse.terrain.b, [onest])
+            finally:
+                N.MAX_SUBSTEPS = lim
+            return
+        oi, subs = N.coupled_step(cs, cstate, ns.coarse.terrain.b, [onest])
+        assert gi.tau == oi.tau, k
+        assert gi.substeps_total == subs[0], (k, gi.substeps_total, subs)
+    assert_state_bitwise(_down(coarse, cstate), cstate, f"coarse seed {seed}")
+    assert_state_bitwise(_down(nest.fine, onest.state), onest.state, f"fine seed {seed}")

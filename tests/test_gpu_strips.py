@@ -92,3 +92,23 @@ def test_strip_host_steps_from_pinned_windows(parts):
     assert_bitwise(H, ref.H, "H")
     assert_bitwise(X, ref.HUx, "HUx")
     assert_bitwise(Y, ref.HUy, "HUy")
+
+
+def test_strip_owning_fewer_rows_than_the_halo_is_rejected():
+    """A neighbour's 3 ghost rows must come from one strip's owned rows:
+    swf_create_strip refuses a smaller strip with a ConfigError (and the
+    splits never produce one, tests/test_multigpu_cpu.py)."""
+    from paper_1705_00614_b200 import ConfigError
+    n = 64
+    def window(j0, j1):
+        w0, w1 = M.window_rows(j0, j1, n)
+        sc = S.floodplain(n, 50.0, window=(0, w0, n, w1 - w0))
+        sc.options.block_size = 1  # (strip cuts are block-aligned)
+        return sc
+
+    for j0, j1 in ((30, 32), (0, 2), (62, 64)):
+        sc = window(j0, j1)
+        with pytest.raises(ConfigError, match="at least 3 rows"):
+            M.Strip(sc, n, j0, j1, sc.global_sources, sc.wind)
+    sc = window(29, 32)  # exactly the halo depth is fine
+    M.Strip(sc, n, 29, 32, sc.global_sources, sc.wind).close()
