@@ -1,9 +1,11 @@
 """GPU parity on seeded random scenarios (tests/fuzz_scenarios.py): every
 knob of the step path drawn at random, the CUDA path through the C ABI
 against the compiled reference (the C restatement where oracle/_ref is
-absent), through the three ways the step is driven -- the drop-in
-step(FlowState) on pageable arrays, resident steps, and pinned host buffers
-(write-through) -- with states, StepInfo and aborts bitwise / verbatim."""
+absent), through every way the step is driven -- the drop-in
+step(FlowState) on pageable arrays, resident steps, pinned host buffers
+(write-through), pinned buffers under the opt-in host mirror, and a 20-step
+CUDA-graph run (an abort commits the steps before it) -- with states,
+StepInfo and aborts bitwise / verbatim."""
 import numpy as np
 import pytest
 
@@ -27,6 +29,9 @@ class _Resident:
         return info
 
 
+DRIVERS = ("pageable", "resident", "pinned", "pinned+mirror", "run")
+
+
 @pytest.mark.parametrize("seed", range(150))
 def test_random_scenarios_vs_reference(oracle_built, seed):
     import torch
@@ -37,20 +42,40 @@ def test_random_scenarios_vs_reference(oracle_built, seed):
     o = make(oracle_built.OracleStepper, sc, kind=kind)
     g = make(CsphTvdStepper, sc)
     so = sc.state.copy()
-    how = seed % 3
-    if how == 0:
-        sg, drv = sc.state.copy(), g
-    elif how == 1:
+    how = DRIVERS[seed % len(DRIVERS)]
+    if how == "run":  # 20 steps in one CUDA-graph batch; an abort commits the steps before it
+        from paper_1705_00614_b200 import NumericalError
         sg = sc.state.copy()
-        drv = _Resident(g, sg)
+        g.upload(sg)
+        k, msg = 20, None
+        for q in range(20):
+            try:
+                last = o.step(so)
+            except NumericalError as e:
+                k, msg = q, str(e)
+                break
+        if msg is None:
+            done, info = g.run(20)
+            assert done == 20
+            for f in ("tau", "clamp_deficit_volume", "source_volume", "boundary_outflow_volume"):
+                assert getattr(info, f) == getattr(last, f), f
+        else:
+            with pytest.raises(NumericalError) as eg:
+                g.run(20)
+            assert str(eg.value) == msg
+        g.download(sg)
     else:
-        pin = lambda v: torch.from_numpy(np.array(v, copy=True)).pin_memory().numpy()
-        st = sc.state
-        sg = FlowState(st.nx, st.ny, st.t, pin(st.H), pin(st.HUx), pin(st.HUy))
-        drv = g
-    k, msg = run_pair(o, drv, so, sg, 20)
-    assert_state_bitwise(sg, so, f"seed {seed} ({['pageable', 'resident', 'pinned'][how]}, "
-                                 f"{k} steps{', ' + msg if msg else ''})")
+        if how in ("pageable", "resident"):
+            sg = sc.state.copy()
+        else:
+            pin = lambda v: torch.from_numpy(np.array(v, copy=True)).pin_memory().numpy()
+            st = sc.state
+            sg = FlowState(st.nx, st.ny, st.t, pin(st.H), pin(st.HUx), pin(st.HUy))
+            if how == "pinned+mirror":
+                g.set_host_mirror(True)
+        drv = _Resident(g, sg) if how == "resident" else g
+        k, msg = run_pair(o, drv, so, sg, 20)
+    assert_state_bitwise(sg, so, f"seed {seed} ({how}, {k} steps{', ' + msg if msg else ''})")
 
 
 @pytest.mark.parametrize("seed", range(60))
