@@ -3,8 +3,9 @@ knob of the step path drawn at random, the CUDA path through the C ABI
 against the compiled reference (the C restatement where oracle/_ref is
 absent), through every way the step is driven -- the drop-in
 step(FlowState) on pageable arrays, resident steps, pinned host buffers
-(write-through), pinned buffers under the opt-in host mirror, and a 20-step
-CUDA-graph run (an abort commits the steps before it) -- with states,
+(write-through), pinned buffers under the opt-in host mirror, a 20-step
+CUDA-graph run (an abort commits the steps before it), and the staged path
+(one kernel per reference stage) -- with states,
 StepInfo and aborts bitwise / verbatim."""
 import numpy as np
 import pytest
@@ -29,7 +30,7 @@ class _Resident:
         return info
 
 
-DRIVERS = ("pageable", "resident", "pinned", "pinned+mirror", "run")
+DRIVERS = ("pageable", "resident", "pinned", "pinned+mirror", "run", "staged")
 
 
 @pytest.mark.parametrize("seed", range(150))
@@ -40,9 +41,10 @@ def test_random_scenarios_vs_reference(oracle_built, seed):
     kind = "ref" if oracle_built.available("ref") else "orc"
     sc = random_scenario(seed)
     o = make(oracle_built.OracleStepper, sc, kind=kind)
-    g = make(CsphTvdStepper, sc)
-    so = sc.state.copy()
     how = DRIVERS[seed % len(DRIVERS)]
+    # "staged": the one-kernel-per-reference-stage path (swf_stage.cu)
+    g = make(CsphTvdStepper, sc, mode=1) if how == "staged" else make(CsphTvdStepper, sc)
+    so = sc.state.copy()
     if how == "run":  # 20 steps in one CUDA-graph batch; an abort commits the steps before it
         from paper_1705_00614_b200 import NumericalError
         sg = sc.state.copy()
@@ -65,7 +67,7 @@ def test_random_scenarios_vs_reference(oracle_built, seed):
             assert str(eg.value) == msg
         g.download(sg)
     else:
-        if how in ("pageable", "resident"):
+        if how in ("pageable", "resident", "staged"):
             sg = sc.state.copy()
         else:
             pin = lambda v: torch.from_numpy(np.array(v, copy=True)).pin_memory().numpy()
