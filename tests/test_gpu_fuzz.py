@@ -7,6 +7,8 @@ step(FlowState) on pageable arrays, resident steps, pinned host buffers
 CUDA-graph run (an abort commits the steps before it), and the staged path
 (one kernel per reference stage) -- with states,
 StepInfo and aborts bitwise / verbatim."""
+import os
+
 import numpy as np
 import pytest
 
@@ -33,7 +35,8 @@ class _Resident:
 DRIVERS = ("pageable", "resident", "pinned", "pinned+mirror", "run", "staged")
 
 
-@pytest.mark.parametrize("seed", range(150))
+# SWF_FUZZ_SEEDS widens the sweep (profiles/fuzz_drivers_r3zz.txt ran 3000)
+@pytest.mark.parametrize("seed", range(int(os.environ.get("SWF_FUZZ_SEEDS", "150"))))
 def test_random_scenarios_vs_reference(oracle_built, seed):
     import torch
     from paper_1705_00614_b200 import CsphTvdStepper
