@@ -61,6 +61,9 @@ constexpr int NPART_ALLOC = 5;  // doubles per tile in d_part (see k_reduce)
 #define SWF_PRAGMA_(x) _Pragma(#x)
 #define SWF_UNROLL_(n) SWF_PRAGMA_(unroll n)
 #define SWF_PHASE_LOOP SWF_UNROLL_(SWF_PHASE_UNROLL)
+#ifndef SWF_TMA_L2PROMO  // L2 promotion of the region tensor copies (0 none, 1 64B, 2 128B, 3 256B)
+#define SWF_TMA_L2PROMO 3
+#endif
 #ifndef SWF_TMA  // slim k_step: the region's H, HUx, HUy, b tiles by TMA (cp.async.bulk.tensor)
 #define SWF_TMA 1
 #endif
@@ -3116,7 +3119,7 @@ int fused_prepare(swf_ctx* c) {
       auto mk = [&](CUtensorMap* m, const double* ptr) {
         return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)ptr, dims, strides, box, estr,
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      (CUtensorMapL2promotion)SWF_TMA_L2PROMO,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
       };
       bool ok = mk(&c->tma_b, c->b);
