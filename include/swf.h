@@ -325,6 +325,8 @@ int swf_strip_unpack(swf_ctx* ctx, int side, const double* src);
  *              swf_strip_forces(ctx, dt_cap, 0)   begin + interior tile rows
  *              (exchange done) unpack_async(side)
  *              swf_strip_forces(ctx, dt_cap, 1)   ghost-dependent tile rows
+ *              (block sizes not dividing 16: part 0 is empty and part 1
+ *               runs the whole phase 1 -- same results, no overlap)
  *              swf_strip_local_speed(ctx, dev)    strip CFL speed -> device
  *              (allreduce-MAX of dev across strips, on the device, over the
  *               8 bytes as int64: a stopped strip publishes a marker above

@@ -2725,7 +2725,12 @@ int fused_enqueue_phase1(swf_ctx* c, double dt_cap, int part) {
   const Geo& G = c->geo;
   int rc;
   bool fm = mask_fused(G);
-  if (part == 0 && !fm) return set_err(c, SWF_ECONFIG, "split phase 1 needs a block size dividing 16");
+  // The interior/ghost split needs the block mask inside k_forces (block
+  // sizes dividing 16); otherwise k_mask reads the ghost rows, so the whole
+  // phase 1 runs in the second (post-exchange) part and the first is empty --
+  // the same results, without the overlap.
+  if (!fm && part == 0) return SWF_OK;
+  if (!fm && part == 1) part = -1;
   if (part == -2) {
     part = -1;
   } else if (part <= 0) {

@@ -86,9 +86,8 @@ def test_random_scenarios_vs_reference(oracle_built, seed):
 @pytest.mark.parametrize("seed", range(60))
 def test_random_scenarios_row_strips_vs_single_grid(seed):
     """The same random scenarios split into 2-4 row strips (virtual ranks on
-    this GPU; synchronous protocol, or the asynchronous one where the block
-    size divides 16): the assembled owned rows bitwise equal to the single
-    grid (itself bitwise to the reference above)."""
+    this GPU; synchronous or asynchronous protocol): the assembled owned rows
+    bitwise equal to the single grid (itself bitwise to the reference above)."""
     from paper_1705_00614_b200 import CsphTvdStepper, NumericalError
     from paper_1705_00614_b200 import multigpu as M
     from fuzz_scenarios import window
@@ -115,7 +114,7 @@ def test_random_scenarios_row_strips_vs_single_grid(seed):
         s = M.Strip(ws, ny, j0, j1, ws.global_sources, ws.wind)
         s.upload(ws.state.H, ws.state.HUx, ws.state.HUy, 0.0)
         strips.append((s, ws, w0))
-    if seed % 2 and 16 % bs == 0:
+    if seed % 2:  # (block sizes not dividing 16: no interior/ghost overlap, same results)
         res = M.local_steps_async([s for s, _, _ in strips], 15)
         assert all(d == 15 for d, _ in res)
     else:

@@ -147,3 +147,48 @@ def test_native_multi_device_abort_leaves_state():
     np.testing.assert_array_equal(st.H, before[0])
     np.testing.assert_array_equal(st.HUx, before[1])
     assert st.t == before[2]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(60))
+def test_native_group_random_scenarios_vs_reference(oracle_built, seed):
+    """The C++ drop-in with StepperOptions.devices = 2 or 3 (the in-process
+    swf_group; strips share this GPU) on the seeded random scenarios of
+    tests/fuzz_scenarios.py, step by step against the compiled reference:
+    state, tau, block counts and aborts (same step, same message)."""
+    from fuzz_scenarios import random_scenario
+    sc = random_scenario(seed)
+    T, P, K, O, W, srcs, st = to_native(sc)
+    O.devices = 2 + seed % 2
+    try:
+        g = sw.CsphTvdStepper(T, P, K, O)
+    except sw.ConfigError as e:
+        assert "too many devices" in str(e) or "block rows" in str(e), str(e)
+        pytest.skip(str(e))
+    if sc.wind.any():
+        g.set_wind(W)
+    if srcs:
+        g.set_sources(srcs)
+    kind = "ref" if oracle_built.available("ref") else "orc"
+    o = make(oracle_built.OracleStepper, sc, kind=kind)
+    ref = sc.state.copy()
+    for k in range(15):
+        ea = eb = None
+        try:
+            a = g.step(st)
+        except (sw.NumericalError, sw.ConfigError) as e:
+            ea = e
+        try:
+            b = o.step(ref)
+        except Exception as e:  # noqa: BLE001 -- compared below
+            eb = e
+        if ea or eb:
+            assert ea is not None and eb is not None, (k, ea, eb)
+            assert str(ea) == str(eb), (k, str(ea), str(eb))
+            break
+        assert a.tau == b.tau, k
+        assert (a.lagrangian_blocks, a.flux_blocks, a.total_blocks) == \
+            (b.lagrangian_blocks, b.flux_blocks, b.total_blocks), k
+    out = sc.state.copy()
+    out.H[:], out.HUx[:], out.HUy[:], out.t = st.H, st.HUx, st.HUy, st.t
+    assert_state_bitwise(out, ref, f"seed {seed}, {O.devices}-device group")

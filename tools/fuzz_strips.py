@@ -30,9 +30,7 @@ def main():
         n_y, bs = sc.terrain.ny, sc.options.block_size
         rng = np.random.default_rng(seed)
         parts = int(rng.integers(2, 5))
-        # the asynchronous protocol splits phase 1 by tile rows: block sizes
-        # dividing 16 only (ConfigError otherwise, swf_strip_forces)
-        mode = "async" if seed % 2 and 16 % bs == 0 else "sync"
+        mode = "async" if seed % 2 else "sync"
         one = make(CsphTvdStepper, sc)
         st = sc.state.copy()
         one.upload(st)
