@@ -12,7 +12,8 @@ import sys
 
 import numpy as np
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
 
 
 def main():
@@ -67,6 +68,21 @@ def main():
     for _ in range(2):
         M.local_step(strips)
     M.local_steps_async(strips, 2)
+    # a random scenario (tests/fuzz_scenarios.py: block size 7, open edges,
+    # sources, wind) in 2 strips through the asynchronous protocol
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from fuzz_scenarios import random_scenario, window
+    rs = random_scenario(3)
+    rs.options.block_size = 7
+    ny = rs.terrain.ny
+    rstrips = []
+    for j0, j1 in M.strip_bounds(ny, 2, 7):
+        w0, w1 = M.window_rows(j0, j1, ny)
+        ws = window(rs, w0, w1)
+        s = M.Strip(ws, ny, j0, j1, ws.global_sources, ws.wind)
+        s.upload(ws.state.H, ws.state.HUx, ws.state.HUy, 0.0)
+        rstrips.append(s)
+    M.local_steps_async(rstrips, 2)
     # single-process device group (pybind module over the C++ drop-in)
     try:
         from paper_1705_00614_b200 import swflood_native as sw
@@ -79,6 +95,11 @@ def main():
         fs = sw.FlowState.dry(T)
         fs.H[:] = full.state.H
         gg.step(fs)
+        gg.step(fs)
+        O.block_size = 7  # the unsplit phase 1 of a block size not dividing 16
+        gg = sw.CsphTvdStepper(T, P, sw.TimestepControl(), O)
+        fs = sw.FlowState.dry(T)
+        fs.H[:] = full.state.H
         gg.step(fs)
     except ImportError:
         pass
