@@ -58,11 +58,13 @@ int check_device_error(swf_ctx* c) {
   unsigned long long kind = key >> 58;
   const Geo& G = c->geo;
   if (kind == ERR_DT) {
-    // stepper.cpp:259-262 (std::to_string formats with %f)
-    char buf[256];
-    snprintf(buf, sizeof buf,
-             "timestep %f s fell below the abort floor %f s (max wave speed %f m/s)",
-             c->h_sc->err_val[0], c->h_sc->err_val[1], c->h_sc->err_val[2]);
+    // stepper.cpp:259-262 (std::to_string formats with %f; a speed near
+    // DBL_MAX prints ~310 digits, so the text is sized, not truncated)
+    const char* fmt = "timestep %f s fell below the abort floor %f s (max wave speed %f m/s)";
+    const double* v = c->h_sc->err_val;
+    std::string buf((size_t)snprintf(nullptr, 0, fmt, v[0], v[1], v[2]) + 1, '\0');
+    snprintf(&buf[0], buf.size(), fmt, v[0], v[1], v[2]);
+    buf.pop_back();
     return set_err(c, SWF_ENUMERICAL, buf);
   }
   if (kind == ERR_PEER)
