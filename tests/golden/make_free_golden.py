@@ -1,4 +1,5 @@
-"""Generate tests/golden/free_api_ref.bin.gz: the output of
+"""Generate tests/golden/free_api_ref.bin.gz (and free_api_ref_s<seed>.bin.gz
+for the seeded random variants): the output of
 tests/native/free_api_test.cpp compiled against the REFERENCE headers and
 linked with the reference objects oracle/Makefile builds from
 /root/reference/proj (run in the build container, where the reference is
@@ -31,20 +32,30 @@ def build_ref_exe(exe):
     return exe
 
 
-def reference_output():
+SEEDS = range(1, 9)  # the seeded random variants (free_api_test.cpp argv[2])
+
+
+def seeded_path(seed):
+    return os.path.join(HERE, f"free_api_ref_s{seed}.bin.gz")
+
+
+def reference_output(seed=0):
     with tempfile.TemporaryDirectory() as d:
         exe = build_ref_exe(os.path.join(d, "free_ref"))
         out = os.path.join(d, "free_ref.bin")
-        subprocess.run([exe, out], check=True, stdout=subprocess.DEVNULL)
+        subprocess.run([exe, out] + ([str(seed)] if seed else []), check=True,
+                       stdout=subprocess.DEVNULL)
         with open(out, "rb") as f:
             return f.read()
 
 
 def main():
-    data = reference_output()
-    with gzip.open(OUT, "wb", compresslevel=9) as f:
-        f.write(data)
-    print(f"{OUT}: {len(data)} bytes")
+    for seed in [0] + list(SEEDS):
+        data = reference_output(seed)
+        path = OUT if seed == 0 else seeded_path(seed)
+        with gzip.open(path, "wb", compresslevel=9) as f:
+            f.write(data)
+        print(f"{path}: {len(data)} bytes")
 
 
 if __name__ == "__main__":

@@ -13,6 +13,10 @@
 // Test infrastructure.  Usage: free_api_test OUT.bin
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
+#include <string>
+#include <exception>
+#include <algorithm>
 #include <cstdio>
 #include <type_traits>
 #include <vector>
@@ -84,58 +88,89 @@ static void put(const BlockMask& m) {
   }
 }
 
+// seed 0: the fixed case of tests/golden/free_api_ref.bin.gz; seed > 0: the
+// same program on a seeded random variant (grid shape, bed, water level,
+// films, momenta, Manning field, viscosity, latitude, wind, sources), whose
+// reference outputs are tests/golden/free_api_ref_s<seed>.bin.gz
+static unsigned long long rng_state = 0;
+static double U(double a, double b, double fixed) {
+  if (!rng_state) return fixed;
+  rng_state ^= rng_state << 13;
+  rng_state ^= rng_state >> 7;
+  rng_state ^= rng_state << 17;
+  return a + (b - a) * (double)(rng_state >> 11) * (1.0 / 9007199254740992.0);
+}
+static int Ui(int a, int b, int fixed) {  // [a, b]
+  return rng_state ? std::min(b, a + (int)U(0.0, (double)(b - a + 1), 0.0)) : fixed;
+}
+
 int main(int argc, char** argv) {
   if (argc < 2) return 2;
   out = std::fopen(argv[1], "wb");
   if (!out) return 2;
+  if (argc > 2) rng_state = 0x9E3779B97F4A7C15ull * (unsigned long long)std::atoll(argv[2]);
 
   // a tilted, bumpy basin: wet pools, dry banks above and below the water
   // surface, a thin film near eps_dry, a Manning field
-  const int nx = 41, ny = 29;
+  const int nx = Ui(5, 48, 41), ny = Ui(5, 40, 29);
+  const double slope = U(-4e-3, 4e-3, 2e-3), amp = U(0.1, 2.0, 0.9), kx = U(0.05, 0.8, 0.31),
+               ky = U(0.05, 0.8, 0.23), level = U(-0.5, 1.2, 0.6);
+  const int film_a = Ui(5, 40, 23), film_b = Ui(5, 40, 31);
   Terrain T;
   T.nx = nx;
   T.ny = ny;
-  T.h = 12.5;
+  T.h = U(0.5, 60.0, 12.5);
   T.b.resize(T.cells());
   for (int j = 0; j < ny; ++j)
     for (int i = 0; i < nx; ++i)
-      T.b[T.idx(i, j)] = 2e-3 * T.xc(i) + 0.9 * std::cos(0.31 * i) * std::sin(0.23 * j + 0.4);
+      T.b[T.idx(i, j)] = slope * T.xc(i) + amp * std::cos(kx * i) * std::sin(ky * j + 0.4);
   PhysicalParams P;
-  P.nu = 0.75;
-  P.omega_z = latitude_to_omega_z(48.7);
+  P.nu = U(0.0, 3.0, 0.75);
+  P.omega_z = latitude_to_omega_z(U(-80.0, 80.0, 48.7));
   P.n_field.resize(T.cells());
   for (int k = 0; k < (int)T.cells(); ++k) P.n_field[k] = 0.02 + 0.015 * ((k * 7) % 5) / 4.0;
+  const double vx = U(-1.5, 1.5, 0.3), vy = U(-1.5, 1.5, 0.25);
   FlowState S = FlowState::dry(T);
   for (int j = 0; j < ny; ++j)
     for (int i = 0; i < nx; ++i) {
       const int k = S.idx(i, j);
-      double e = 0.6 + 0.25 * std::sin(0.17 * i + 0.05 * j);
+      double e = level + 0.25 * std::sin(0.17 * i + 0.05 * j);
       S.H[k] = std::max(0.0, e - T.b[k]);
-      if ((i * 13 + j * 7) % 23 == 0) S.H[k] = 0.6e-6;  // just above eps_dry
-      if ((i * 5 + j * 11) % 31 == 0) S.H[k] = 0.4e-6;  // dry film
-      S.HUx[k] = S.H[k] * (0.3 * std::cos(0.2 * j) - 0.1);
-      S.HUy[k] = S.H[k] * (0.25 * std::sin(0.3 * i));
+      if ((i * 13 + j * 7) % film_a == 0) S.H[k] = 0.6e-6;  // just above eps_dry
+      if ((i * 5 + j * 11) % film_b == 0) S.H[k] = 0.4e-6;  // dry film
+      S.HUx[k] = S.H[k] * (vx * std::cos(0.2 * j) - 0.1);
+      S.HUy[k] = S.H[k] * (vy * std::sin(0.3 * i));
     }
   S.enforce_dry_rule(P.eps_dry);
   WindForcing W;
-  W.series = {{0.0, 4.0, -1.0}, {100.0, 6.5, 2.0}, {250.0, -3.0, 5.0}};
+  W.series = {{0.0, U(-20, 20, 4.0), U(-20, 20, -1.0)},
+              {100.0, U(-20, 20, 6.5), U(-20, 20, 2.0)},
+              {250.0, U(-20, 20, -3.0), U(-20, 20, 5.0)}};
   WindForcing none;
 
+  auto rect = [&](int i0, int j0, int i1, int j1) {
+    CellRect c;
+    c.i0 = Ui(0, nx - 1, i0);
+    c.j0 = Ui(0, ny - 1, j0);
+    c.i1 = Ui(c.i0, nx - 1, i1);
+    c.j1 = Ui(c.j0, ny - 1, j1);
+    return c;
+  };
   std::vector<SourceSpec> src(3);
   src[0].kind = SourceSpec::Kind::Discharge;
   src[0].name = "inflow";
-  src[0].cells = {0, 10, 2, 15};
-  src[0].hydrograph = {{0.0, 10.0}, {60.0, 250.0}, {300.0, 40.0}};
-  src[0].source_velocity = {0.8, -0.1};
+  src[0].cells = rect(0, 10, 2, 15);
+  src[0].hydrograph = {{0.0, U(0, 500, 10.0)}, {60.0, U(0, 500, 250.0)}, {300.0, U(0, 500, 40.0)}};
+  src[0].source_velocity = {U(-1, 1, 0.8), U(-1, 1, -0.1)};
   src[1].kind = SourceSpec::Kind::Rain;
   src[1].name = "rain";
-  src[1].cells = {1, 12, 30, 20};  // overlaps the inflow
-  src[1].rate = 2.5e-5;
+  src[1].cells = rect(1, 12, 30, 20);  // overlaps the inflow
+  src[1].rate = U(0.0, 1e-3, 2.5e-5);
   src[2].kind = SourceSpec::Kind::Discharge;
   src[2].name = "drain";
-  src[2].cells = {38, 3, 40, 6};
-  src[2].hydrograph = {{0.0, -15.0}};
-  src[2].source_velocity = {-0.2, 0.3};
+  src[2].cells = rect(38, 3, 40, 6);
+  src[2].hydrograph = {{0.0, U(-100, 0, -15.0)}};
+  src[2].source_velocity = {U(-1, 1, -0.2), U(-1, 1, 0.3)};
 
   // forcing.hpp:34-47 at every cell
   for (int j = 0; j < ny; ++j)
@@ -193,13 +228,19 @@ int main(int argc, char** argv) {
   c = a;
   CsphTvdStepper d(std::move(c));
   FlowState Sa = S, Sb = S, Sd = S;
-  for (int n = 0; n < 6; ++n) {
-    StepInfo ia = a.step(Sa), ib = b.step(Sb), id = d.step(Sd);
-    put(ia.tau);
-    put(ib.tau);
-    put(id.tau);
-    put_i(ia.flux_blocks);
-    put_i(id.lagrangian_blocks);
+  try {  // (a random variant may abort: the message is part of the output)
+    for (int n = 0; n < 6; ++n) {
+      StepInfo ia = a.step(Sa), ib = b.step(Sb), id = d.step(Sd);
+      put(ia.tau);
+      put(ib.tau);
+      put(id.tau);
+      put_i(ia.flux_blocks);
+      put_i(id.lagrangian_blocks);
+    }
+  } catch (const std::exception& e) {
+    put_i(-1);
+    const std::string m = e.what();
+    std::fwrite(m.data(), 1, m.size(), out);
   }
   put(Sa.t);
   put(Sa.H);

@@ -104,18 +104,27 @@ def test_free_api_golden_is_the_reference_output():
     import make_free_golden
     with gzip.open(FREE_GOLDEN, "rb") as f:
         assert f.read() == make_free_golden.reference_output()
+    for seed in make_free_golden.SEEDS:  # the seeded random variants
+        with gzip.open(make_free_golden.seeded_path(seed), "rb") as f:
+            assert f.read() == make_free_golden.reference_output(seed), seed
 
 
 @pytest.mark.gpu
-def test_free_api_matches_reference_bit_for_bit(tmp_path):
+@pytest.mark.parametrize("seed", range(0, 9))
+def test_free_api_matches_reference_bit_for_bit(tmp_path, seed):
+    """Seed 0: the fixed case; 1-8: seeded random variants of it (grid
+    shape, bed, level, films, momenta, viscosity, latitude, wind, sources)."""
     import gzip
     import numpy as np
     exe = build_free_exe()
     out = tmp_path / "free.bin"
-    r = subprocess.run([exe, str(out)], capture_output=True, text=True, timeout=600)
+    r = subprocess.run([exe, str(out)] + ([str(seed)] if seed else []), capture_output=True,
+                       text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     got = out.read_bytes()
-    with gzip.open(FREE_GOLDEN, "rb") as f:
+    golden = FREE_GOLDEN if seed == 0 else os.path.join(ROOT, "tests", "golden",
+                                                         f"free_api_ref_s{seed}.bin.gz")
+    with gzip.open(golden, "rb") as f:
         want = f.read()
     assert len(got) == len(want)
     if got != want:
