@@ -48,6 +48,10 @@ def test_random_scenarios_vs_reference(oracle_built, seed):
     # "staged": the one-kernel-per-reference-stage path (swf_stage.cu)
     g = make(CsphTvdStepper, sc, mode=1) if how == "staged" else make(CsphTvdStepper, sc)
     so = sc.state.copy()
+    # a third of the seeds cap the step (stepper.hpp:84-86: tau = min(CFL tau, dt_cap))
+    # (every driver meets capped and uncapped seeds: the cap cycles per driver round)
+    dt_cap = [0.0, 0.0, float(np.random.default_rng(seed).uniform(1e-4, 0.5))][
+        (seed // len(DRIVERS)) % 3]
     if how == "run":  # 20 steps in one CUDA-graph batch; an abort commits the steps before it
         from paper_1705_00614_b200 import NumericalError
         sg = sc.state.copy()
@@ -55,18 +59,18 @@ def test_random_scenarios_vs_reference(oracle_built, seed):
         k, msg = 20, None
         for q in range(20):
             try:
-                last = o.step(so)
+                last = o.step(so, dt_cap)
             except NumericalError as e:
                 k, msg = q, str(e)
                 break
         if msg is None:
-            done, info = g.run(20)
+            done, info = g.run(20, dt_cap)
             assert done == 20
             for f in ("tau", "clamp_deficit_volume", "source_volume", "boundary_outflow_volume"):
                 assert getattr(info, f) == getattr(last, f), f
         else:
             with pytest.raises(NumericalError) as eg:
-                g.run(20)
+                g.run(20, dt_cap)
             assert str(eg.value) == msg
         g.download(sg)
     else:
@@ -79,8 +83,8 @@ def test_random_scenarios_vs_reference(oracle_built, seed):
             if how == "pinned+mirror":
                 g.set_host_mirror(True)
         drv = _Resident(g, sg) if how == "resident" else g
-        k, msg = run_pair(o, drv, so, sg, 20)
-    assert_state_bitwise(sg, so, f"seed {seed} ({how}, {k} steps{', ' + msg if msg else ''})")
+        k, msg = run_pair(o, drv, so, sg, 20, dt_cap)
+    assert_state_bitwise(sg, so, f"seed {seed} ({how}, cap {dt_cap}, {k} steps{', ' + msg if msg else ''})")
 
 
 @pytest.mark.parametrize("seed", range(60))
