@@ -463,7 +463,9 @@ class RankStrip:
     torch.distributed: NCCL on device buffers (production), or gloo with host
     staging (SWF_DIST_BACKEND=gloo; lets 2+ ranks share one GPU in tests)."""
 
-    def __init__(self, config: str, n_full: int = 0, no_skip: bool = False):
+    def __init__(self, config: str, n_full: int = 0, no_skip: bool = False, scenario=None):
+        """config: a BASELINE.json config id, or `scenario` (a full-grid
+        scenarios.Scenario, e.g. a test's random case) with config "custom"."""
         import torch
         import torch.distributed as dist
         from . import scenarios as S
@@ -497,13 +499,19 @@ class RankStrip:
                 dist.init_process_group(self.backend)
         self.xdev = self.dev if self.backend == "nccl" else torch.device("cpu")
         self.weak = config == "C5W"
-        self.n = n_full or {"C3": 16384, "C5": 32768, "C2": 2048, "C5W": 32768}[config]
-        # rows of the global grid: square, or 4096 per GPU for weak scaling
-        self.ny = S.WEAK_ROWS * self.world if self.weak else self.n
+        self.full_sc = scenario
+        if scenario is not None:
+            self.n, self.ny = scenario.terrain.nx, scenario.terrain.ny
+        else:
+            self.n = n_full or {"C3": 16384, "C5": 32768, "C2": 2048, "C5W": 32768}[config]
+            # rows of the global grid: square, or 4096 per GPU for weak scaling
+            self.ny = S.WEAK_ROWS * self.world if self.weak else self.n
         # strips balanced by the initial activity of each block row (the wet
         # area is unevenly spread over the rows; equal row counts would leave
         # the busiest strip ~18 % above the mean at 8 GPUs on C3)
-        if self.world > 1 and config in ("C3", "C5") and \
+        if scenario is not None:
+            self.bounds = strip_bounds(self.ny, self.world, scenario.options.block_size)
+        elif self.world > 1 and config in ("C3", "C5") and \
                 os.environ.get("SWF_BALANCE_STRIPS", "1") != "0":
             wts = row_weights(config, self.n, 16, device=f"cuda:{self.local}")
             self.bounds = balanced_bounds(wts, self.world, 16, self.n)
@@ -520,7 +528,9 @@ class RankStrip:
         config, n_full, no_skip = self.config, self.n_full, self.no_skip
         self.j0, self.j1 = self.bounds[self.rank]
         self.w0, self.w1 = window_rows(self.j0, self.j1, self.ny)
-        if self.weak:
+        if self.full_sc is not None:
+            sc = S.window_of(self.full_sc, self.w0, self.w1)
+        elif self.weak:
             sc = S.build("C5", device=f"cuda:{self.local}",
                          window=(0, self.w0, self.n, self.w1 - self.w0))
         elif config in ("C3", "C5") and n_full:

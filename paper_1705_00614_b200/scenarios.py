@@ -270,6 +270,26 @@ def lake_at_rest(n: int = 128, h: float = 10.0, level: float = 0.0, seed: int = 
                     full_shape=(n, n), window=(0, 0, n, n))
 
 
+def window_of(sc: Scenario, w0: int, w1: int) -> Scenario:
+    """Rows [w0, w1) of a full-grid scenario (a strip's local window: terrain,
+    Manning field, state); the sources stay in full-grid cells
+    (global_sources), as strips take them, and the wind is shared."""
+    import copy
+    T = sc.terrain
+    nx = T.nx
+    sl = slice(w0 * nx, w1 * nx)
+    p = copy.deepcopy(sc.params)
+    if p.n_field is not None and len(p.n_field):
+        p.n_field = np.array(p.n_field[sl], copy=True)
+    st = sc.state
+    ws = FlowState(nx, w1 - w0, st.t, np.array(st.H[sl]), np.array(st.HUx[sl]),
+                   np.array(st.HUy[sl]))
+    return Scenario(sc.name, Terrain(nx, w1 - w0, T.h, T.x0, T.y0 + w0 * T.h,
+                                     np.array(T.b[sl])), p, sc.control, sc.options, ws,
+                    wind=sc.wind, full_shape=(nx, T.ny), window=(0, w0, nx, w1 - w0),
+                    global_sources=list(sc.global_sources or sc.sources))
+
+
 def build(config: str, device: str = "cpu", window=None) -> Scenario:
     """Scenario for a BASELINE.json config id: C1, C1w, C2, C3, C5."""
     if config in ("C1", "C1-dry"):

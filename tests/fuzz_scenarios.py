@@ -128,20 +128,8 @@ def run_pair(a, b, sa, sb, steps, dt_cap=0.0):
     return steps, None
 
 
+
 def window(sc: Scenario, w0: int, w1: int) -> Scenario:
-    """Rows [w0, w1) of a full-grid scenario (a strip's local window); the
-    sources stay in full-grid cells (global_sources), as strips take them."""
-    import copy
-    T = sc.terrain
-    nx = T.nx
-    sl = slice(w0 * nx, w1 * nx)
-    p = copy.deepcopy(sc.params)
-    if p.n_field is not None and len(p.n_field):
-        p.n_field = np.array(p.n_field[sl], copy=True)
-    st = sc.state
-    ws = FlowState(nx, w1 - w0, st.t, np.array(st.H[sl]), np.array(st.HUx[sl]),
-                   np.array(st.HUy[sl]))
-    return Scenario(sc.name, Terrain(nx, w1 - w0, T.h, T.x0, T.y0 + w0 * T.h,
-                                     np.array(T.b[sl])), p, sc.control, sc.options, ws,
-                    wind=sc.wind, full_shape=(nx, T.ny), window=(0, w0, nx, w1 - w0),
-                    global_sources=list(sc.sources))
+    """Rows [w0, w1) of a full-grid scenario (scenarios.window_of)."""
+    from paper_1705_00614_b200.scenarios import window_of
+    return window_of(sc, w0, w1)

@@ -15,7 +15,16 @@ def main():
     from paper_1705_00614_b200 import CsphTvdStepper, multigpu as M, scenarios as S
     n = int(os.environ.get("SWF_CHECK_N", "512"))
     steps = int(os.environ.get("SWF_CHECK_STEPS", "20"))
-    rs = M.RankStrip("C3", n_full=n)
+    fuzz = os.environ.get("SWF_CHECK_FUZZ")  # a seed of tests/fuzz_scenarios.py
+    if fuzz is not None:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from fuzz_scenarios import random_scenario
+        full = random_scenario(int(fuzz))
+        rs = M.RankStrip("custom", scenario=full)
+        n = full.terrain.nx
+    else:
+        full = None
+        rs = M.RankStrip("C3", n_full=n)
     p2p = os.environ.get("SWF_HALO") == "p2p"
     if p2p:
         assert rs.setup_p2p(), "P2P halo setup failed"
@@ -38,10 +47,13 @@ def main():
     got = rs.gather_state()
     ok = 1
     if rs.rank == 0:
-        full = S.floodplain(n, 50.0, device="cuda")
+        if full is None:
+            full = S.floodplain(n, 50.0, device="cuda")
         one = CsphTvdStepper(full.terrain, full.params, full.control, full.options)
-        one.set_wind(full.wind)
-        one.set_sources(full.sources)
+        if full.wind.any():
+            one.set_wind(full.wind)
+        if full.sources:
+            one.set_sources(full.sources)
         st = full.state.copy()
         one.upload(st)
         one.run(steps)

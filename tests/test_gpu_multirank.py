@@ -37,3 +37,46 @@ def test_torchrun_strips_bitwise(world, halo, migrate):
     r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "bitwise_equal=True" in r.stdout
+
+
+def _fuzz_seeds(count, steps, world):
+    """Random scenarios (tests/fuzz_scenarios.py) that split into `world`
+    strips of >= 3 rows and do not abort within `steps` (checked on the CPU
+    oracle), so a torchrun run of them must complete and match."""
+    from fuzz_scenarios import random_scenario
+    from helpers import make
+    from oracle import pyorc
+    from paper_1705_00614_b200 import multigpu as M
+    out, seed = [], 0
+    while len(out) < count and seed < 400:
+        sc = random_scenario(seed)
+        try:
+            M.strip_bounds(sc.terrain.ny, world, sc.options.block_size)
+            o = make(pyorc.OracleStepper, sc, kind="orc")
+            st = sc.state.copy()
+            for _ in range(steps):
+                o.step(st)
+            out.append(seed)
+        except Exception:  # noqa: BLE001 -- too small to split, or aborts
+            pass
+        seed += 1
+    return out
+
+
+@pytest.mark.parametrize("world,halo", [(2, "copy"), (3, "copy"), (2, "p2p"), (3, "p2p")])
+def test_torchrun_strips_random_scenarios(oracle_built, world, halo):
+    """The torchrun strip path (RankStrip: exchange, device allreduce-max,
+    P2P or copy halos) on seeded random scenarios (tests/fuzz_scenarios.py:
+    any block size, open / reflective edges, sources, wind): bitwise equal
+    to the single grid."""
+    seeds = _fuzz_seeds(3, 12, world)
+    assert seeds
+    for seed in seeds[(0 if halo == "copy" else 1):][:2]:
+        env = dict(os.environ, SWF_DIST_BACKEND="gloo", SWF_CHECK_FUZZ=str(seed),
+                   SWF_CHECK_STEPS="12", SWF_HALO=halo)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={world}", "--master-addr", "127.0.0.1", "--master-port",
+               str(_port()), os.path.join(ROOT, "tests", "multirank_check.py")]
+        r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600, cwd=ROOT)
+        assert r.returncode == 0, f"seed {seed}: " + r.stdout[-3000:] + r.stderr[-3000:]
+        assert "bitwise_equal=True" in r.stdout, seed
