@@ -271,12 +271,13 @@ class Strip:
     def mask(self):
         """(interior, halo) block counts of the owned block rows (last step),
         shaped (block rows, nbx)."""
-        nb = (self.nx + 15) // 16 * ((self.j1 - self.j0 + 15) // 16 + 1)
-        inn, hal = np.zeros(nb, np.int32), np.zeros(nb, np.int32)
         a, b = C.c_int(), C.c_int()
+        # the shape first (any block size), then the counts into arrays of it
+        self._rc(self._lib.swf_download_mask(self.ctx, None, None, C.byref(a), C.byref(b)))
+        n = a.value * b.value
+        inn, hal = np.zeros(max(n, 1), np.int32), np.zeros(max(n, 1), np.int32)
         self._rc(self._lib.swf_download_mask(self.ctx, inn.ctypes.data_as(A.PI),
                                              hal.ctypes.data_as(A.PI), C.byref(a), C.byref(b)))
-        n = a.value * b.value
         return inn[:n].reshape(b.value, a.value), hal[:n].reshape(b.value, a.value)
 
     # P2P halo (include/swf.h "P2P halo")
@@ -509,8 +510,10 @@ class RankStrip:
         # strips balanced by the initial activity of each block row (the wet
         # area is unevenly spread over the rows; equal row counts would leave
         # the busiest strip ~18 % above the mean at 8 GPUs on C3)
+        # block size of the strips' masks (the configs use the default 16)
+        self.bs = scenario.options.block_size if scenario is not None else 16
         if scenario is not None:
-            self.bounds = strip_bounds(self.ny, self.world, scenario.options.block_size)
+            self.bounds = strip_bounds(self.ny, self.world, self.bs)
         elif self.world > 1 and config in ("C3", "C5") and \
                 os.environ.get("SWF_BALANCE_STRIPS", "1") != "0":
             wts = row_weights(config, self.n, 16, device=f"cuda:{self.local}")
@@ -554,7 +557,7 @@ class RankStrip:
         inn, hal = self.strip.mask()
         act = ((inn > 0) | (hal > 0)).sum(axis=1).astype(np.float64)
         nbx = inn.shape[1]
-        return (act + dry_cost * (nbx - act)) * 256.0
+        return (act + dry_cost * (nbx - act)) * float(self.bs * self.bs)
 
     def rebalance(self, threshold: float = 0.03) -> bool:
         """Re-cut the strips from the current activity when that lowers the
@@ -566,7 +569,7 @@ class RankStrip:
         parts = [None] * self.world
         dist.all_gather_object(parts, self.block_row_weights())
         w = np.concatenate(parts)
-        new = rebalance_bounds(w, self.bounds, 16, self.ny, threshold)
+        new = rebalance_bounds(w, self.bounds, self.bs, self.ny, threshold)
         if new is None:
             return False
         self.migrate(new)

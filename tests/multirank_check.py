@@ -35,9 +35,11 @@ def main():
             # accepted), then force a move of every interior cut by a block row
             rs.rebalance(threshold=-1.0)
             b = [list(x) for x in rs.bounds]
+            bs = rs.bs
+            keep = max(bs, M.HALO)  # a block row, and at least the halo, stays on each side
             for q in range(1, rs.world):
-                d = 16 if q % 2 else -16
-                if b[q - 1][0] + 16 <= b[q][0] + d <= b[q][1] - 16:
+                d = bs if q % 2 else -bs
+                if b[q - 1][0] + keep <= b[q][0] + d <= b[q][1] - keep:
                     b[q - 1][1] = b[q][0] = b[q][0] + d
             rs.migrate([tuple(x) for x in b])
         if p2p:

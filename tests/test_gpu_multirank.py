@@ -63,17 +63,19 @@ def _fuzz_seeds(count, steps, world):
     return out
 
 
-@pytest.mark.parametrize("world,halo", [(2, "copy"), (3, "copy"), (2, "p2p"), (3, "p2p")])
-def test_torchrun_strips_random_scenarios(oracle_built, world, halo):
+@pytest.mark.parametrize("world,halo,migrate", [(2, "copy", "0"), (3, "copy", "0"),
+                                               (2, "p2p", "0"), (3, "p2p", "0"),
+                                               (3, "copy", "1"), (2, "p2p", "1")])
+def test_torchrun_strips_random_scenarios(oracle_built, world, halo, migrate):
     """The torchrun strip path (RankStrip: exchange, device allreduce-max,
     P2P or copy halos) on seeded random scenarios (tests/fuzz_scenarios.py:
     any block size, open / reflective edges, sources, wind): bitwise equal
-    to the single grid."""
+    to the single grid; migrate=1 re-cuts and moves the strips mid-run."""
     seeds = _fuzz_seeds(3, 12, world)
     assert seeds
     for seed in seeds[(0 if halo == "copy" else 1):][:2]:
         env = dict(os.environ, SWF_DIST_BACKEND="gloo", SWF_CHECK_FUZZ=str(seed),
-                   SWF_CHECK_STEPS="12", SWF_HALO=halo)
+                   SWF_CHECK_STEPS="12", SWF_HALO=halo, SWF_CHECK_MIGRATE=migrate)
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                f"--nproc-per-node={world}", "--master-addr", "127.0.0.1", "--master-port",
                str(_port()), os.path.join(ROOT, "tests", "multirank_check.py")]
