@@ -188,3 +188,48 @@ def test_random_scenarios_stagewise_vs_reference(oracle_built, seed):
         both(lambda: a.final_update(sa, ta), lambda: b.final_update(sb, tb))
         assert_state_bitwise(sb, sa, f"seed {seed} step {step}")
         assert b._volumes() == a._volumes()
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_scenarios_strip_host_steps(seed):
+    """The strips' host-buffer step (swf_strip_host_phase1/2, the multi-GPU
+    e2e path) on the random scenarios: every strip reads its window from one
+    pinned global state and writes its owned cells back in place, bitwise
+    equal to the single grid."""
+    import torch
+    from paper_1705_00614_b200 import CsphTvdStepper, NumericalError
+    from paper_1705_00614_b200 import multigpu as M
+    from fuzz_scenarios import window
+    from helpers import assert_bitwise
+    sc = random_scenario(seed)
+    nx, ny, bs = sc.terrain.nx, sc.terrain.ny, sc.options.block_size
+    try:
+        bounds = M.strip_bounds(ny, 2 + seed % 2, bs)
+    except ValueError:
+        pytest.skip("grid too small for that many strips of >= 3 rows")
+    one = make(CsphTvdStepper, sc)
+    ref = sc.state.copy()
+    one.upload(ref)
+    try:
+        one.run(10)
+    except NumericalError:
+        pytest.skip("the scenario aborts (covered against the reference above)")
+    one.download(ref)
+    pin = lambda a: torch.from_numpy(np.array(a, copy=True)).pin_memory().numpy()
+    H, X, Y = pin(sc.state.H), pin(sc.state.HUx), pin(sc.state.HUy)
+    strips = []
+    for j0, j1 in bounds:
+        w0, w1 = M.window_rows(j0, j1, ny)
+        ws = window(sc, w0, w1)
+        strips.append((M.Strip(ws, ny, j0, j1, ws.global_sources, ws.wind), w0 * nx))
+    t = 0.0
+    for _ in range(10):
+        sp = [s.host_phase1(H[o:], X[o:], Y[o:], t) for s, o in strips]
+        g = max(sp)
+        ts = [s.host_phase2(H[o:], X[o:], Y[o:], g)[0] for s, o in strips]
+        assert len(set(ts)) == 1
+        t = ts[0]
+    assert t == ref.t
+    assert_bitwise(H, ref.H, f"seed {seed} H")
+    assert_bitwise(X, ref.HUx, f"seed {seed} HUx")
+    assert_bitwise(Y, ref.HUy, f"seed {seed} HUy")
