@@ -180,6 +180,7 @@ __global__ void k_tau(Geo G, const DevSrc* src, const double* ht, const double* 
                       const double* wt, const double* wv, double* sig, StepScalars* sc,
                       double dt_cap, double global_speed, const double* gspeed) {
   sc->mask_fresh = 0;  // k_flist has consumed it
+  sc->step_open = 0;
   if (stopped(sc)) return;
   unsigned long long mb = sc->speed_bits;
   for (int q = 0; q < SPEED_SLOTS; ++q) mb = sc->speed_slots[q] > mb ? sc->speed_slots[q] : mb;
@@ -205,6 +206,7 @@ __global__ void k_tau(Geo G, const DevSrc* src, const double* ht, const double* 
   if (dt_cap > 0.0) tau = smin(tau, dt_cap);
   sc->tau = tau;
   mid_scalars(G, src, ht, hq, wt, wv, sig, sc, tau);
+  sc->step_open = 1;
 }
 
 __global__ void k_mid(Geo G, const DevSrc* src, const double* ht, const double* hq,
@@ -976,7 +978,8 @@ __device__ __forceinline__ void step_tile(const Geo& G, const StepArgs& A, const
   const PhysConst& P = G.P;  // reciprocals refined at context creation (fused_prepare)
   StepScalars* sc = A.sc;
   if (threadIdx.x == 0) s_dflag = 0;
-  if (__syncthreads_or(stopped(sc))) return;
+  // (not stopped(): see StepScalars::step_open)
+  if (__syncthreads_or(!*(volatile const int*)&sc->step_open)) return;
   bool sok = true;  // every speculative division of this thread accepted
   unsigned long long my_err = ERR_NONE;  // published once the tile is known exact
   const int tid = threadIdx.x;

@@ -60,6 +60,12 @@ struct StepScalars {
                    // cleared by k_tau
   int redo_n[3];   // tiles queued for the exact redo: [0] k_forces, [1] k_step / k_flux, [2] k_lag
   int list_n[2];   // work-list lengths: [0] k_forces, [1] k_step (k_lag and k_flux share it)
+  // k_step of this step may run (set by k_tau): an error raised BY this
+  // step's k_step does not stop its other tiles or its redo tiles, so the
+  // reported cell is the first in the reference's block order, not the
+  // first found; an error from before (an earlier step, the dt floor, a
+  // stopped peer strip, an idle substep) does
+  int step_open;
   int list_take[3];  // work-list cursors of the persistent grids: [2] k_lag
 };
 

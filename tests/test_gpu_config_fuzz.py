@@ -119,3 +119,13 @@ def test_invalid_and_extreme_configs_like_the_reference(oracle_built, seed):
         assert go[1].t == ro[1].t
     else:
         assert go == ro, (what, ro, go)
+
+
+def test_abort_cell_from_a_redone_tile_wins_in_block_order(oracle_built):
+    """Seed 7974 (a NaN rain rate): at step 1 two tiles hit the h/2
+    displacement abort; the one earlier in the reference's block order had a
+    rejected speculative division and is recomputed by the exact redo launch
+    after the other had published its error.  The abort must still name the
+    first cell in block order (it named the later one while an error raised
+    by the same step stopped the redo; StepScalars::step_open)."""
+    test_invalid_and_extreme_configs_like_the_reference(oracle_built, 7974)
